@@ -1,0 +1,25 @@
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+    config.addinivalue_line("markers", "slow: long-running case")
+
+
+@pytest.fixture(scope="session")
+def golden():
+    arr = np.load(os.path.join(GOLDEN_DIR, "golden.npz"))
+    with open(os.path.join(GOLDEN_DIR, "golden.json")) as fh:
+        meta = json.load(fh)
+    return {k: arr[k] for k in arr.files}, meta
