@@ -1,0 +1,157 @@
+/*
+ * pgmres.h -- C-ABI of libpgmres.so, the B200 (sm_100a) hot path of
+ * polynomial-preconditioned restarted GMRES(m) (Loe, Thornquist & Boman,
+ * arxiv 1907.00072; reference package `polygmres` v0.1.0).
+ *
+ * Plain C types only: pointers, sizes, doubles.  No torch types cross this
+ * boundary.  Device pointers (`const double* d_*`) are caller-owned device
+ * allocations; `stream` is a cudaStream_t passed as void*.  Every call is
+ * asynchronous on `stream` unless stated; results written to device memory.
+ *
+ * Status: every function returns int, PG_OK (0) or a negative PG_ERR_* code;
+ * pg_last_error() returns the message of the calling thread's last failure.
+ * The Python host layer maps the codes onto the reference's exception types
+ * (errors.py:4-70): PG_ERR_DIMENSION -> DimensionMismatchError,
+ * PG_ERR_PARAMETER -> ParameterError, PG_ERR_CUDA/PG_ERR_ALLOC -> DeviceError.
+ *
+ * Each entry point names the reference interface it replaces (file:line under
+ * /root/reference/pkg/src/polygmres).  INTEGRATION.md shows the ctypes
+ * binding a maintainer adds to the reference to route through this library.
+ */
+#ifndef PGMRES_H
+#define PGMRES_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PG_API __attribute__((visibility("default")))
+
+#define PG_OK 0
+#define PG_ERR_DIMENSION (-1)
+#define PG_ERR_PARAMETER (-2)
+#define PG_ERR_CUDA (-3)
+#define PG_ERR_ALLOC (-4)
+
+/* SELL-C-sigma slice height (one warp of rows). */
+#define PG_SLICE 32
+/* Largest basis / power-sequence width the tall-skinny kernels accept. */
+#define PG_KMAX 64
+
+/* pg_poly_pass flags */
+#define PG_PASS_FIRST 1   /* acc = y0*x[row] + yk*(A x)[row]; acc_in unused   */
+#define PG_PASS_WRITE_W 2 /* also store w = A x (the next pass's operand)     */
+
+typedef struct pg_matrix pg_matrix;
+typedef struct pg_workspace pg_workspace;
+
+/* ---- library / errors -------------------------------------------------- */
+PG_API int pg_version(void); /* ABI version, currently 1 */
+PG_API int pg_last_error(char* buf, size_t len);
+PG_API int pg_device_count(int* count);
+/* Make `device` current for the calling thread (kernels launch on it). */
+PG_API int pg_set_device(int device);
+
+/* ---- host-side SELL-C-sigma plan (no GPU needed; used by tests) ----------
+ * Replaces the CSR layout of CsrMatrix (sparse.py:42-148) with SELL-C-sigma:
+ * rows (optionally length-sorted inside windows of `sigma` rows) are grouped
+ * in slices of 32; slice s stores entry j of its lane t at
+ * slice_ptr[s] + j*32 + t.  Entry order inside a row is the CSR order, so the
+ * device SpMV sums each row in exactly the reference's order.
+ * pg_sell_size: padded entry count and slice count for (row_ptr, sigma).
+ * pg_sell_fill: fills caller arrays: slice_ptr[n_slices+1], slice_w[n_slices],
+ * row_len[n_slices*32], perm[n_slices*32] (-1 = padding lane),
+ * col[padded], val[padded]. */
+PG_API int pg_sell_size(int64_t nrows, const int64_t* row_ptr, int sigma,
+                        int64_t* n_slices, int64_t* padded_nnz);
+PG_API int pg_sell_fill(int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                        const int64_t* col_idx, const double* values, int sigma,
+                        int64_t* slice_ptr, int32_t* slice_w, int32_t* row_len,
+                        int32_t* perm, int32_t* col, double* val);
+
+/* ---- device operator ------------------------------------------------------
+ * Replaces MatrixOperator(matrix) (gmres.py:46-60) / CsrMatrix storage.
+ * Host CSR in (int64 row_ptr[nrows+1], int64 col_idx[nnz] in
+ * [0, ncols), float64 values[nnz]); the library keeps a device SELL copy.
+ * For a row-block shard, ncols = owned rows + ghost columns (local numbering,
+ * owned columns first).  `device` is the CUDA ordinal to allocate on. */
+PG_API int pg_matrix_create(int device, int64_t nrows, int64_t ncols,
+                            const int64_t* row_ptr, const int64_t* col_idx,
+                            const double* values, int sigma, pg_matrix** out);
+PG_API int pg_matrix_destroy(pg_matrix* mat);
+/* stats[8] = {nrows, ncols, nnz, padded_nnz, n_slices, device_bytes,
+ *             max_width, sigma} */
+PG_API int pg_matrix_stats(const pg_matrix* mat, int64_t* stats);
+
+/* ---- reduction workspace (one per stream) --------------------------------
+ * Block partials + a completion counter for the deterministic fixed-order
+ * "last block reduces" pattern.  Not shareable between concurrent streams. */
+PG_API int pg_workspace_create(int device, pg_workspace** out);
+PG_API int pg_workspace_destroy(pg_workspace* ws);
+
+/* ---- SpMV and the fused polynomial pass ------------------------------------
+ * pg_spmv: y = A x.  Replaces spmv() (sparse.py:151-168), bitwise: per row
+ * a sequential sum in stored column order of separately rounded products.
+ * x has ncols entries, y nrows. */
+PG_API int pg_spmv(const pg_matrix* mat, const double* d_x, double* d_y, void* stream);
+
+/* One pass of apply_poly's running-power recurrence (polyprec.py:205-211),
+ * fused into the SpMV epilogue:
+ *   w   = A x
+ *   acc = (FIRST ? y0*x[row] : acc_in[row]) + yk*w      (mul, then add)
+ *   out = base ? base[row] + acc : acc                  (x + p(A)u, gmres.py:330)
+ *   if WRITE_W: w_out[row] = w
+ * acc_out may alias acc_in; base may alias acc_out. */
+PG_API int pg_poly_pass(const pg_matrix* mat, const double* d_x, const double* d_acc_in,
+                        const double* d_base, double* d_acc_out, double* d_w_out,
+                        double y0, double yk, int flags, void* stream);
+
+/* r = b - A x and the partial sum of r^2 into d_nsq[0] (gmres.py:334-335). */
+PG_API int pg_residual(const pg_matrix* mat, const double* d_x, const double* d_b,
+                       double* d_r, double* d_nsq, pg_workspace* ws, void* stream);
+
+/* ---- two-pass classical Gram-Schmidt (ortho.py:33-70) ----------------------
+ * V is column-major with leading dimension ld (even); columns 0..k-1 are the
+ * basis, 1 <= k <= PG_KMAX; z, w2 have n entries.  Coefficient vectors are
+ * device arrays of k doubles (sum over THIS shard's rows; a multi-GPU caller
+ * all-reduces them between phases).
+ *   phase 1: c1 = V^T z                                      (ortho.py:53)
+ *   phase 2: w1 = z - V c1 (on the fly);  c2 = V^T w1         (ortho.py:54-55)
+ *   phase 3: w2 = (z - V c1) - V c2;  nsq = sum w2^2          (ortho.py:56,59)
+ * then pg_normalize: out = w2 / sqrt(nsq)                    (ortho.py:70) */
+PG_API int pg_cgs2_phase1(const double* d_V, int64_t ld, int k, const double* d_z,
+                          int64_t n, double* d_c1, pg_workspace* ws, void* stream);
+PG_API int pg_cgs2_phase2(const double* d_V, int64_t ld, int k, const double* d_z,
+                          int64_t n, const double* d_c1, double* d_c2, pg_workspace* ws,
+                          void* stream);
+PG_API int pg_cgs2_phase3(const double* d_V, int64_t ld, int k, const double* d_z,
+                          int64_t n, const double* d_c1, const double* d_c2, double* d_w2,
+                          double* d_nsq, pg_workspace* ws, void* stream);
+PG_API int pg_normalize(const double* d_x, const double* d_nsq, int64_t n, double* d_out,
+                        void* stream);
+
+/* ---- polynomial construction / recovery helpers ---------------------------
+ * pg_gram: G = P^T P for the ncols columns of P (full symmetric ncols x ncols,
+ * row-major) -- the Gram blocks of _normal_equations (polyprec.py:115-122).
+ * pg_gemv: out = V[:, :k] y (gmres.py:326), y a device array of k doubles.
+ * pg_dot: d_out[0] = sum x*y (np.linalg.norm's squared sum, gmres.py:241).
+ * pg_scale_add: out = (base ? base + a*v : a*v) (polyprec.py:205, gmres.py:330).
+ * pg_gather: out[i] = x[idx[i]] (halo packing for row-block shards). */
+PG_API int pg_gram(const double* d_P, int64_t ld, int ncols, int64_t n, double* d_G,
+                   pg_workspace* ws, void* stream);
+PG_API int pg_gemv(const double* d_V, int64_t ld, int k, const double* d_y, int64_t n,
+                   double* d_out, void* stream);
+PG_API int pg_dot(const double* d_x, const double* d_y, int64_t n, double* d_out,
+                  pg_workspace* ws, void* stream);
+PG_API int pg_scale_add(const double* d_base, double a, const double* d_v, int64_t n,
+                        double* d_out, void* stream);
+PG_API int pg_gather(const double* d_x, const int32_t* d_idx, int64_t m, double* d_out,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PGMRES_H */

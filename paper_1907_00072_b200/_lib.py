@@ -1,0 +1,106 @@
+"""ctypes binding of libpgmres.so (include/pgmres.h).
+
+The library is loaded on first use and a missing or unloadable library is a
+hard error: there is no CPU fallback anywhere in this package.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+from . import errors
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpgmres.so")
+HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "pgmres.h")
+
+PG_OK = 0
+PG_ERR_DIMENSION = -1
+PG_ERR_PARAMETER = -2
+PG_ERR_CUDA = -3
+PG_ERR_ALLOC = -4
+PG_SLICE = 32
+PG_KMAX = 64
+PG_PASS_FIRST = 1
+PG_PASS_WRITE_W = 2
+
+_i64 = C.c_int64
+_i32 = C.c_int
+_p = C.c_void_p
+_d = C.c_double
+_pi64 = C.POINTER(C.c_int64)
+
+_SIGNATURES = {
+    "pg_version": ([], C.c_int),
+    "pg_last_error": ([C.c_char_p, C.c_size_t], C.c_int),
+    "pg_device_count": ([C.POINTER(C.c_int)], C.c_int),
+    "pg_set_device": ([_i32], C.c_int),
+    "pg_sell_size": ([_i64, _p, _i32, _pi64, _pi64], C.c_int),
+    "pg_sell_fill": ([_i64, _i64, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p], C.c_int),
+    "pg_matrix_create": ([_i32, _i64, _i64, _p, _p, _p, _i32, C.POINTER(_p)], C.c_int),
+    "pg_matrix_destroy": ([_p], C.c_int),
+    "pg_matrix_stats": ([_p, _pi64], C.c_int),
+    "pg_workspace_create": ([_i32, C.POINTER(_p)], C.c_int),
+    "pg_workspace_destroy": ([_p], C.c_int),
+    "pg_spmv": ([_p, _p, _p, _p], C.c_int),
+    "pg_poly_pass": ([_p, _p, _p, _p, _p, _p, _d, _d, _i32, _p], C.c_int),
+    "pg_residual": ([_p, _p, _p, _p, _p, _p, _p], C.c_int),
+    "pg_cgs2_phase1": ([_p, _i64, _i32, _p, _i64, _p, _p, _p], C.c_int),
+    "pg_cgs2_phase2": ([_p, _i64, _i32, _p, _i64, _p, _p, _p, _p], C.c_int),
+    "pg_cgs2_phase3": ([_p, _i64, _i32, _p, _i64, _p, _p, _p, _p, _p, _p], C.c_int),
+    "pg_normalize": ([_p, _p, _i64, _p, _p], C.c_int),
+    "pg_gram": ([_p, _i64, _i32, _i64, _p, _p, _p], C.c_int),
+    "pg_gemv": ([_p, _i64, _i32, _p, _i64, _p, _p], C.c_int),
+    "pg_dot": ([_p, _p, _i64, _p, _p, _p], C.c_int),
+    "pg_scale_add": ([_p, _d, _p, _i64, _p, _p], C.c_int),
+    "pg_gather": ([_p, _p, _i64, _p, _p], C.c_int),
+}
+
+_lib = None
+
+
+def header_symbols(path: str = HEADER_PATH):
+    """Names of every PG_API entry point declared in include/pgmres.h."""
+    text = open(path).read()
+    return sorted(set(re.findall(r"PG_API\s+[\w\s\*]+?\b(pg_\w+)\s*\(", text)))
+
+
+def load():
+    """Load (once) and return the library; raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise errors.DeviceError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (the device path has no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (args, res) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    buf = C.create_string_buffer(1024)
+    load().pg_last_error(buf, len(buf))
+    return buf.value.decode(errors="replace")
+
+
+def check(code: int, what: str = ""):
+    if code == PG_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if code == PG_ERR_DIMENSION:
+        raise errors.DimensionMismatchError(msg)
+    if code == PG_ERR_PARAMETER:
+        raise errors.ParameterError(msg)
+    raise errors.DeviceError(msg)
+
+
+def call(name: str, *args):
+    check(getattr(load(), name)(*args), name)

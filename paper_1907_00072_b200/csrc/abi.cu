@@ -1,0 +1,287 @@
+// libpgmres: library plumbing -- errors, SELL-C-sigma construction, device
+// operator and workspace lifetime.
+//
+// The SELL build replaces the reference's CSR storage (sparse.py:42-148) with
+// a warp-sliced layout; the entry order inside each row is preserved so the
+// device SpMV reproduces spmv()'s per-row sequential sum (sparse.py:164-168).
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace pg {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+int grid_for(int device, const void* kernel, int block, size_t smem, int64_t work_blocks) {
+  int sms = 0, per_sm = 0;
+  PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem));
+  if (per_sm < 1) per_sm = 1;
+  int64_t g = (int64_t)sms * per_sm;
+  if (g > kMaxBlocks) g = kMaxBlocks;
+  if (work_blocks < g) g = work_blocks;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// ---------------------------------------------------------------------------
+// host SELL-C-sigma plan
+// ---------------------------------------------------------------------------
+static void validate_csr(int64_t nrows, const int64_t* row_ptr) {
+  PG_REQUIRE(nrows >= 0, PG_ERR_PARAMETER, "nrows must be non-negative");
+  PG_REQUIRE(nrows < (int64_t(1) << 31) - 64, PG_ERR_PARAMETER, "nrows exceeds int32 range");
+  PG_REQUIRE(row_ptr != nullptr, PG_ERR_PARAMETER, "row_ptr is null");
+  PG_REQUIRE(row_ptr[0] == 0, PG_ERR_PARAMETER, "row_ptr[0] must be 0");
+  for (int64_t r = 0; r < nrows; ++r)
+    PG_REQUIRE(row_ptr[r + 1] >= row_ptr[r], PG_ERR_PARAMETER, "row_ptr must be non-decreasing");
+}
+
+// Lane order: rows sorted by decreasing length inside windows of sigma rows
+// (stable, so sigma <= 1 is the identity).
+static std::vector<int32_t> lane_order(int64_t nrows, const int64_t* row_ptr, int sigma) {
+  std::vector<int32_t> order(nrows);
+  std::iota(order.begin(), order.end(), 0);
+  if (sigma > 1) {
+    for (int64_t w0 = 0; w0 < nrows; w0 += sigma) {
+      int64_t w1 = std::min<int64_t>(nrows, w0 + sigma);
+      std::stable_sort(order.begin() + w0, order.begin() + w1, [&](int32_t a, int32_t b) {
+        return (row_ptr[a + 1] - row_ptr[a]) > (row_ptr[b + 1] - row_ptr[b]);
+      });
+    }
+  }
+  return order;
+}
+
+struct SellHost {
+  int64_t n_slices = 0, padded = 0;
+  int max_width = 0;
+  std::vector<int64_t> slice_ptr;
+  std::vector<int32_t> slice_w, row_len, perm;
+};
+
+static SellHost sell_plan(int64_t nrows, const int64_t* row_ptr, int sigma) {
+  validate_csr(nrows, row_ptr);
+  SellHost h;
+  h.n_slices = (nrows + PG_SLICE - 1) / PG_SLICE;
+  std::vector<int32_t> order = lane_order(nrows, row_ptr, sigma);
+  h.slice_ptr.assign(h.n_slices + 1, 0);
+  h.slice_w.assign(h.n_slices, 0);
+  h.row_len.assign(h.n_slices * PG_SLICE, 0);
+  h.perm.assign(h.n_slices * PG_SLICE, -1);
+  for (int64_t s = 0; s < h.n_slices; ++s) {
+    int32_t w = 0;
+    for (int t = 0; t < PG_SLICE; ++t) {
+      int64_t lane = s * PG_SLICE + t;
+      if (lane >= nrows) break;
+      int32_t r = order[lane];
+      int64_t len = row_ptr[r + 1] - row_ptr[r];
+      PG_REQUIRE(len < (int64_t(1) << 30), PG_ERR_PARAMETER, "row too long");
+      h.perm[lane] = r;
+      h.row_len[lane] = (int32_t)len;
+      w = std::max<int32_t>(w, (int32_t)len);
+    }
+    h.slice_w[s] = w;
+    h.max_width = std::max(h.max_width, (int)w);
+    h.slice_ptr[s + 1] = h.slice_ptr[s] + (int64_t)w * PG_SLICE;
+  }
+  h.padded = h.slice_ptr[h.n_slices];
+  return h;
+}
+
+static void sell_fill(const SellHost& h, int64_t ncols, const int64_t* row_ptr,
+                      const int64_t* col_idx, const double* values, int32_t* col, double* val) {
+  PG_REQUIRE(ncols >= 0 && ncols < (int64_t(1) << 31), PG_ERR_PARAMETER,
+             "ncols exceeds int32 range");
+  std::memset(col, 0, sizeof(int32_t) * h.padded);
+  std::memset(val, 0, sizeof(double) * h.padded);
+  for (int64_t s = 0; s < h.n_slices; ++s) {
+    int64_t base = h.slice_ptr[s];
+    for (int t = 0; t < PG_SLICE; ++t) {
+      int64_t lane = s * PG_SLICE + t;
+      int32_t r = h.perm[lane];
+      if (r < 0) continue;
+      int64_t q0 = row_ptr[r], len = h.row_len[lane];
+      for (int64_t j = 0; j < len; ++j) {
+        int64_t c = col_idx[q0 + j];
+        PG_REQUIRE(c >= 0 && c < ncols, PG_ERR_PARAMETER, "column indices out of range");
+        col[base + j * PG_SLICE + t] = (int32_t)c;
+        val[base + j * PG_SLICE + t] = values[q0 + j];
+      }
+    }
+  }
+}
+
+template <class T>
+static T* upload(const T* host, size_t count, size_t& bytes) {
+  T* d = nullptr;
+  size_t nb = sizeof(T) * std::max<size_t>(count, 1);
+  cudaError_t e = cudaMalloc(&d, nb);
+  if (e != cudaSuccess) throw Error(PG_ERR_ALLOC, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  if (count) PG_CUDA(cudaMemcpy(d, host, sizeof(T) * count, cudaMemcpyHostToDevice));
+  bytes += nb;
+  return d;
+}
+
+static void free_matrix(pg_matrix* m) {
+  if (!m) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(m->device);
+  cudaFree(m->slice_ptr);
+  cudaFree(m->slice_w);
+  cudaFree(m->row_len);
+  cudaFree(m->perm);
+  cudaFree(m->col);
+  cudaFree(m->val);
+  cudaSetDevice(cur);
+  delete m;
+}
+
+struct DeviceScope {
+  int prev = 0;
+  explicit DeviceScope(int dev) {
+    PG_CUDA(cudaGetDevice(&prev));
+    PG_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceScope() { cudaSetDevice(prev); }
+};
+
+}  // namespace pg
+
+using namespace pg;
+
+extern "C" {
+
+PG_API int pg_version(void) { return 1; }
+
+PG_API int pg_last_error(char* buf, size_t len) {
+  if (!buf || !len) return PG_ERR_PARAMETER;
+  std::strncpy(buf, g_last_error.c_str(), len - 1);
+  buf[len - 1] = '\0';
+  return PG_OK;
+}
+
+PG_API int pg_device_count(int* count) {
+  return guard([&] {
+    PG_REQUIRE(count, PG_ERR_PARAMETER, "count is null");
+    PG_CUDA(cudaGetDeviceCount(count));
+  });
+}
+
+PG_API int pg_set_device(int device) {
+  return guard([&] { PG_CUDA(cudaSetDevice(device)); });
+}
+
+PG_API int pg_sell_size(int64_t nrows, const int64_t* row_ptr, int sigma, int64_t* n_slices,
+                        int64_t* padded_nnz) {
+  return guard([&] {
+    SellHost h = sell_plan(nrows, row_ptr, sigma);
+    if (n_slices) *n_slices = h.n_slices;
+    if (padded_nnz) *padded_nnz = h.padded;
+  });
+}
+
+PG_API int pg_sell_fill(int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                        const int64_t* col_idx, const double* values, int sigma,
+                        int64_t* slice_ptr, int32_t* slice_w, int32_t* row_len, int32_t* perm,
+                        int32_t* col, double* val) {
+  return guard([&] {
+    SellHost h = sell_plan(nrows, row_ptr, sigma);
+    std::copy(h.slice_ptr.begin(), h.slice_ptr.end(), slice_ptr);
+    std::copy(h.slice_w.begin(), h.slice_w.end(), slice_w);
+    std::copy(h.row_len.begin(), h.row_len.end(), row_len);
+    std::copy(h.perm.begin(), h.perm.end(), perm);
+    sell_fill(h, ncols, row_ptr, col_idx, values, col, val);
+  });
+}
+
+PG_API int pg_matrix_create(int device, int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                            const int64_t* col_idx, const double* values, int sigma,
+                            pg_matrix** out) {
+  return guard([&] {
+    PG_REQUIRE(out, PG_ERR_PARAMETER, "out is null");
+    *out = nullptr;
+    SellHost h = sell_plan(nrows, row_ptr, sigma);
+    std::vector<int32_t> col(std::max<int64_t>(h.padded, 1));
+    std::vector<double> val(std::max<int64_t>(h.padded, 1));
+    sell_fill(h, ncols, row_ptr, col_idx, values, col.data(), val.data());
+    DeviceScope scope(device);
+    pg_matrix* m = new pg_matrix();
+    std::memset(m, 0, sizeof(*m));
+    m->device = device;
+    m->nrows = nrows;
+    m->ncols = ncols;
+    m->nnz = row_ptr[nrows];
+    m->padded_nnz = h.padded;
+    m->n_slices = h.n_slices;
+    m->sigma = sigma;
+    m->max_width = h.max_width;
+    try {
+      m->slice_ptr = upload(h.slice_ptr.data(), h.slice_ptr.size(), m->bytes);
+      m->slice_w = upload(h.slice_w.data(), h.slice_w.size(), m->bytes);
+      m->row_len = upload(h.row_len.data(), h.row_len.size(), m->bytes);
+      if (sigma > 1) m->perm = upload(h.perm.data(), h.perm.size(), m->bytes);
+      m->col = upload(col.data(), (size_t)h.padded, m->bytes);
+      m->val = upload(val.data(), (size_t)h.padded, m->bytes);
+    } catch (...) {
+      free_matrix(m);
+      throw;
+    }
+    *out = m;
+  });
+}
+
+PG_API int pg_matrix_destroy(pg_matrix* mat) {
+  return guard([&] { free_matrix(mat); });
+}
+
+PG_API int pg_matrix_stats(const pg_matrix* m, int64_t* s) {
+  return guard([&] {
+    PG_REQUIRE(m && s, PG_ERR_PARAMETER, "null argument");
+    s[0] = m->nrows;
+    s[1] = m->ncols;
+    s[2] = m->nnz;
+    s[3] = m->padded_nnz;
+    s[4] = m->n_slices;
+    s[5] = (int64_t)m->bytes;
+    s[6] = m->max_width;
+    s[7] = m->sigma;
+  });
+}
+
+PG_API int pg_workspace_create(int device, pg_workspace** out) {
+  return guard([&] {
+    PG_REQUIRE(out, PG_ERR_PARAMETER, "out is null");
+    DeviceScope scope(device);
+    pg_workspace* w = new pg_workspace();
+    w->device = device;
+    PG_CUDA(cudaDeviceGetAttribute(&w->num_sms, cudaDevAttrMultiProcessorCount, device));
+    size_t nb = sizeof(double) * (size_t)kMaxBlocks * kMaxOut;
+    if (cudaMalloc(&w->partials, nb) != cudaSuccess ||
+        cudaMalloc(&w->counter, 64) != cudaSuccess) {
+      cudaFree(w->partials);
+      delete w;
+      throw Error(PG_ERR_ALLOC, "workspace allocation failed");
+    }
+    PG_CUDA(cudaMemset(w->counter, 0, 64));
+    *out = w;
+  });
+}
+
+PG_API int pg_workspace_destroy(pg_workspace* ws) {
+  return guard([&] {
+    if (!ws) return;
+    DeviceScope scope(ws->device);
+    cudaFree(ws->partials);
+    cudaFree(ws->counter);
+    delete ws;
+  });
+}
+
+}  // extern "C"

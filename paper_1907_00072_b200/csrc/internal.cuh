@@ -1,0 +1,132 @@
+// Internal declarations shared by the libpgmres translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "pgmres.h"
+
+namespace pg {
+
+// ---------------------------------------------------------------- errors --
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+#define PG_CUDA(expr)                                                              \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      throw ::pg::Error(PG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define PG_REQUIRE(cond, code, msg) \
+  do {                              \
+    if (!(cond)) throw ::pg::Error((code), (msg)); \
+  } while (0)
+
+// Wrap an ABI body: exceptions -> status codes + last-error text.
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return PG_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return PG_ERR_ALLOC;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return PG_ERR_CUDA;
+  }
+}
+
+inline void check_launch() { PG_CUDA(cudaGetLastError()); }
+
+// ------------------------------------------------------------ structures --
+}  // namespace pg
+
+struct pg_matrix {
+  int device;
+  int64_t nrows, ncols, nnz, padded_nnz, n_slices;
+  int sigma, max_width;
+  int64_t* slice_ptr;  // [n_slices+1] entry offset of each slice
+  int32_t* slice_w;    // [n_slices]   slice width (max row length)
+  int32_t* row_len;    // [n_slices*32] true length of the lane's row
+  int32_t* perm;       // [n_slices*32] local row of lane (nullptr if sigma<=1)
+  int32_t* col;        // [padded]  SELL column indices (int32)
+  double* val;         // [padded]  SELL values
+  size_t bytes;
+};
+
+namespace pg {
+// Number of per-block partial slots a reduction may use.
+constexpr int kMaxBlocks = 1024;
+// Gram upper bound: ncols <= PG_KMAX -> ncols^2 outputs.
+constexpr int kMaxOut = PG_KMAX * PG_KMAX;
+}  // namespace pg
+
+struct pg_workspace {
+  int device;
+  int num_sms;
+  double* partials;        // [kMaxBlocks * kMaxOut]
+  unsigned int* counter;   // completion counter (self-resetting)
+};
+
+namespace pg {
+// Deterministic fixed-order finish: every block has written `nout` partials
+// at partials[blk*nout + i]; the last block to arrive sums them in block
+// order into out[i] and resets the counter.  Call from all threads.
+__device__ inline void last_block_reduce(double* partials, unsigned int* counter, int nout,
+                                         double* out) {
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int prev = atomicAdd(counter, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < nout; i += blockDim.x) {
+    double s = 0.0;
+    for (unsigned int b = 0; b < gridDim.x; ++b) {
+      s += __ldcg(partials + (size_t)b * nout + i);
+    }
+    out[i] = s;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// Deterministic block-wide sum of one double per thread (blockDim multiple of
+// 32, <= 1024).  Result valid in thread 0.
+__device__ inline double block_sum(double v) {
+  __shared__ double warp_part[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) warp_part[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    int nw = blockDim.x >> 5;
+    for (int i = 0; i < nw; ++i) s += warp_part[i];
+  }
+  return s;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int grid_for(int device, const void* kernel, int block, size_t smem, int64_t work_blocks);
+
+}  // namespace pg

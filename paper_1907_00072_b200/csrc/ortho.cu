@@ -1,0 +1,471 @@
+// libpgmres: tall-skinny kernels -- CGS2 phases (ortho.py:33-70), the
+// power-basis Gram matrix (polyprec.py:115-122), the recovery GEMV
+// (gmres.py:326) and the small vector kernels.
+//
+// All of these are HBM-bound (<= 0.25 flop/B), so no tensor cores: the point
+// is to read each basis column the minimum number of times.  The reference
+// makes 4 passes over V per CGS2 step (two dgemv_T, two dgemv_N); here:
+//   phase 1  c1 = V^T z                         1 read of V
+//   phase 2  w1 = z - V c1 (row-local), c2 = V^T w1   1 read of V (tile in smem)
+//   phase 3  w2 = (z - V c1) - V c2, |w2|^2     1 read of V (w1 recomputed)
+// Reductions are deterministic: fixed per-lane / per-warp / per-block order,
+// then the last block to finish sums the block partials in block order.
+//
+// Tile kernels stage a 128-row x (k[+1]) column tile in shared memory with
+// 16-byte cp.async copies, double buffered, so the next tile's HBM reads are
+// in flight while the current tile is reduced.
+
+#include "internal.cuh"
+
+namespace pg {
+
+constexpr int kTileRows = 128;
+constexpr int kTileStride = kTileRows + 2;  // 16-B aligned column stride (doubles)
+constexpr int kTileThreads = 256;
+constexpr int kWarps = kTileThreads / 32;
+constexpr int kColsPerWarp = (PG_KMAX + kWarps - 1) / kWarps;               // 8
+constexpr int kPairsPerThread = (PG_KMAX * (PG_KMAX + 1) / 2 + kTileThreads - 1) / kTileThreads;  // 9
+
+enum TileMode { kDots = 1, kUpdDots = 2, kGram = 3 };
+
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, int bytes) {
+  unsigned saddr = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(src),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Stage tile `tile` of columns 0..ncol-1 (column k = z when z != nullptr).
+__device__ __forceinline__ void stage_tile(double* buf, const double* __restrict__ V, int64_t ld,
+                                           int k, const double* __restrict__ z, int64_t n,
+                                           int64_t tile) {
+  const int ncol = z ? k + 1 : k;
+  const int64_t row0 = tile * kTileRows;
+  const int64_t rows = min((int64_t)kTileRows, n - row0);
+  constexpr int kChunks = kTileRows / 2;
+  for (int c = threadIdx.x; c < ncol * kChunks; c += kTileThreads) {
+    const int colx = c / kChunks, ch = c - colx * kChunks;
+    const double* src = (colx < k ? V + (int64_t)colx * ld : z) + row0 + 2 * ch;
+    const int64_t valid = rows - 2 * ch;
+    int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
+    if (bytes == 0) src = V ? V : z;  // not dereferenced; keep the address legal
+    cp_async16(buf + colx * kTileStride + 2 * ch, src, bytes);
+  }
+}
+
+// Row projection t = sum_i V[r,i] c[i], sequential in i with FMA.  Phase 2
+// (from the smem tile) and phase 3 (from global) use this same order, so the
+// recomputed w1 is bit-identical.
+template <class Load>
+__device__ __forceinline__ double row_proj(int k, const double* c, Load load) {
+  double t = 0.0;
+  for (int i = 0; i < k; ++i) t = __fma_rn(load(i), c[i], t);
+  return t;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTileThreads)
+    tile_kernel(const double* __restrict__ V, int64_t ld, int k, const double* __restrict__ z,
+                int64_t n, const double* __restrict__ c1, double* partials,
+                unsigned int* counter, double* out) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double c1s[PG_KMAX];
+  const bool has_z = (MODE != kGram);
+  const int ncol = has_z ? k + 1 : k;
+  double* const buf0 = smem;
+  double* const buf1 = smem + ncol * kTileStride;
+  double* w1s = smem + 2 * ncol * kTileStride;  // kUpdDots only
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  if (MODE == kUpdDots)
+    for (int i = threadIdx.x; i < k; i += kTileThreads) c1s[i] = c1[i];
+
+  const int64_t ntiles = (n + kTileRows - 1) / kTileRows;
+  int64_t tile = blockIdx.x;
+
+  // per-thread accumulators
+  constexpr int NACC = (MODE == kGram) ? kPairsPerThread : kColsPerWarp;
+  double acc[NACC];
+#pragma unroll
+  for (int m = 0; m < NACC; ++m) acc[m] = 0.0;
+  int pi[kPairsPerThread], pj[kPairsPerThread];
+  const int npairs = k * (k + 1) / 2;
+  if (MODE == kGram) {
+#pragma unroll
+    for (int m = 0; m < kPairsPerThread; ++m) {
+      int p = threadIdx.x + m * kTileThreads, i = 0;
+      if (p < npairs) {
+        int rem = p;
+        while (rem >= k - i) { rem -= k - i; ++i; }
+        pi[m] = i;
+        pj[m] = i + rem;
+      } else {
+        pi[m] = pj[m] = -1;
+      }
+    }
+  }
+
+  int it = 0;
+  if (tile < ntiles) stage_tile(buf0, V, ld, k, has_z ? z : nullptr, n, tile);
+  cp_async_commit();
+  for (; tile < ntiles; tile += gridDim.x, ++it) {
+    const int64_t next = tile + gridDim.x;
+    if (next < ntiles) stage_tile((it & 1) ? buf0 : buf1, V, ld, k, has_z ? z : nullptr, n, next);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* S = (it & 1) ? buf1 : buf0;
+
+    if (MODE == kDots || MODE == kUpdDots) {
+      const double* vec = S + k * kTileStride;  // z column
+      if (MODE == kUpdDots) {
+        if (threadIdx.x < kTileRows) {
+          const int r = threadIdx.x;
+          const double t = row_proj(k, c1s, [&](int i) { return S[i * kTileStride + r]; });
+          w1s[r] = __dsub_rn(S[k * kTileStride + r], t);
+        }
+        __syncthreads();
+        vec = w1s;
+      }
+#pragma unroll
+      for (int m = 0; m < kColsPerWarp; ++m) {
+        const int i = warp + m * kWarps;
+        if (i < k) {
+          const double* col = S + i * kTileStride;
+#pragma unroll
+          for (int q = 0; q < kTileRows / 32; ++q)
+            acc[m] = __fma_rn(col[lane + 32 * q], vec[lane + 32 * q], acc[m]);
+        }
+      }
+    } else {  // Gram: all pairs i <= j
+#pragma unroll
+      for (int m = 0; m < kPairsPerThread; ++m) {
+        if (pi[m] >= 0) {
+          const double* a = S + pi[m] * kTileStride;
+          const double* b = S + pj[m] * kTileStride;
+          double s = acc[m];
+#pragma unroll 8
+          for (int r = 0; r < kTileRows; ++r) s = __fma_rn(a[r], b[r], s);
+          acc[m] = s;
+        }
+      }
+    }
+    __syncthreads();  // buffer (it&1) is restaged next iteration
+  }
+  cp_async_wait<0>();
+
+  // block partials, then deterministic cross-block finish
+  if (MODE == kGram) {
+    double* part = partials + (size_t)blockIdx.x * (k * k);
+#pragma unroll
+    for (int m = 0; m < kPairsPerThread; ++m) {
+      if (pi[m] >= 0) {
+        part[pi[m] * k + pj[m]] = acc[m];
+        part[pj[m] * k + pi[m]] = acc[m];
+      }
+    }
+    last_block_reduce(partials, counter, k * k, out);
+  } else {
+#pragma unroll
+    for (int m = 0; m < kColsPerWarp; ++m) {
+      double v = acc[m];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      const int i = warp + m * kWarps;
+      if (lane == 0 && i < k) partials[(size_t)blockIdx.x * k + i] = v;
+    }
+    last_block_reduce(partials, counter, k, out);
+  }
+}
+
+// Phase 3 / GEMV: one thread per row, streaming the k columns from HBM.
+//   PHASE3: w2 = (z - V c1) - V c2 -> out, sum w2^2 -> nsq
+//   GEMV:   out = V y
+constexpr int kRowThreads = 256;
+
+template <bool PHASE3>
+__global__ void __launch_bounds__(kRowThreads)
+    rows_kernel(const double* __restrict__ V, int64_t ld, int k, const double* __restrict__ z,
+                int64_t n, const double* __restrict__ c1, const double* __restrict__ c2,
+                double* __restrict__ out, double* partials, unsigned int* counter, double* nsq) {
+  __shared__ double cs1[PG_KMAX], cs2[PG_KMAX];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    cs1[i] = c1[i];
+    if (PHASE3) cs2[i] = c2[i];
+  }
+  __syncthreads();
+  double local = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+    const double* vr = V + r;
+    if (PHASE3) {
+      double t1 = 0.0, t2 = 0.0;
+      int i = 0;
+      for (; i + 8 <= k; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(vr + (int64_t)(i + u) * ld);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          t1 = __fma_rn(v[u], cs1[i + u], t1);
+          t2 = __fma_rn(v[u], cs2[i + u], t2);
+        }
+      }
+      for (; i < k; ++i) {
+        const double v = __ldcs(vr + (int64_t)i * ld);
+        t1 = __fma_rn(v, cs1[i], t1);
+        t2 = __fma_rn(v, cs2[i], t2);
+      }
+      const double w1 = __dsub_rn(z[r], t1);
+      const double w2 = __dsub_rn(w1, t2);
+      out[r] = w2;
+      local = __fma_rn(w2, w2, local);
+    } else {
+      double t = 0.0;
+      int i = 0;
+      for (; i + 8 <= k; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(vr + (int64_t)(i + u) * ld);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t = __fma_rn(v[u], cs1[i + u], t);
+      }
+      for (; i < k; ++i) t = __fma_rn(__ldcs(vr + (int64_t)i * ld), cs1[i], t);
+      out[r] = t;
+    }
+  }
+  if (PHASE3) {
+    const double s = block_sum(local);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    last_block_reduce(partials, counter, 1, nsq);
+  }
+}
+
+__global__ void dot_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                           double* partials, unsigned int* counter, double* out) {
+  double local = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    local = __fma_rn(x[i], y[i], local);
+  const double s = block_sum(local);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  last_block_reduce(partials, counter, 1, out);
+}
+
+__global__ void normalize_kernel(const double* __restrict__ x, const double* __restrict__ nsq,
+                                 int64_t n, double* __restrict__ out) {
+  const double nrm = sqrt(*nsq);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = __ddiv_rn(x[i], nrm);
+}
+
+__global__ void scale_add_kernel(const double* base, double a, const double* v, int64_t n,
+                                 double* out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double t = __dmul_rn(a, v[i]);
+    out[i] = base ? __dadd_rn(base[i], t) : t;
+  }
+}
+
+__global__ void gather_kernel(const double* __restrict__ x, const int32_t* __restrict__ idx,
+                              int64_t m, double* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride)
+    out[i] = x[idx[i]];
+}
+
+// ------------------------------------------------------------------ host --
+static int current_device() {
+  int d = 0;
+  PG_CUDA(cudaGetDevice(&d));
+  return d;
+}
+
+static void check_ws(pg_workspace* ws) {
+  PG_REQUIRE(ws, PG_ERR_PARAMETER, "workspace is null");
+  PG_REQUIRE(ws->device == current_device(), PG_ERR_PARAMETER,
+             "workspace belongs to another device");
+}
+
+static void check_tall(const double* V, int64_t ld, int k, int64_t n, int kmin) {
+  PG_REQUIRE(n >= 0, PG_ERR_DIMENSION, "n must be non-negative");
+  PG_REQUIRE(k >= kmin && k <= PG_KMAX, PG_ERR_DIMENSION, "basis width out of range");
+  PG_REQUIRE(k == 0 || (V && ld >= n), PG_ERR_DIMENSION, "leading dimension smaller than n");
+}
+
+static size_t tile_smem_max() {
+  return sizeof(double) * ((size_t)2 * (PG_KMAX + 1) * kTileStride + kTileRows);
+}
+
+static size_t tile_smem(int mode, int k) {
+  const int ncol = (mode == kGram) ? k : k + 1;
+  size_t b = sizeof(double) * (size_t)2 * ncol * kTileStride;
+  if (mode == kUpdDots) b += sizeof(double) * kTileRows;
+  return b;
+}
+
+template <int MODE>
+static void launch_tile(const double* V, int64_t ld, int k, const double* z, int64_t n,
+                        const double* c1, double* out, pg_workspace* ws, cudaStream_t st) {
+  check_ws(ws);
+  PG_REQUIRE(ld % 2 == 0, PG_ERR_PARAMETER, "leading dimension must be even");
+  PG_REQUIRE(((uintptr_t)V & 15) == 0 && (!z || ((uintptr_t)z & 15) == 0), PG_ERR_PARAMETER,
+             "tile operands must be 16-byte aligned");
+  const size_t smem = tile_smem(MODE, k);
+  const int dev = ws->device;
+  PG_REQUIRE(dev >= 0 && dev < 64, PG_ERR_PARAMETER, "device ordinal out of range");
+  static bool attr_set[4][64] = {};
+  static int grid_cache[4][PG_KMAX + 1][64] = {};
+  if (!attr_set[MODE][dev]) {
+    PG_CUDA(cudaFuncSetAttribute(tile_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tile_smem_max()));
+    attr_set[MODE][dev] = true;
+  }
+  const int64_t ntiles = (n + kTileRows - 1) / kTileRows;
+  if (ntiles == 0) {
+    PG_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * (MODE == kGram ? k * k : k), st));
+    return;
+  }
+  int g = grid_cache[MODE][k][dev];
+  if (g == 0) {
+    g = grid_for(dev, (const void*)tile_kernel<MODE>, kTileThreads, smem, int64_t(1) << 40);
+    grid_cache[MODE][k][dev] = g;
+  }
+  if (ntiles < g) g = (int)ntiles;
+  tile_kernel<MODE><<<g, kTileThreads, smem, st>>>(V, ld, k, z, n, c1, ws->partials,
+                                                   ws->counter, out);
+  check_launch();
+}
+
+static int simple_grid(int64_t n, int threads, pg_workspace* ws) {
+  int sms = ws ? ws->num_sms : 148;
+  int64_t need = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)sms * (2048 / threads);
+  if (cap > kMaxBlocks) cap = kMaxBlocks;
+  int64_t g = need < cap ? need : cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace pg
+
+using namespace pg;
+
+extern "C" {
+
+PG_API int pg_cgs2_phase1(const double* d_V, int64_t ld, int k, const double* d_z, int64_t n,
+                          double* d_c1, pg_workspace* ws, void* stream) {
+  return guard([&] {
+    check_tall(d_V, ld, k, n, 1);
+    PG_REQUIRE(d_z && d_c1, PG_ERR_PARAMETER, "null argument");
+    launch_tile<kDots>(d_V, ld, k, d_z, n, nullptr, d_c1, ws, as_stream(stream));
+  });
+}
+
+PG_API int pg_cgs2_phase2(const double* d_V, int64_t ld, int k, const double* d_z, int64_t n,
+                          const double* d_c1, double* d_c2, pg_workspace* ws, void* stream) {
+  return guard([&] {
+    check_tall(d_V, ld, k, n, 1);
+    PG_REQUIRE(d_z && d_c1 && d_c2, PG_ERR_PARAMETER, "null argument");
+    launch_tile<kUpdDots>(d_V, ld, k, d_z, n, d_c1, d_c2, ws, as_stream(stream));
+  });
+}
+
+PG_API int pg_cgs2_phase3(const double* d_V, int64_t ld, int k, const double* d_z, int64_t n,
+                          const double* d_c1, const double* d_c2, double* d_w2, double* d_nsq,
+                          pg_workspace* ws, void* stream) {
+  return guard([&] {
+    check_tall(d_V, ld, k, n, 0);
+    check_ws(ws);
+    PG_REQUIRE(d_z && d_w2 && d_nsq && (k == 0 || (d_c1 && d_c2)), PG_ERR_PARAMETER,
+               "null argument");
+    cudaStream_t st = as_stream(stream);
+    if (n == 0) {
+      PG_CUDA(cudaMemsetAsync(d_nsq, 0, sizeof(double), st));
+      return;
+    }
+    const int g = simple_grid(n, kRowThreads, ws);
+    rows_kernel<true><<<g, kRowThreads, 0, st>>>(d_V, ld, k, d_z, n, d_c1, d_c2, d_w2,
+                                                  ws->partials, ws->counter, d_nsq);
+    check_launch();
+  });
+}
+
+PG_API int pg_normalize(const double* d_x, const double* d_nsq, int64_t n, double* d_out,
+                        void* stream) {
+  return guard([&] {
+    PG_REQUIRE(d_x && d_nsq && d_out, PG_ERR_PARAMETER, "null argument");
+    if (n == 0) return;
+    const int g = simple_grid(n, 256, nullptr);
+    normalize_kernel<<<g, 256, 0, as_stream(stream)>>>(d_x, d_nsq, n, d_out);
+    check_launch();
+  });
+}
+
+PG_API int pg_gram(const double* d_P, int64_t ld, int ncols, int64_t n, double* d_G,
+                   pg_workspace* ws, void* stream) {
+  return guard([&] {
+    check_tall(d_P, ld, ncols, n, 1);
+    PG_REQUIRE(d_G, PG_ERR_PARAMETER, "null argument");
+    launch_tile<kGram>(d_P, ld, ncols, nullptr, n, nullptr, d_G, ws, as_stream(stream));
+  });
+}
+
+PG_API int pg_gemv(const double* d_V, int64_t ld, int k, const double* d_y, int64_t n,
+                   double* d_out, void* stream) {
+  return guard([&] {
+    check_tall(d_V, ld, k, n, 0);
+    PG_REQUIRE(d_out && (k == 0 || d_y), PG_ERR_PARAMETER, "null argument");
+    if (n == 0) return;
+    const int g = simple_grid(n, kRowThreads, nullptr);
+    rows_kernel<false><<<g, kRowThreads, 0, as_stream(stream)>>>(
+        d_V, ld, k, nullptr, n, d_y, nullptr, d_out, nullptr, nullptr, nullptr);
+    check_launch();
+  });
+}
+
+PG_API int pg_dot(const double* d_x, const double* d_y, int64_t n, double* d_out,
+                  pg_workspace* ws, void* stream) {
+  return guard([&] {
+    check_ws(ws);
+    PG_REQUIRE(d_x && d_y && d_out, PG_ERR_PARAMETER, "null argument");
+    cudaStream_t st = as_stream(stream);
+    if (n == 0) {
+      PG_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double), st));
+      return;
+    }
+    const int g = simple_grid(n, 256, ws);
+    dot_kernel<<<g, 256, 0, st>>>(d_x, d_y, n, ws->partials, ws->counter, d_out);
+    check_launch();
+  });
+}
+
+PG_API int pg_scale_add(const double* d_base, double a, const double* d_v, int64_t n,
+                        double* d_out, void* stream) {
+  return guard([&] {
+    PG_REQUIRE(d_v && d_out, PG_ERR_PARAMETER, "null argument");
+    if (n == 0) return;
+    const int g = simple_grid(n, 256, nullptr);
+    scale_add_kernel<<<g, 256, 0, as_stream(stream)>>>(d_base, a, d_v, n, d_out);
+    check_launch();
+  });
+}
+
+PG_API int pg_gather(const double* d_x, const int32_t* d_idx, int64_t m, double* d_out,
+                     void* stream) {
+  return guard([&] {
+    if (m == 0) return;
+    PG_REQUIRE(d_x && d_idx && d_out, PG_ERR_PARAMETER, "null argument");
+    const int g = simple_grid(m, 256, nullptr);
+    gather_kernel<<<g, 256, 0, as_stream(stream)>>>(d_x, d_idx, m, d_out);
+    check_launch();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,524 @@
+"""Device runtime: row-block shards, halo plans, communicators and the vector
+engine the solver drives.
+
+A *shard* is one contiguous block of rows ``[r0, r1)`` living on one GPU: its
+slice of A as a SELL-C-sigma ``pg_matrix`` (columns renumbered: owned columns
+first, then the ghost columns it reads from other shards, grouped by owner),
+a reduction workspace and its device.  A distributed vector is a Python list
+holding one float64 tensor per local shard, of length ``n_ext`` (owned rows +
+ghost slots).  The solver is written once over that list:
+
+* ``SoloComm``   -- every shard of the job lives in this process (1 shard on 1
+  GPU for the default path; or P *virtual* shards on one GPU, which exercises
+  the partition / halo / reduction logic with the real kernels on one device);
+* ``DistComm``   -- one shard per process, ``torch.distributed`` (NCCL on GPUs):
+  halo = batched point-to-point send/recv of boundary entries before each SpMV,
+  and one all-reduce per batched-dot phase.
+
+No reference CPU arithmetic lives here; every flop on the path is a libpgmres
+kernel.  PyTorch provides device memory, streams and the collectives.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DeviceError, DimensionMismatchError, ParameterError
+
+F64 = torch.float64
+KMAX = _lib.PG_KMAX
+ROW_ALIGN = 64  # leading-dimension alignment of basis blocks (rows)
+
+
+def _pad(n: int) -> int:
+    return max(ROW_ALIGN, (n + ROW_ALIGN - 1) // ROW_ALIGN * ROW_ALIGN)
+
+
+def ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the PP-GMRES device path has no CPU fallback")
+
+
+# ---------------------------------------------------------------------------
+# partition and halo plan
+# ---------------------------------------------------------------------------
+def balanced_offsets(row_ptr: np.ndarray, parts: int, align: int = 1) -> np.ndarray:
+    """Row offsets of ``parts`` contiguous blocks with ~equal nnz, boundaries
+    rounded to multiples of ``align`` rows (e.g. a grid plane)."""
+    n = len(row_ptr) - 1
+    if parts < 1:
+        raise ParameterError("parts must be >= 1")
+    nnz = int(row_ptr[-1])
+    offs = [0]
+    for p in range(1, parts):
+        target = nnz * p / parts
+        r = int(np.searchsorted(row_ptr, target, side="left"))
+        r = int(round(r / align) * align) if align > 1 else r
+        offs.append(min(max(r, offs[-1]), n))
+    offs.append(n)
+    return np.array(offs, dtype=np.int64)
+
+
+@dataclass
+class HaloPlan:
+    """Ghost layout of one shard.  ``recv[q] = (offset, count)``: the ghost slots
+    ``[offset, offset+count)`` of the local vector are filled from shard q (ghost
+    columns sorted by global index, so each owner's ghosts are contiguous).
+    ``send[q]``: local row indices this shard sends to shard q."""
+
+    ghosts: np.ndarray
+    recv: dict = field(default_factory=dict)
+    send: dict = field(default_factory=dict)
+
+
+def ghost_columns(cols: np.ndarray, r0: int, r1: int) -> np.ndarray:
+    outside = cols[(cols < r0) | (cols >= r1)]
+    return np.unique(outside)
+
+
+def plan_recv(ghosts: np.ndarray, offsets: np.ndarray, n_local: int) -> dict:
+    owners = np.searchsorted(offsets, ghosts, side="right") - 1
+    recv = {}
+    for q in np.unique(owners):
+        idx = np.nonzero(owners == q)[0]
+        recv[int(q)] = (n_local + int(idx[0]), int(len(idx)))
+    return recv
+
+
+def localize_columns(cols: np.ndarray, r0: int, r1: int, ghosts: np.ndarray) -> np.ndarray:
+    """Global -> local column numbering; entry order (hence the per-row sum
+    order of the SpMV) is untouched."""
+    inside = (cols >= r0) & (cols < r1)
+    return np.where(inside, cols - r0, (r1 - r0) + np.searchsorted(ghosts, cols)).astype(np.int64)
+
+
+def choose_sigma(row_ptr: np.ndarray) -> int:
+    """SELL sorting window: 1 (no reordering) unless slice padding with natural
+    row order exceeds 15% of nnz (irregular rows, e.g. config 3)."""
+    lens = np.diff(row_ptr)
+    n = len(lens)
+    if n == 0:
+        return 1
+    pad = (-n) % 32
+    L = np.concatenate([lens, np.zeros(pad, lens.dtype)]).reshape(-1, 32)
+    padded = int(L.max(axis=1).sum()) * 32
+    return 1 if padded <= 1.15 * max(1, int(row_ptr[-1])) else 4096
+
+
+# ---------------------------------------------------------------------------
+# one shard
+# ---------------------------------------------------------------------------
+class Shard:
+    def __init__(self, index: int, device: torch.device, r0: int, r1: int,
+                 row_ptr: np.ndarray, cols_global: np.ndarray, values: np.ndarray,
+                 offsets: np.ndarray, sigma: int | None = None):
+        lib = _lib.load()
+        self.index = index
+        self.device = device
+        self.dev_ord = device.index if device.index is not None else torch.cuda.current_device()
+        self.r0, self.r1 = int(r0), int(r1)
+        self.n = self.r1 - self.r0
+        ghosts = ghost_columns(cols_global, self.r0, self.r1)
+        self.plan = HaloPlan(ghosts, plan_recv(ghosts, offsets, self.n))
+        self.n_ext = self.n + len(ghosts)
+        self.ld = _pad(self.n_ext)
+        cols_local = localize_columns(cols_global, self.r0, self.r1, ghosts)
+        self.sigma = choose_sigma(row_ptr) if sigma is None else int(sigma)
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        cl = np.ascontiguousarray(cols_local, dtype=np.int64)
+        vl = np.ascontiguousarray(values, dtype=np.float64)
+        h = _lib.C.c_void_p()
+        _lib.call("pg_matrix_create", self.dev_ord, self.n, self.n_ext, rp.ctypes.data,
+                  cl.ctypes.data, vl.ctypes.data, self.sigma, _lib.C.byref(h))
+        self.mat = h
+        w = _lib.C.c_void_p()
+        _lib.call("pg_workspace_create", self.dev_ord, _lib.C.byref(w))
+        self.ws = w
+        self.nnz = int(row_ptr[-1])
+        st = (_lib.C.c_int64 * 8)()
+        _lib.call("pg_matrix_stats", self.mat, st)
+        self.stats = dict(zip(("nrows", "ncols", "nnz", "padded_nnz", "n_slices",
+                               "device_bytes", "max_width", "sigma"), list(st)))
+        # small per-shard device scratch: [c1 | c2 | nsq | spare]
+        self.scal = torch.zeros(2 * KMAX + 8, dtype=F64, device=device)
+        self.coef = torch.zeros(KMAX, dtype=F64, device=device)
+        self.send_idx: dict = {}
+        self.send_buf: dict = {}
+        self._lib = lib
+
+    # send lists (local indices) are installed once every shard's ghost needs are known
+    def set_send(self, q: int, local_idx: np.ndarray):
+        local_idx = np.ascontiguousarray(local_idx, dtype=np.int32)
+        self.plan.send[q] = local_idx
+        contiguous = len(local_idx) > 0 and np.all(np.diff(local_idx) == 1)
+        if contiguous:
+            self.send_idx[q] = (int(local_idx[0]), int(len(local_idx)))
+        else:
+            self.send_idx[q] = torch.from_numpy(local_idx).to(self.device)
+            self.send_buf[q] = torch.empty(len(local_idx), dtype=F64, device=self.device)
+
+    @property
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def activate(self):
+        _lib.call("pg_set_device", self.dev_ord)
+
+    def vec(self) -> torch.Tensor:
+        return torch.zeros(self.n_ext, dtype=F64, device=self.device)
+
+    def block(self, cols: int) -> torch.Tensor:
+        """Column-major n x cols block: row-major (cols, ld) tensor."""
+        return torch.zeros((cols, self.ld), dtype=F64, device=self.device)
+
+    def packed_send(self, x: torch.Tensor, q: int) -> torch.Tensor:
+        sel = self.send_idx[q]
+        if isinstance(sel, tuple):
+            a, c = sel
+            return x[a:a + c]
+        buf = self.send_buf[q]
+        _lib.call("pg_gather", ptr(x), ptr(sel), len(sel), ptr(buf), self.stream)
+        return buf
+
+    def close(self):
+        if getattr(self, "mat", None):
+            _lib.load().pg_matrix_destroy(self.mat)
+            self.mat = None
+        if getattr(self, "ws", None):
+            _lib.load().pg_workspace_destroy(self.ws)
+            self.ws = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# communicators
+# ---------------------------------------------------------------------------
+class SoloComm:
+    """All shards of the job are in this process (1 GPU, or P virtual shards).
+    Halo = device copies; all-reduce = fixed-order sum over shards."""
+
+    distributed = False
+    world = 1
+
+    def __init__(self, shards):
+        self.shards = shards
+
+    def halo(self, xs):
+        if len(self.shards) == 1:
+            return
+        for p, s in enumerate(self.shards):
+            for q, (off, cnt) in s.plan.recv.items():
+                src = self.shards[q].packed_send(xs[q], p)
+                xs[p][off:off + cnt].copy_(src, non_blocking=True)
+
+    def allreduce(self, bufs):
+        if len(bufs) == 1:
+            return
+        total = bufs[0].clone()
+        for b in bufs[1:]:
+            total += b.to(total.device)
+        for b in bufs:
+            b.copy_(total)
+
+
+class DistComm:
+    """One shard per process; torch.distributed (NCCL for CUDA tensors, gloo
+    for the CPU host-logic tests).  Halo: one batched send/recv round of
+    boundary entries per SpMV.  Dots: one all-reduce per batched phase."""
+
+    distributed = True
+
+    def __init__(self, shards, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.shards = shards
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def halo(self, xs):
+        dist = self.dist
+        s = self.shards[0]
+        x = xs[0]
+        ops = []
+        for q in sorted(s.plan.send):
+            ops.append(dist.P2POp(dist.isend, s.packed_send(x, q), q, self.group))
+        for q, (off, cnt) in sorted(s.plan.recv.items()):
+            ops.append(dist.P2POp(dist.irecv, x[off:off + cnt], q, self.group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+
+    def allreduce(self, bufs):
+        self.dist.all_reduce(bufs[0], group=self.group)
+
+
+def exchange_send_lists(shards, comm):
+    """Turn every shard's ghost needs into the owners' send lists (the
+    Epetra-Import construction).  In-process: direct; distributed: one
+    all_gather_object of the per-rank needs at setup time."""
+    if isinstance(comm, SoloComm):
+        for p, s in enumerate(shards):
+            for q, (off, cnt) in s.plan.recv.items():
+                need = s.plan.ghosts[off - s.n: off - s.n + cnt]
+                shards[q].set_send(p, need - shards[q].r0)
+        return
+    s = shards[0]
+    needs = {q: s.plan.ghosts[off - s.n: off - s.n + cnt] for q, (off, cnt) in s.plan.recv.items()}
+    gathered = [None] * comm.world
+    comm.dist.all_gather_object(gathered, needs, group=comm.group)
+    for p, nd in enumerate(gathered):
+        if p != comm.rank and comm.rank in nd:
+            s.set_send(p, np.asarray(nd[comm.rank]) - s.r0)
+
+
+# ---------------------------------------------------------------------------
+# the engine: every vector op of the solver, over the shard list
+# ---------------------------------------------------------------------------
+class Engine:
+    def __init__(self, shards, comm, n_global: int):
+        self.shards = shards
+        self.comm = comm
+        self.N = int(n_global)
+        self.P = len(shards)
+
+    # ---- construction -------------------------------------------------------
+    @classmethod
+    def build(cls, matrix, device=None, parts: int = 1, sigma=None, offsets=None):
+        """All shards in this process.  ``matrix``: whole square CSR (reference
+        CsrMatrix or CsrHost); ``parts`` > 1 splits it into virtual shards."""
+        require_cuda()
+        n = int(matrix.nrows)
+        row_ptr = np.asarray(matrix.row_ptr, dtype=np.int64)
+        cols = np.asarray(matrix.col_idx, dtype=np.int64)
+        vals = np.asarray(matrix.values, dtype=np.float64)
+        devs = device if isinstance(device, (list, tuple)) else [device] * parts
+        devs = [torch.device("cuda", torch.cuda.current_device()) if d is None else torch.device(d)
+                for d in devs]
+        offs = balanced_offsets(row_ptr, parts) if offsets is None else np.asarray(offsets)
+        shards = []
+        for p in range(parts):
+            a, b = int(offs[p]), int(offs[p + 1])
+            q0, q1 = int(row_ptr[a]), int(row_ptr[b])
+            shards.append(Shard(p, devs[p], a, b, row_ptr[a:b + 1] - q0, cols[q0:q1],
+                                vals[q0:q1], offs, sigma))
+        comm = SoloComm(shards)
+        exchange_send_lists(shards, comm)
+        return cls(shards, comm, n)
+
+    @classmethod
+    def build_distributed(cls, block, offsets, device, group=None, sigma=None):
+        """One shard per process: ``block`` is this rank's row block (global
+        column indices, ``block.row_offset == offsets[rank]``)."""
+        require_cuda()
+        import torch.distributed as dist
+        rank = dist.get_rank(group)
+        offs = np.asarray(offsets, dtype=np.int64)
+        if int(block.row_offset) != int(offs[rank]) or int(block.nrows) != int(offs[rank + 1] - offs[rank]):
+            raise DimensionMismatchError("row block does not match the partition offsets")
+        s = Shard(rank, torch.device(device), int(offs[rank]), int(offs[rank + 1]),
+                  np.asarray(block.row_ptr), np.asarray(block.col_idx),
+                  np.asarray(block.values), offs, sigma)
+        comm = DistComm([s], group)
+        exchange_send_lists([s], comm)
+        return cls([s], comm, int(offs[-1]))
+
+    def close(self):
+        for s in self.shards:
+            s.close()
+
+    # ---- vectors --------------------------------------------------------------
+    def vecs(self):
+        return [s.vec() for s in self.shards]
+
+    def blocks(self, cols):
+        return [s.block(cols) for s in self.shards]
+
+    @property
+    def local_n(self) -> int:
+        return sum(s.n for s in self.shards)
+
+    def from_host(self, v, pinned=False):
+        """Global (or, distributed, rank-local) host vector -> shard vectors."""
+        v = np.asarray(v, dtype=np.float64)
+        out = self.vecs()
+        if self.comm.distributed and v.shape == (self.local_n,):
+            parts = [v]
+        elif v.shape == (self.N,):
+            parts = [v[s.r0:s.r1] for s in self.shards]
+        else:
+            raise DimensionMismatchError("vector length does not match operator")
+        for s, t, part in zip(self.shards, out, parts):
+            src = torch.from_numpy(np.ascontiguousarray(part))
+            if pinned:
+                src = src.pin_memory()
+            t[:s.n].copy_(src, non_blocking=pinned)
+        return out
+
+    def from_torch(self, v: torch.Tensor):
+        if v.dtype != F64:
+            v = v.to(F64)
+        if v.dim() != 1:
+            raise DimensionMismatchError("vector must be 1-d")
+        out = self.vecs()
+        if self.comm.distributed and v.shape[0] == self.local_n:
+            for s, t in zip(self.shards, out):
+                t[:s.n].copy_(v)
+            return out
+        if v.shape[0] != self.N:
+            raise DimensionMismatchError("vector length does not match operator")
+        for s, t in zip(self.shards, out):
+            t[:s.n].copy_(v[s.r0:s.r1])
+        return out
+
+    def to_host(self, xs) -> np.ndarray:
+        return np.concatenate([t[:s.n].cpu().numpy() for s, t in zip(self.shards, xs)])
+
+    def to_torch(self, xs) -> torch.Tensor:
+        if len(xs) == 1:
+            return xs[0][:self.shards[0].n].clone()
+        d = self.shards[0].device
+        return torch.cat([t[:s.n].to(d) for s, t in zip(self.shards, xs)])
+
+    def ingest(self, v):
+        if isinstance(v, torch.Tensor):
+            return self.from_torch(v)
+        return self.from_host(v)
+
+    def emit(self, xs, like):
+        if isinstance(like, torch.Tensor):
+            return self.to_torch(xs)
+        return self.to_host(xs)
+
+    # ---- kernels ----------------------------------------------------------------
+    def _each(self):
+        for s in self.shards:
+            if self.P > 1:
+                s.activate()
+            yield s
+
+    def halo(self, xs):
+        self.comm.halo(xs)
+
+    def spmv(self, xs, ys):
+        self.halo(xs)
+        for s, x, y in zip(self._each(), xs, ys):
+            _lib.call("pg_spmv", s.mat, ptr(x), ptr(y), s.stream)
+
+    def poly(self, y, vs, out, acc, w0, w1, base=None):
+        """out = (base +) p(A) v with p = sum_k y_k A^k (polyprec.py:193-212);
+        d = len(y)-1 fused SpMV passes.  acc, w0, w1: scratch shard vectors."""
+        y = [float(c) for c in y]
+        d = len(y) - 1
+        if d == 0:
+            for s, v, o, b in zip(self._each(), vs, out, base or [None] * self.P):
+                _lib.call("pg_scale_add", ptr(b) if b is not None else None, y[0], ptr(v), s.n,
+                          ptr(o), s.stream)
+            return
+        self.halo(vs)
+        cur = vs
+        ws = (w0, w1)
+        for k in range(1, d + 1):
+            last = k == d
+            flags = (_lib.PG_PASS_FIRST if k == 1 else 0) | (0 if last else _lib.PG_PASS_WRITE_W)
+            nxt = ws[k & 1]
+            dst = out if last else acc
+            for i, s in enumerate(self._each()):
+                b = base[i] if (last and base is not None) else None
+                _lib.call("pg_poly_pass", s.mat, ptr(cur[i]), ptr(acc[i]) if k > 1 else None,
+                          ptr(b) if b is not None else None, ptr(dst[i]),
+                          ptr(nxt[i]) if not last else None, y[0], y[k], flags, s.stream)
+            if not last:
+                self.halo(nxt)
+                cur = nxt
+
+    def slot(self, i):
+        """Per-shard 1-element device scalar slot i (0..7) after the coefficients."""
+        return [s.scal[2 * KMAX + i:2 * KMAX + i + 1] for s in self.shards]
+
+    def residual(self, xs, bs, rs, slot=4) -> float:
+        """r = b - A x; returns the global sum of r^2 (host float), also left
+        in device scalar slot ``slot``."""
+        self.halo(xs)
+        nsq = self.slot(slot)
+        for s, x, b, r, q in zip(self._each(), xs, bs, rs, nsq):
+            _lib.call("pg_residual", s.mat, ptr(x), ptr(b), ptr(r), ptr(q), s.ws, s.stream)
+        self.comm.allreduce(nsq)
+        return float(nsq[0].item())
+
+    def dot(self, xs, ys, slot=5) -> float:
+        outs = self.slot(slot)
+        for s, x, y, o in zip(self._each(), xs, ys, outs):
+            _lib.call("pg_dot", ptr(x), ptr(y), s.n, ptr(o), s.ws, s.stream)
+        self.comm.allreduce(outs)
+        return float(outs[0].item())
+
+    def normalize_dev(self, xs, nsq_slices, outs, n_rows=None):
+        for s, x, q, o in zip(self._each(), xs, nsq_slices, outs):
+            _lib.call("pg_normalize", ptr(x), ptr(q), s.n if n_rows is None else n_rows, ptr(o),
+                      s.stream)
+
+    def scale(self, xs, a, outs):
+        for s, x, o in zip(self._each(), xs, outs):
+            _lib.call("pg_scale_add", None, float(a), ptr(x), s.n, ptr(o), s.stream)
+
+    def add(self, base, vs, outs):
+        """out = base + v (x + update, gmres.py:330)."""
+        for s, b, v, o in zip(self._each(), base, vs, outs):
+            _lib.call("pg_scale_add", ptr(b), 1.0, ptr(v), s.n, ptr(o), s.stream)
+
+    def cgs2(self, Vs, k, zs):
+        """Two-pass CGS of z against columns 0..k-1 of V; writes w2/|w2| into
+        column k.  Returns host (c1, c2, nsq) after the three batched
+        all-reduces (one per phase)."""
+        c1 = [s.scal[0:KMAX] for s in self.shards]
+        c2 = [s.scal[KMAX:2 * KMAX] for s in self.shards]
+        nsq = [s.scal[2 * KMAX:2 * KMAX + 1] for s in self.shards]
+        if k > 0:
+            for s, V, z, c in zip(self._each(), Vs, zs, c1):
+                _lib.call("pg_cgs2_phase1", ptr(V), s.ld, k, ptr(z), s.n, ptr(c), s.ws, s.stream)
+            self.comm.allreduce([c[:k] for c in c1])
+            for s, V, z, a, c in zip(self._each(), Vs, zs, c1, c2):
+                _lib.call("pg_cgs2_phase2", ptr(V), s.ld, k, ptr(z), s.n, ptr(a), ptr(c), s.ws,
+                          s.stream)
+            self.comm.allreduce([c[:k] for c in c2])
+        for s, V, z, a, c, q in zip(self._each(), Vs, zs, c1, c2, nsq):
+            col = V[k]
+            _lib.call("pg_cgs2_phase3", ptr(V), s.ld, k, ptr(z), s.n, ptr(a), ptr(c), ptr(col),
+                      ptr(q), s.ws, s.stream)
+        self.comm.allreduce(nsq)
+        # normalisation of column k is launched before the host looks at the
+        # scalars; on breakdown the column is simply never used (ortho.py:67-70)
+        self.normalize_dev([V[k] for V in Vs], nsq, [V[k] for V in Vs])
+        host = self.shards[0].scal[:2 * KMAX + 1].cpu().numpy()
+        return host[:k].copy(), host[KMAX:KMAX + k].copy(), float(host[2 * KMAX])
+
+    def gemv(self, Vs, k, y_host, outs):
+        yt = torch.from_numpy(np.ascontiguousarray(y_host, dtype=np.float64))
+        for s, V, o in zip(self._each(), Vs, outs):
+            s.coef[:k].copy_(yt)
+            _lib.call("pg_gemv", ptr(V), s.ld, k, ptr(s.coef), s.n, ptr(o), s.stream)
+
+    def gram(self, Ps, ncols) -> np.ndarray:
+        outs = [torch.zeros(ncols * ncols, dtype=F64, device=s.device) for s in self.shards]
+        for s, P, o in zip(self._each(), Ps, outs):
+            _lib.call("pg_gram", ptr(P), s.ld, ncols, s.n, ptr(o), s.ws, s.stream)
+        self.comm.allreduce(outs)
+        return outs[0].cpu().numpy().reshape(ncols, ncols)
+
+    def copy(self, src, dst):
+        for s, a, b in zip(self.shards, src, dst):
+            b[:s.n].copy_(a[:s.n])

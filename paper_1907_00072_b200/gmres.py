@@ -1,0 +1,293 @@
+"""Restarted GMRES(m), right-preconditioned by the minimum-residual polynomial,
+with the Krylov basis resident on the GPU (gmres.py:98-372 of the reference).
+
+Per inner iteration the device does the whole vector work -- d fused
+polynomial passes + the wrapper SpMV (``A p(A) v_j``), and the three CGS2
+phases writing the normalized v_{j+1} into the basis -- and the host receives
+2k+1 reduced scalars for the Givens update and the ``implicit < tol`` branch
+(gmres.py:290-313), the only host/device round trip of the iteration.  At a
+cycle end: host back-substitution, device GEMV ``V y``, fused polynomial
+recovery with ``x +=`` in the last pass's epilogue, and the residual SpMV with
+its norm.  Control flow, history rows, counters and exceptions follow the
+reference line for line.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .counters import CostCounters
+from .device import KMAX
+from .errors import (
+    DimensionMismatchError,
+    NumericalBreakdownError,
+    ParameterError,
+    SingularHessenbergError,
+)
+from .ortho import breakdown_test
+from .polyprec import PolyCoefficients, apply_poly
+
+
+class PolynomialWrappedOperator:
+    """``v -> op(p(op) v)``: degree+1 SpMVs per call (gmres.py:98-113)."""
+
+    kind = "polynomial-wrapped"
+
+    def __init__(self, inner, poly: PolyCoefficients):
+        self.inner = inner
+        self.poly = poly
+        self.dimension = inner.dimension
+        self.counters = inner.counters
+
+    def apply(self, v):
+        return self.inner.apply(apply_poly(self.poly, self.inner, v, self.counters))
+
+
+@dataclass(frozen=True)
+class GmresConfig:
+    restart_m: int = 50
+    tol: float = 1e-8
+    max_iters: int = 200000
+    record_history: bool = True
+
+    def __post_init__(self):
+        if self.restart_m < 1:
+            raise ParameterError("restart_m must be at least 1")
+        if not (0.0 < self.tol < 1.0):
+            raise ParameterError("tol must lie in (0, 1)")
+        if self.max_iters < 1:
+            raise ParameterError("max_iters must be at least 1")
+
+
+@dataclass
+class GmresResult:
+    x: object
+    converged: bool
+    iterations: int
+    final_relres: float
+    history: list = field(default_factory=list)
+    counters: CostCounters = field(default_factory=CostCounters)
+    cycles: int = 0
+
+
+def _givens(a, b):
+    r = math.hypot(a, b)
+    if r == 0.0:
+        return 1.0, 0.0, 0.0
+    return a / r, b / r, r
+
+
+def hessenberg_lsq(H, beta: float):
+    """Host Givens least squares of a (j+1) x j Hessenberg matrix
+    (gmres.py:172-206); kept for API parity, not on the device path."""
+    H = np.array(H, dtype=np.float64)
+    if H.ndim != 2 or H.shape[0] != H.shape[1] + 1:
+        raise DimensionMismatchError("H must have shape (j+1, j)")
+    j = H.shape[1]
+    cs, sn, g = np.zeros(j), np.zeros(j), np.zeros(j + 1)
+    g[0] = beta
+    for col in range(j):
+        for i in range(col):
+            t = cs[i] * H[i, col] + sn[i] * H[i + 1, col]
+            H[i + 1, col] = -sn[i] * H[i, col] + cs[i] * H[i + 1, col]
+            H[i, col] = t
+        c, s, r = _givens(H[col, col], H[col + 1, col])
+        cs[col], sn[col] = c, s
+        H[col, col], H[col + 1, col] = r, 0.0
+        g[col + 1] = -s * g[col]
+        g[col] = c * g[col]
+    y = np.zeros(j)
+    for i in range(j - 1, -1, -1):
+        if H[i, i] == 0.0:
+            raise SingularHessenbergError(f"zero rotated diagonal at column {i}")
+        y[i] = (g[i] - H[i, i + 1:j] @ y[i + 1:]) / H[i, i]
+    return y, abs(g[j])
+
+
+def _engine(op):
+    eng = getattr(op, "engine", None)
+    if eng is None:
+        raise ParameterError("the device solver needs a DeviceMatrixOperator "
+                             "(there is no CPU fallback)")
+    return eng
+
+
+class _Workspace:
+    """Device buffers of one solve (allocated once, reused across cycles)."""
+
+    def __init__(self, e, m):
+        self.V = e.blocks(m + 1)
+        self.z = e.vecs()       # A p(A) v_j
+        self.t = e.vecs()       # p(A) v_j / recovery update
+        self.acc = e.vecs()
+        self.w0 = e.vecs()
+        self.w1 = e.vecs()
+        self.r = e.vecs()
+
+    def col(self, j):
+        return [V[j] for V in self.V]
+
+
+def solve(op, b, x0=None, right_prec: PolyCoefficients | None = None,
+          config: GmresConfig | None = None) -> GmresResult:
+    """Restarted GMRES over the device operator (gmres.py:213-343).
+    ``b`` (and ``x0``) may be numpy arrays or torch tensors; ``x`` comes back in
+    the type of ``b``."""
+    if config is None:
+        config = GmresConfig()
+    e = _engine(op)
+    counters = op.counters
+    n = op.dimension
+    if isinstance(b, torch.Tensor):
+        blen = b.shape
+    else:
+        b = np.asarray(b, dtype=np.float64)
+        blen = b.shape
+    if blen != (n,) and not (e.comm.distributed and blen == (e.local_n,)):
+        raise DimensionMismatchError("right-hand side length does not match")
+    m = config.restart_m
+    if m + 1 > KMAX:
+        raise ParameterError(f"restart_m must be at most {KMAX - 1} on the device path")
+    tol = config.tol
+
+    bs = e.ingest(b)
+    norm_b = math.sqrt(e.dot(bs, bs, slot=4))
+    counters.scalar_dots += 1
+    if norm_b == 0.0:
+        return GmresResult(e.emit(e.vecs(), b), True, 0, 0.0, [], counters, 0)
+
+    W = _Workspace(e, m)
+    xs = e.vecs()
+    if x0 is None:
+        e.copy(bs, W.r)
+        beta = norm_b
+        beta_nsq_dev = None
+    else:
+        xs = e.ingest(x0)
+        if any(bool(torch.any(x[:s.n] != 0.0)) for s, x in zip(e.shards, xs)):
+            counters.spmvs += 1
+            beta = math.sqrt(e.residual(xs, bs, W.r, slot=4))
+        else:
+            e.copy(bs, W.r)
+            beta = math.sqrt(e.dot(bs, bs, slot=4))
+        counters.scalar_dots += 1
+
+    poly = right_prec if right_prec else None  # reference truthiness (gmres.py:261)
+    d = poly.degree if poly is not None else 0
+
+    history: list = []
+    total_iters = 0
+    cycles = 0
+    true_relres = beta / norm_b
+    converged = true_relres < tol
+    Hrot = np.empty((m + 1, m))
+    cs = np.empty(m)
+    sn = np.empty(m)
+    g = np.empty(m + 1)
+
+    while not converged and total_iters < config.max_iters:
+        # V[:, 0] = r / beta: beta = sqrt(nsq) with nsq still in device slot 4
+        e.normalize_dev(W.r, e.slot(4), W.col(0))
+        g[0] = beta
+        j = 0
+        breakdown = False
+        pending_row = None
+        while j < m and total_iters < config.max_iters:
+            vj = W.col(j)
+            if poly is not None:
+                counters.spmvs += d
+                counters.vector_updates += d + 1
+                e.poly(poly.y, vj, W.t, W.acc, W.w0, W.w1)
+                counters.spmvs += 1
+                e.spmv(W.t, W.z)
+            else:
+                counters.spmvs += 1
+                e.spmv(vj, W.z)
+            c1, c2, nsq = e.cgs2(W.V, j + 1, W.z)
+            coeffs = c1 + c2
+            new_norm = math.sqrt(nsq) if nsq >= 0.0 else float("nan")
+            counters.dots += 3
+            counters.scalar_dots += 2 * (j + 1) + 1
+            counters.vector_updates += 2 * (j + 1)
+            if not (math.isfinite(new_norm) and np.all(np.isfinite(coeffs))):
+                raise NumericalBreakdownError(total_iters + 1)
+            step_breakdown = breakdown_test(coeffs, new_norm)
+            if not step_breakdown:
+                counters.vector_updates += 1
+
+            hcol = np.empty(j + 2)
+            hcol[:j + 1] = coeffs
+            hcol[j + 1] = new_norm
+            for i in range(j):
+                t = cs[i] * hcol[i] + sn[i] * hcol[i + 1]
+                hcol[i + 1] = -sn[i] * hcol[i] + cs[i] * hcol[i + 1]
+                hcol[i] = t
+            c, s_, rot = _givens(hcol[j], hcol[j + 1])
+            cs[j], sn[j] = c, s_
+            hcol[j] = rot
+            Hrot[:j + 1, j] = hcol[:j + 1]
+            g[j + 1] = -s_ * g[j]
+            g[j] = c * g[j]
+
+            total_iters += 1
+            j += 1
+            implicit = abs(g[j]) / norm_b
+            pending_row = (total_iters, implicit)
+            if step_breakdown:
+                breakdown = True
+                break
+            # v_{j} already normalized in place on the device by Engine.cgs2
+            if implicit < tol:
+                break
+            if j < m and total_iters < config.max_iters and config.record_history:
+                history.append((total_iters, implicit) + counters.snapshot()[:3])
+                pending_row = None
+
+        # cycle end (gmres.py:318-341)
+        y = np.empty(j)
+        for i in range(j - 1, -1, -1):
+            if Hrot[i, i] == 0.0:
+                raise SingularHessenbergError(f"zero rotated diagonal at column {i}")
+            y[i] = (g[i] - Hrot[i, i + 1:j] @ y[i + 1:]) / Hrot[i, i]
+        e.gemv(W.V, j, y, W.t)
+        counters.vector_updates += j
+        if poly is not None:
+            counters.spmvs += d
+            counters.vector_updates += d + 1
+            e.poly(poly.y, W.t, xs, W.acc, W.w0, W.w1, base=xs)  # x = x + p(A)(V y)
+        else:
+            e.add(xs, W.t, xs)
+        counters.vector_updates += 1
+        cycles += 1
+
+        counters.spmvs += 1
+        beta = math.sqrt(e.residual(xs, bs, W.r, slot=4))
+        counters.scalar_dots += 1
+        true_relres = beta / norm_b
+        if config.record_history and pending_row is not None:
+            history.append(pending_row + counters.snapshot()[:3])
+        if breakdown or true_relres < tol:
+            converged = True
+
+    return GmresResult(e.emit(xs, b), converged, total_iters, true_relres, history, counters,
+                       cycles)
+
+
+def cost_report(counters: CostCounters, deg: int, restart_m: int) -> dict:
+    """Communication-proxy summary (gmres.py:350-372)."""
+    dots, spmvs = counters.dots, counters.spmvs
+    return {
+        "global_sync_proxy_dots": dots,
+        "neighbor_exchange_proxy_spmvs": spmvs,
+        "scalar_dots": counters.scalar_dots,
+        "vector_updates": counters.vector_updates,
+        "prec_applies": counters.prec_applies,
+        "spmvs_per_global_sync": (spmvs / dots) if dots else 0.0,
+        "spmvs_per_iteration": deg + 1,
+        "dots_per_iteration": 3,
+        "ca_grouping_spmvs_per_sync": deg * restart_m,
+    }

@@ -1,0 +1,201 @@
+"""GMRES minimum-residual polynomial on the device (polyprec.py:24-226 of the
+reference).
+
+Construction (``build_poly`` / ``auto_degree``): the power sequence
+``[v, Av, ..., A^{d+1} v]`` is built on the GPU with d+1 exact-order SpMVs
+(bit-identical to the reference's), its Gram matrix with one tall-skinny
+kernel plus one all-reduce; the (d+1)x(d+1) Cholesky stays on the host with the
+reference's relative pivot floor (polyprec.py:60-93).
+
+Application (``apply_poly``): the running-power recurrence fused into the
+SpMV passes (``Engine.poly``): d passes, each streaming A once and updating
+the accumulator in its epilogue, bit-identical to the reference.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .counters import CostCounters
+from .device import KMAX
+from .errors import CholeskyFailure, DimensionMismatchError, ParameterError
+
+DEFAULT_DEGREE_CAP = 20
+
+
+@dataclass(frozen=True)
+class PolyCoefficients:
+    """``p(A) = y[0] + y[1] A + ... + y[d] A^d`` (polyprec.py:24-43)."""
+
+    degree: int
+    y: np.ndarray
+    seed_norm: float
+    seed_mode: str = "unspecified"
+
+    def __post_init__(self):
+        object.__setattr__(self, "y", np.asarray(self.y, dtype=np.float64))
+        if self.y.shape != (self.degree + 1,):
+            raise ParameterError("coefficient vector must have length degree + 1")
+        if not np.all(np.isfinite(self.y)):
+            raise ParameterError("polynomial coefficients must be finite")
+
+
+@dataclass(frozen=True)
+class GramSystem:
+    G: np.ndarray
+    rhs: np.ndarray
+
+
+def dense_cholesky(system: GramSystem) -> np.ndarray:
+    """Host Cholesky solve of the Gram system.  Fails (``CholeskyFailure``,
+    1-based pivot) when ``pivot <= order*eps*G[k,k]`` -- the floor of the
+    reference code (polyprec.py:80-82), not SPEC.md:329's."""
+    G = np.asarray(system.G, dtype=np.float64)
+    rhs = np.asarray(system.rhs, dtype=np.float64)
+    m = G.shape[0]
+    if G.shape != (m, m) or rhs.shape != (m,):
+        raise DimensionMismatchError("Gram system shapes are inconsistent")
+    eps = np.finfo(np.float64).eps
+    L = np.zeros((m, m))
+    for k in range(m):
+        pivot = G[k, k] - L[k, :k] @ L[k, :k]
+        if pivot <= m * eps * G[k, k]:
+            raise CholeskyFailure(k + 1)
+        L[k, k] = np.sqrt(pivot)
+        if k + 1 < m:
+            L[k + 1:, k] = (G[k + 1:, k] - L[k + 1:, :k] @ L[k, :k]) / L[k, k]
+    z = np.zeros(m)
+    for k in range(m):
+        z[k] = (rhs[k] - L[k, :k] @ z[:k]) / L[k, k]
+    y = np.zeros(m)
+    for k in range(m - 1, -1, -1):
+        y[k] = (z[k] - L[k + 1:, k] @ y[k + 1:]) / L[k, k]
+    return y
+
+
+def _engine(op):
+    eng = getattr(op, "engine", None)
+    if eng is None:
+        raise ParameterError("the device path needs a DeviceMatrixOperator")
+    return eng
+
+
+def _device_power_gram(op, v0, top: int, counters: CostCounters):
+    """Unit seed, then the ``top``+1 power columns on the device and their
+    full Gram matrix on the host.  Returns (Gram (top+1)^2, seed_norm)."""
+    e = _engine(op)
+    if isinstance(v0, torch.Tensor):
+        if v0.shape != (op.dimension,) and not (e.comm.distributed and v0.shape == (e.local_n,)):
+            raise DimensionMismatchError("seed vector length does not match operator")
+    else:
+        v0 = np.asarray(v0, dtype=np.float64)
+        if v0.shape != (op.dimension,) and not (e.comm.distributed and v0.shape == (e.local_n,)):
+            raise DimensionMismatchError("seed vector length does not match operator")
+    if top + 1 > KMAX:
+        raise ParameterError(f"power sequence of {top + 1} columns exceeds the kernel limit {KMAX}")
+    vs = e.ingest(v0)
+    nsq = e.dot(vs, vs, slot=6)
+    seed_norm = float(np.sqrt(nsq))
+    if seed_norm == 0.0:
+        raise ParameterError("seed vector v0 must be nonzero")
+    P = e.blocks(top + 1)
+    # column 0 = v0 / |v0| (exact division, as numpy's v0 / seed_norm)
+    e.normalize_dev(vs, e.slot(6), [blk[0] for blk in P])
+    for k in range(top):
+        op.counters.spmvs += 1
+        e.spmv([blk[k] for blk in P], [blk[k + 1] for blk in P])
+    G = e.gram(P, top + 1)
+    del P
+    return G, seed_norm
+
+
+def _normal_equations(Gfull: np.ndarray, deg: int, counters: CostCounters) -> GramSystem:
+    # AV = powers[:, 1:deg+2]  ->  G = AV^T AV, rhs = AV^T v  (polyprec.py:115-122)
+    counters.dots += 2
+    counters.scalar_dots += (deg + 1) * (deg + 1) + (deg + 1)
+    return GramSystem(Gfull[1:deg + 2, 1:deg + 2].copy(), Gfull[1:deg + 2, 0].copy())
+
+
+def build_poly(op, v0, deg: int, counters: CostCounters,
+               seed_mode: str = "unspecified") -> PolyCoefficients:
+    """Degree-``deg`` minimum-residual polynomial (polyprec.py:125-147):
+    deg+1 device SpMVs, 2 dots, host Cholesky."""
+    if deg < 0:
+        raise ParameterError("polynomial degree must be non-negative")
+    Gfull, seed_norm = _device_power_gram(op, v0, deg + 1, counters)
+    counters.scalar_dots += 1
+    y = dense_cholesky(_normal_equations(Gfull, deg, counters))
+    return PolyCoefficients(deg, y, seed_norm, seed_mode)
+
+
+def auto_degree(op, v0, cap: int = DEFAULT_DEGREE_CAP, counters: CostCounters | None = None,
+                seed_mode: str = "unspecified") -> PolyCoefficients:
+    """Largest degree <= cap whose Gram system factors (polyprec.py:150-190):
+    one shared power sequence of cap+1 SpMVs, nested Gram blocks re-factored on
+    the host, degree-0 fallback."""
+    if cap < 1:
+        raise ParameterError("degree cap must be at least 1")
+    if counters is None:
+        counters = CostCounters()
+    Gfull, seed_norm = _device_power_gram(op, v0, cap + 1, counters)
+    counters.scalar_dots += 1
+    full = _normal_equations(Gfull, cap, counters)
+    best = None
+    for d in range(1, cap + 1):
+        try:
+            y = dense_cholesky(GramSystem(full.G[:d + 1, :d + 1], full.rhs[:d + 1]))
+        except CholeskyFailure:
+            continue
+        if np.all(np.isfinite(y)):
+            best = (d, y)
+    if best is None:
+        try:
+            y0 = dense_cholesky(GramSystem(full.G[:1, :1], full.rhs[:1]))
+        except CholeskyFailure:
+            y0 = np.zeros(1)
+        return PolyCoefficients(0, y0, seed_norm, seed_mode)
+    return PolyCoefficients(best[0], best[1], seed_norm, seed_mode)
+
+
+def build_poly_or_auto(op, v0, deg: int, counters: CostCounters,
+                       seed_mode: str = "unspecified"):
+    """Degree policy for requested degrees beyond what the power basis can
+    build: ``build_poly(deg)``, and on CholeskyFailure
+    ``auto_degree(cap=deg)``.  Returns (PolyCoefficients, failed_pivot|None).
+    The reference has no such helper; bench and parity tests apply the same
+    policy to the reference oracle."""
+    try:
+        return build_poly(op, v0, deg, counters, seed_mode), None
+    except CholeskyFailure as exc:
+        return auto_degree(op, v0, deg, counters, seed_mode), exc.pivot
+
+
+def apply_poly(p: PolyCoefficients, op, v, counters: CostCounters):
+    """``p(op) v`` (polyprec.py:193-212): ``degree`` fused SpMV passes,
+    ``degree + 1`` counted vector updates.  Bit-identical to the reference."""
+    e = _engine(op)
+    if isinstance(v, np.ndarray) or not isinstance(v, torch.Tensor):
+        vv = np.asarray(v, dtype=np.float64)
+        if vv.shape != (op.dimension,) and not (e.comm.distributed and vv.shape == (e.local_n,)):
+            raise DimensionMismatchError("vector length does not match operator")
+        v = vv
+    elif v.shape != (op.dimension,) and not (e.comm.distributed and v.shape == (e.local_n,)):
+        raise DimensionMismatchError("vector length does not match operator")
+    vs = e.ingest(v)
+    out, acc, w0, w1 = e.vecs(), e.vecs(), e.vecs(), e.vecs()
+    op.counters.spmvs += p.degree
+    counters.vector_updates += p.degree + 1
+    e.poly(p.y, vs, out, acc, w0, w1)
+    return e.emit(out, v)
+
+
+def lambda_p_lambda(p: PolyCoefficients, points) -> np.ndarray:
+    """alpha * p(alpha) by Horner (polyprec.py:215-226; host diagnostic)."""
+    pts = np.asarray(points, dtype=np.float64)
+    val = np.zeros_like(pts)
+    for c in p.y[::-1]:
+        val = val * pts + c
+    return pts * val
