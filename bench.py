@@ -1,0 +1,395 @@
+"""PP-GMRES benchmark (BASELINE.json metric: time-to-solution (s), plus the
+fused p(A)v SpMV's HBM GB/s against the measured roofline).
+
+One *step* = one polynomial-preconditioned GMRES solve of the workload:
+degree policy (``build_poly(d)``, on Cholesky failure ``auto_degree(cap=d)``)
++ ``solve``, with the matrix, b and v0 already resident in HBM.  Default
+workload = configs[1] (the 3-D 7-point convection-diffusion problem, n=1e6,
+GMRES(50), requested degree 25, tol 1e-10).  L2 is flushed (256 MiB write)
+between timed steps; every step is timed with CUDA events on the solve's
+stream; the job time is the max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+Under torchrun (N > 1) each rank owns one row block (z-planes) of the matrix:
+halo exchange before every SpMV and one all-reduce per batched dot phase
+(NCCL).  ``--impl reference`` times the CPU oracle port of the reference
+(oracle/pgmres_oracle.py) on a bounded sample of the same workload, rank 0
+only, and extrapolates to the full solve.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1907_00072_b200 import workloads as wl  # noqa: E402
+
+METRIC = ("PP-GMRES time-to-solution (s); fused p(A)v SpMV HBM GB/s vs ~8 TB/s roofline")
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _traffic(kernel_key: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/ncu_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(kernel_key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1907_00072_b200 as pg
+    from paper_1907_00072_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    conf = wl.CONFIGS[args.config]
+    N = wl.config_n(conf)
+
+    t_gen = time.perf_counter()
+    counters = pg.CostCounters()
+    if world > 1:
+        # row blocks aligned to grid planes (z for 3-D, rows for 2-D)
+        plane = conf.get("grid", 1) ** (2 if conf["gen"] in ("convdiff3d_7pt", "aniso27") else 1)
+        nplanes = N // plane
+        offs = np.array([(nplanes * p // world) * plane for p in range(world)] + [N])
+        r0, r1 = int(offs[rank]), int(offs[rank + 1])
+        block = wl.make_matrix(conf, rows=(r0, r1))
+        op = pg.DeviceMatrixOperator.distributed(block, offs, counters, device=dev)
+        if conf["rhs"] == "axrandom":
+            raise SystemExit("axrandom rhs is single-GPU only in the bench")
+        b_host = wl.splitmix_uniform(0, r1 - r0, start=r0)
+        v0_host = wl.splitmix_uniform(1, r1 - r0, start=r0)
+        nnz_local = block.nnz
+    else:
+        A = wl.make_matrix(conf)
+        op = pg.DeviceMatrixOperator(A, counters, device=dev)
+        b_host = wl.make_rhs(conf, A)
+        v0_host = wl.make_v0(N)
+        nnz_local = A.nnz
+        r0, r1 = 0, N
+    gen_s = time.perf_counter() - t_gen
+    e = op.engine
+    b_dev = torch.from_numpy(b_host).to(dev)
+    v0_dev = torch.from_numpy(v0_host).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    cfg = pg.GmresConfig(conf["m"], conf["tol"], args.max_iters)
+
+    def step(b, v0):
+        c = pg.CostCounters()
+        op.counters = c
+        poly, pivot = pg.build_poly_or_auto(op, v0, conf["degree"], c)
+        res = pg.solve(op, b, right_prec=poly, config=cfg)
+        return poly, pivot, res, c
+
+    for _ in range(args.warmup):
+        step(b_dev, v0_dev)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    times, results = [], []
+    e.timer = []
+    launches0 = _lib.launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # evict L2 (126 MB) between steps -- outside the events
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        out = step(b_dev, v0_dev)
+        ev1.record(stream)
+        results.append(out)
+        times.append((ev0, ev1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    launches = _lib.launches() - launches0
+    per_step = [a.elapsed_time(b) / 1e3 for a, b in times]
+    total = sum(per_step)
+    # kernel-level roofline of the dominant kernel (fused polynomial pass)
+    kt = sum(a.elapsed_time(b) for a, b, _ in e.timer) / 1e3
+    kb = sum(nb for _, _, nb in e.timer)
+    nk = len(e.timer)
+    e.timer = None
+    if world > 1:
+        t = torch.tensor([total, kt], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total, kt = float(t[0]), float(t[1])
+        kb_t = torch.tensor([kb], dtype=torch.float64, device=dev)
+        dist.all_reduce(kb_t)
+        kb = float(kb_t[0])
+
+    poly, pivot, res, c = results[-1]
+
+    # ---- e2e: public API from pinned host buffers, x back to the host -----
+    b_pin = torch.from_numpy(b_host).pin_memory()
+    v0_pin = torch.from_numpy(v0_host).pin_memory()
+    e2e_times = []
+    for i in range(max(1, min(args.steps, 3)) + 1):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cc = pg.CostCounters()
+        op.counters = cc
+        p2, _ = pg.build_poly_or_auto(op, v0_pin, conf["degree"], cc)
+        r2 = pg.solve(op, b_pin, right_prec=p2, config=cfg)
+        x_host = r2.x  # CPU tensor (D2H inside the timed region)
+        torch.cuda.synchronize()
+        if i > 0:  # first call is a warm-up
+            e2e_times.append(time.perf_counter() - t0)
+    e2e = float(np.mean(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t[0])
+    assert x_host.device.type == "cpu"
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(conf, res.iterations, res.cycles, sample_iters=args.cpu_sample_iters)
+
+    if rank == 0:
+        peak, peak_src = _peaks()
+        achieved = (kb / kt / 1e9) if kt > 0 else None
+        st = op.stats[0]
+        line = {
+            "metric": METRIC,
+            "value": total / args.steps,
+            "unit": "s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": False,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (generated operator, SplitMix64 b and v0)",
+            "config": {
+                "workload": conf["name"],
+                "n": N, "nnz": int(nnz_local) if world == 1 else None,
+                "restart_m": conf["m"], "tol": conf["tol"],
+                "degree_requested": conf["degree"], "degree_effective": poly.degree,
+                "build_poly_failed_pivot": pivot,
+                "iterations": res.iterations, "cycles": res.cycles,
+                "converged": bool(res.converged), "final_relres": res.final_relres,
+                "spmvs": c.spmvs, "dots": c.dots,
+                "parallelism": f"rowblock{world}",
+                "l2": "256 MiB buffer written between timed steps (outside the events)",
+                "sell": {"padded_nnz": st["padded_nnz"], "sigma": st["sigma"]},
+                "generation_s": round(gen_s, 2),
+            },
+            "roofline": {
+                "kernel": "sell_kernel<kPoly> (fused SpMV + polynomial epilogue)",
+                "bound": "hbm",
+                "achieved": achieved,
+                "peak": peak,
+                "peak_source": peak_src,
+                "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": _traffic("poly_pass_bytes_per_launch"),
+                "launches_timed": nk,
+                "kernel_s_per_step": kt / args.steps,
+                "share_of_step": kt / total if total else None,
+                "algorithmic_bytes_per_launch": kb / max(nk, 1),
+            },
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": 16 * N,
+                    "d2h_bytes_per_step": 8 * N,
+                    "note": "public API (build_poly_or_auto + solve) from pinned host b/v0, x to host"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port) -- bounded sample, extrapolated
+# ---------------------------------------------------------------------------
+def cpu_baseline(conf, iterations, cycles, sample_iters=5, threads=1):
+    from threadpoolctl import threadpool_limits
+
+    from oracle import pgmres_oracle as orc
+
+    A_h = wl.make_matrix(conf)
+    b = wl.make_rhs(conf, A_h)
+    v0 = wl.make_v0(A_h.nrows)
+    with threadpool_limits(limits=threads):
+        t = orc.Tally()
+        A = orc.OracleMatrix.of(A_h, t)
+        t0 = time.perf_counter()
+        _, eff, y, _ = orc.degree_policy(A, v0, conf["degree"], t)
+        t1 = time.perf_counter()
+        orc.gmres(A, b, y=y, m=conf["m"], tol=conf["tol"], max_iters=sample_iters)
+        t2 = time.perf_counter()
+    build_s, sample_s = t1 - t0, t2 - t1
+    # the sample = sample_iters inner iterations + one cycle end (GEMV, p(A)
+    # recovery, residual ~ one more iteration's SpMVs)
+    est = build_s + sample_s * (iterations + cycles) / (sample_iters + 1)
+    return {"value": est, "unit": "s", "cores": threads, "kind": "port",
+            "sample": (f"oracle (numpy port of the reference) on {conf['name']}: full degree "
+                       f"policy build ({build_s:.2f} s, effective degree {eff}) + "
+                       f"{sample_iters} GMRES iterations incl. one cycle end "
+                       f"({sample_s:.2f} s), extrapolated to {iterations} iterations / "
+                       f"{cycles} cycles"),
+            "measured_s": round(build_s + sample_s, 3)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    conf = wl.CONFIGS[args.config]
+    ref_iters = _reference_iterations(args.config)
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(conf, ref_iters[0], ref_iters[1], sample_iters=args.cpu_sample_iters,
+                          threads=threads)
+        if i >= args.warmup:
+            vals.append(cb)
+    v = float(np.mean([c["value"] for c in vals]))
+    cb = dict(vals[-1])
+    cb["value"] = v
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * v,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": conf["name"], "n": wl.config_n(conf),
+                                        "iterations_extrapolated_to": ref_iters[0],
+                                        "cycles": ref_iters[1]},
+        "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def _reference_iterations(config: int):
+    """Full-solve iteration / cycle counts of the reference on this workload
+    (tests/golden/cfg2_full_oracle.json, measured in the build container)."""
+    if config == 2:
+        try:
+            with open(os.path.join(ROOT, "tests", "golden", "cfg2_full_oracle.json")) as fh:
+                g = json.load(fh)
+            return g["iterations"], g["cycles"]
+        except Exception:
+            pass
+    return 50, 1
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--max-iters", type=int, default=200000)
+    ap.add_argument("--cpu-sample-iters", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

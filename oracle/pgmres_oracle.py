@@ -219,6 +219,48 @@ def gram(powers, deg, tally):
     return G, rhs
 
 
+def gram_exact(powers):
+    """Correctly rounded Gram matrix of the power columns (each entry: exact
+    products by Dekker splitting, exactly rounded sum by math.fsum).  Not the
+    reference's arithmetic -- the reference's G carries OpenBLAS rounding whose
+    order depends on the host CPU -- but the arbiter of the Cholesky-failure
+    degree decision in exact arithmetic."""
+    split = 134217729.0  # 2^27 + 1
+    k = powers.shape[1]
+    G = np.zeros((k, k))
+
+    def halves(a):
+        t = split * a
+        hi = t - (t - a)
+        return hi, a - hi
+
+    for i in range(k):
+        ah, al = halves(powers[:, i])
+        for j in range(i, k):
+            b = powers[:, j]
+            bh, bl = halves(b)
+            p = powers[:, i] * b
+            e = ((ah * bh - p) + ah * bl + al * bh) + al * bl
+            G[i, j] = G[j, i] = math.fsum(np.concatenate([p, e]))
+    return G
+
+
+def auto_deg_from_gram(Gfull, cap):
+    """auto_degree's selection loop (polyprec.py:171-190) on a given full
+    Gram of [v, Av, ..., A^{cap+1} v]."""
+    G = Gfull[1:cap + 2, 1:cap + 2]
+    rhs = Gfull[1:cap + 2, 0]
+    best = None
+    for d in range(1, cap + 1):
+        try:
+            yy = chol_solve(G[:d + 1, :d + 1], rhs[:d + 1])
+        except CholeskyFailureOracle:
+            continue
+        if np.all(np.isfinite(yy)):
+            best = (d, yy)
+    return best
+
+
 def min_res_poly(op, v0, deg, tally):
     """``build_poly`` (polyprec.py:125-147): returns (y, seed_norm)."""
     if deg < 0:

@@ -40,7 +40,8 @@ def _stale(target, deps):
 
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
-    headers = [os.path.join(INCLUDE, "pgmres.h"), os.path.join(CSRC, "internal.cuh")]
+    headers = [os.path.join(INCLUDE, "pgmres.h"), os.path.join(CSRC, "internal.cuh"),
+               os.path.join(CSRC, "pipeline.cuh")]
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     if not force and not _stale(LIB, srcs + headers + [__file__]):
         return LIB

@@ -102,5 +102,21 @@ def check(code: int, what: str = ""):
     raise errors.DeviceError(msg)
 
 
+#: entry points that launch exactly one libpgmres kernel per call
+LAUNCHING = frozenset({
+    "pg_spmv", "pg_poly_pass", "pg_residual", "pg_cgs2_phase1", "pg_cgs2_phase2",
+    "pg_cgs2_phase3", "pg_normalize", "pg_gram", "pg_gemv", "pg_dot", "pg_scale_add",
+    "pg_gather",
+})
+#: per-entry-point launch tally (bench.py reports it as gpu_launches)
+LAUNCH_COUNT: dict = {}
+
+
+def launches() -> int:
+    return sum(LAUNCH_COUNT.values())
+
+
 def call(name: str, *args):
     check(getattr(load(), name)(*args), name)
+    if name in LAUNCHING:
+        LAUNCH_COUNT[name] = LAUNCH_COUNT.get(name, 0) + 1

@@ -64,14 +64,20 @@ struct pg_matrix {
   int32_t* perm;       // [n_slices*32] local row of lane (nullptr if sigma<=1)
   int32_t* col;        // [padded]  SELL column indices (int32)
   double* val;         // [padded]  SELL values
+  int32_t* unit_slice; // [n_units+1] first slice of each TMA streaming unit
+  int64_t n_units;
+  bool use_tma;        // every slice fits a ring stage (kUnitEntries)
   size_t bytes;
 };
 
 namespace pg {
+// Entries per TMA streaming unit of the SpMV ring (12 B each: int32 + f64).
+constexpr int kUnitEntries = 3072;
 // Number of per-block partial slots a reduction may use.
 constexpr int kMaxBlocks = 1024;
-// Gram upper bound: ncols <= PG_KMAX -> ncols^2 outputs.
-constexpr int kMaxOut = PG_KMAX * PG_KMAX;
+// Per-block partial slots: the Gram stores (hi, lo) for each of the
+// ncols*(ncols+1)/2 pairs, ncols <= PG_KMAX.
+constexpr int kMaxOut = PG_KMAX * (PG_KMAX + 1);
 }  // namespace pg
 
 struct pg_workspace {
@@ -97,12 +103,17 @@ __device__ inline void last_block_reduce(double* partials, unsigned int* counter
   __syncthreads();
   if (!am_last) return;
   __threadfence();
-  for (int i = threadIdx.x; i < nout; i += blockDim.x) {
+  // warp w finishes outputs w, w+nw, ...: lane l sums blocks l, l+32, ... (all
+  // loads independent), then a fixed xor tree -- deterministic for a given grid
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned int G = gridDim.x;
+  for (int i = warp; i < nout; i += nw) {
     double s = 0.0;
-    for (unsigned int b = 0; b < gridDim.x; ++b) {
-      s += __ldcg(partials + (size_t)b * nout + i);
-    }
-    out[i] = s;
+#pragma unroll 8
+    for (unsigned int b = lane; b < G; b += 32) s += __ldcg(partials + (size_t)b * nout + i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[i] = s;
   }
   if (threadIdx.x == 0) *counter = 0u;
 }

@@ -58,6 +58,25 @@ __device__ __forceinline__ void stage_tile(double* buf, const double* __restrict
   }
 }
 
+// Error-free transformations for the compensated Gram sums: the power-basis
+// normal equations are so ill-conditioned (cond ~1e14 at the usable degrees)
+// that the Cholesky-failure degree signal (polyprec.py:80-82) is decided by
+// the rounding of G.  Accumulating each entry in double-double makes G
+// accurate to ~1 ulp, so the device takes the exact-arithmetic decision.
+__device__ __forceinline__ void dd_add(double x, double& hi, double& lo) {
+  const double s = __dadd_rn(hi, x);
+  const double bb = __dsub_rn(s, hi);
+  const double err = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(x, bb));
+  hi = s;
+  lo = __dadd_rn(lo, err);
+}
+__device__ __forceinline__ void dd_fma(double a, double b, double& hi, double& lo) {
+  const double p = __dmul_rn(a, b);
+  const double e = __fma_rn(a, b, -p);  // exact product error
+  dd_add(p, hi, lo);
+  lo = __dadd_rn(lo, e);
+}
+
 // Row projection t = sum_i V[r,i] c[i], sequential in i with FMA.  Phase 2
 // (from the smem tile) and phase 3 (from global) use this same order, so the
 // recomputed w1 is bit-identical.
@@ -91,8 +110,11 @@ __global__ void __launch_bounds__(kTileThreads)
   // per-thread accumulators
   constexpr int NACC = (MODE == kGram) ? kPairsPerThread : kColsPerWarp;
   double acc[NACC];
+  double acc_lo[(MODE == kGram) ? kPairsPerThread : 1];
 #pragma unroll
   for (int m = 0; m < NACC; ++m) acc[m] = 0.0;
+#pragma unroll
+  for (int m = 0; m < (MODE == kGram ? kPairsPerThread : 1); ++m) acc_lo[m] = 0.0;
   int pi[kPairsPerThread], pj[kPairsPerThread];
   const int npairs = k * (k + 1) / 2;
   if (MODE == kGram) {
@@ -142,16 +164,17 @@ __global__ void __launch_bounds__(kTileThreads)
             acc[m] = __fma_rn(col[lane + 32 * q], vec[lane + 32 * q], acc[m]);
         }
       }
-    } else {  // Gram: all pairs i <= j
+    } else {  // Gram: all pairs i <= j, compensated (double-double) sums
 #pragma unroll
       for (int m = 0; m < kPairsPerThread; ++m) {
         if (pi[m] >= 0) {
           const double* a = S + pi[m] * kTileStride;
           const double* b = S + pj[m] * kTileStride;
-          double s = acc[m];
-#pragma unroll 8
-          for (int r = 0; r < kTileRows; ++r) s = __fma_rn(a[r], b[r], s);
-          acc[m] = s;
+          double hi = acc[m], lo = acc_lo[m];
+#pragma unroll 4
+          for (int r = 0; r < kTileRows; ++r) dd_fma(a[r], b[r], hi, lo);
+          acc[m] = hi;
+          acc_lo[m] = lo;
         }
       }
     }
@@ -161,15 +184,36 @@ __global__ void __launch_bounds__(kTileThreads)
 
   // block partials, then deterministic cross-block finish
   if (MODE == kGram) {
-    double* part = partials + (size_t)blockIdx.x * (k * k);
+    // packed upper triangle, (hi, lo) per pair
+    double* part = partials + (size_t)blockIdx.x * (2 * npairs);
 #pragma unroll
     for (int m = 0; m < kPairsPerThread; ++m) {
-      if (pi[m] >= 0) {
-        part[pi[m] * k + pj[m]] = acc[m];
-        part[pj[m] * k + pi[m]] = acc[m];
+      const int p = threadIdx.x + m * kTileThreads;
+      if (p < npairs) {
+        part[2 * p] = acc[m];
+        part[2 * p + 1] = acc_lo[m];
       }
     }
-    last_block_reduce(partials, counter, k * k, out);
+    __shared__ bool am_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+      double hi = 0.0, lo = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) {
+        dd_add(__ldcg(partials + (size_t)b * 2 * npairs + 2 * p), hi, lo);
+        lo += __ldcg(partials + (size_t)b * 2 * npairs + 2 * p + 1);
+      }
+      int i = 0, rem = p;
+      while (rem >= k - i) { rem -= k - i; ++i; }
+      const int j = i + rem;
+      out[i * k + j] = hi + lo;
+      out[j * k + i] = hi + lo;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
   } else {
 #pragma unroll
     for (int m = 0; m < kColsPerWarp; ++m) {

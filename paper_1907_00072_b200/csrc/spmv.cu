@@ -1,25 +1,39 @@
 // libpgmres: SELL-C-sigma fp64 SpMV and the fused polynomial pass.
 //
 // One thread owns one row (one lane of a 32-row slice).  Slice entries are
-// stored lane-interleaved (entry j of lane t at slice_ptr[s] + j*32 + t), so
-// each warp-wide load of the value / index streams is a contiguous 256 B /
-// 128 B segment.  The row sum is accumulated sequentially in stored column
-// order with separately rounded products (__dmul_rn / __dadd_rn: never
-// contracted to FMA), which is bit-for-bit the reference SpMV
-// (sparse.py:164-168, np.bincount over values*x[col]).
+// stored lane-interleaved (entry j of lane t at slice_ptr[s] + j*32 + t).
+// The row sum is accumulated sequentially in stored column order with
+// separately rounded products (__dmul_rn / __dadd_rn: never contracted to
+// FMA), which is bit-for-bit the reference SpMV (sparse.py:164-168,
+// np.bincount over values*x[col]).
 //
 // The polynomial recurrence of apply_poly (polyprec.py:205-211) runs in the
 // epilogue of the same pass: acc <- acc + y_k * (A w)[row], so a degree-d
 // application streams A exactly d times with no separate axpy kernels.
+//
+// Two kernels share that row arithmetic:
+//  * sell_tma_kernel (default): one persistent CTA per SM.  A producer warp
+//    streams "units" (runs of consecutive slices, <= kUnitEntries entries) of
+//    the index and value arrays into a kStages-deep shared-memory ring with
+//    cp.async.bulk + mbarrier transaction counts; 8 consumer warps take the
+//    slices round-robin, issue all x gathers of a row chunk at once and run
+//    the epilogue.  The matrix stream never waits on the gather latency.
+//  * sell_kernel: plain grid of one-row-per-thread loads, for matrices with a
+//    slice too wide for a ring stage.
 
 #include "internal.cuh"
+#include "pipeline.cuh"
 
 namespace pg {
 
 enum SellMode { kSpmv = 0, kPoly = 1, kResid = 2 };
 
 constexpr int kSellThreads = 256;
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 8;
+constexpr int kConsumerWarps = 16;
+constexpr int kTmaThreads = (kConsumerWarps + 1) * 32;
+constexpr int kStages = 6;
+constexpr size_t kTmaSmem = (size_t)kStages * kUnitEntries * (sizeof(int32_t) + sizeof(double));
 
 struct SellArgs {
   const int64_t* __restrict__ slice_ptr;
@@ -32,25 +46,76 @@ struct SellArgs {
   int64_t nlanes;
 };
 
-// Sequential row sum, exact reference order.
-__device__ __forceinline__ double sell_row(const SellArgs& a, int64_t lane,
-                                           const double* __restrict__ x) {
-  const int64_t s = lane >> 5;
-  const int t = (int)(lane & 31);
-  const int w = __ldg(a.slice_w + s);
-  const int len = __ldg(a.row_len + lane);
-  const int64_t base = __ldg(a.slice_ptr + s) + t;
-  const int32_t* __restrict__ cp = a.col + base;
-  const double* __restrict__ vp = a.val + base;
+struct Epi {
+  const double* acc_in;
+  const double* base;
+  double* acc_out;
+  double* w_out;
+  const double* b;
+  double y0, yk;
+  int flags;
+};
+
+__device__ __forceinline__ int64_t lane_row(const SellArgs& a, int64_t lane) {
+  if (a.perm) return __ldg(a.perm + lane);
+  return lane < a.nrows ? lane : -1;
+}
+
+// Epilogue operands of a row, loaded BEFORE the row's gathers so that their
+// HBM latency overlaps the gather latency.
+struct Pre {
+  double a, b;
+};
+
+template <int MODE>
+__device__ __forceinline__ Pre epi_load(const Epi& e, const double* __restrict__ x, int64_t row) {
+  Pre p{0.0, 0.0};
+  if (row < 0) return p;
+  if (MODE == kPoly) {
+    p.a = (e.flags & PG_PASS_FIRST) ? x[row] : e.acc_in[row];
+    if (e.base) p.b = e.base[row];
+  } else if (MODE == kResid) {
+    p.a = e.b[row];
+  }
+  return p;
+}
+
+// Row epilogue; returns the residual entry (kResid) for the norm.
+template <int MODE>
+__device__ __forceinline__ double epilogue(const Epi& e, const Pre& p, int64_t row, double ax) {
+  if (MODE == kSpmv) {
+    e.acc_out[row] = ax;
+    return 0.0;
+  } else if (MODE == kPoly) {
+    double t = (e.flags & PG_PASS_FIRST) ? __dmul_rn(e.y0, p.a) : p.a;
+    t = __dadd_rn(t, __dmul_rn(e.yk, ax));
+    if (e.flags & PG_PASS_WRITE_W) e.w_out[row] = ax;
+    if (e.base) t = __dadd_rn(p.b, t);
+    e.acc_out[row] = t;
+    return 0.0;
+  } else {
+    const double r = __dsub_rn(p.a, ax);
+    e.acc_out[row] = r;
+    return r;
+  }
+}
+
+// Sequential row sum over entries held at p_col[j*32], p_val[j*32].
+template <class ColPtr, class ValPtr>
+__device__ __forceinline__ double row_sum(ColPtr cp, ValPtr vp, int w, int len,
+                                          const double* __restrict__ x) {
   double acc = 0.0;
-  int j = 0;
-  for (; j + kUnroll <= w; j += kUnroll) {
-    int c[kUnroll];
+  for (int j = 0; j < w; j += kUnroll) {
     double v[kUnroll], xv[kUnroll];
+    int c[kUnroll];
+    // all index / value loads of the chunk first (bounded by the uniform slice
+    // width), then all gathers (bounded by this row's length)
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      c[u] = __ldcs(cp + (int64_t)(j + u) * PG_SLICE);
-      v[u] = __ldcs(vp + (int64_t)(j + u) * PG_SLICE);
+      if (j + u < w) {
+        c[u] = cp(j + u);
+        v[u] = vp(j + u);
+      }
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) xv[u] = (j + u < len) ? __ldg(x + c[u]) : 0.0;
@@ -58,24 +123,23 @@ __device__ __forceinline__ double sell_row(const SellArgs& a, int64_t lane,
     for (int u = 0; u < kUnroll; ++u)
       if (j + u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
   }
-  for (; j < w; ++j) {
-    int c = __ldcs(cp + (int64_t)j * PG_SLICE);
-    double v = __ldcs(vp + (int64_t)j * PG_SLICE);
-    if (j < len) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + c)));
-  }
   return acc;
 }
 
-__device__ __forceinline__ int64_t lane_row(const SellArgs& a, int64_t lane) {
-  if (a.perm) return __ldg(a.perm + lane);
-  return lane < a.nrows ? lane : -1;
+template <int MODE>
+__device__ __forceinline__ void finish_resid(double local, double* partials, unsigned* counter,
+                                             double* nsq) {
+  if (MODE == kResid) {
+    const double s = block_sum(local);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    last_block_reduce(partials, counter, 1, nsq);
+  }
 }
 
+// ------------------------------------------------------------ plain kernel --
 template <int MODE>
 __global__ void __launch_bounds__(kSellThreads)
-    sell_kernel(SellArgs a, const double* __restrict__ x, const double* acc_in,
-                const double* base, double* acc_out, double* w_out, double y0, double yk,
-                int flags, const double* __restrict__ b, double* partials,
+    sell_kernel(SellArgs a, const double* __restrict__ x, Epi e, double* partials,
                 unsigned int* counter, double* nsq) {
   double local = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -83,26 +147,94 @@ __global__ void __launch_bounds__(kSellThreads)
        lane += stride) {
     const int64_t row = lane_row(a, lane);
     if (row < 0) continue;
-    const double ax = sell_row(a, lane, x);
-    if (MODE == kSpmv) {
-      acc_out[row] = ax;
-    } else if (MODE == kPoly) {
-      double t = (flags & PG_PASS_FIRST) ? __dmul_rn(y0, x[row]) : acc_in[row];
-      t = __dadd_rn(t, __dmul_rn(yk, ax));
-      if (flags & PG_PASS_WRITE_W) w_out[row] = ax;
-      if (base) t = __dadd_rn(base[row], t);
-      acc_out[row] = t;
-    } else {  // residual r = b - A x, sum r^2
-      const double r = __dsub_rn(b[row], ax);
-      acc_out[row] = r;
-      local = fma(r, r, local);
+    const int64_t s = lane >> 5;
+    const int w = __ldg(a.slice_w + s);
+    const int len = __ldg(a.row_len + lane);
+    const int64_t base = __ldg(a.slice_ptr + s) + (lane & 31);
+    const int32_t* __restrict__ cpp = a.col + base;
+    const double* __restrict__ vpp = a.val + base;
+    const Pre pre = epi_load<MODE>(e, x, row);
+    const double ax = row_sum([&](int j) { return __ldcs(cpp + (int64_t)j * PG_SLICE); },
+                              [&](int j) { return __ldcs(vpp + (int64_t)j * PG_SLICE); }, w,
+                              len, x);
+    const double r = epilogue<MODE>(e, pre, row, ax);
+    if (MODE == kResid) local = __fma_rn(r, r, local);
+  }
+  finish_resid<MODE>(local, partials, counter, nsq);
+}
+
+// -------------------------------------------------------- TMA ring kernel --
+template <int MODE>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    sell_tma_kernel(SellArgs a, const int32_t* __restrict__ unit_slice, int64_t n_units,
+                    const double* __restrict__ x, Epi e, double* partials,
+                    unsigned int* counter, double* nsq) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  int32_t* scol = reinterpret_cast<int32_t*>(smem_raw);
+  double* sval = reinterpret_cast<double*>(smem_raw + (size_t)kStages * kUnitEntries * 4);
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) uint64_t empty[kStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  double local = 0.0;
+  if (warp == kConsumerWarps) {
+    // producer: one elected lane streams this CTA's units into the ring
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+        const int s = it % kStages;
+        mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+        const int64_t e0 = __ldg(a.slice_ptr + __ldg(unit_slice + u));
+        const int64_t e1 = __ldg(a.slice_ptr + __ldg(unit_slice + u + 1));
+        const uint32_t ne = (uint32_t)(e1 - e0);
+        mbar_expect_tx(&full[s], ne * 12u);  // tx 0 (empty unit) completes at once
+        if (ne) {
+          bulk_g2s(scol + (size_t)s * kUnitEntries, a.col + e0, ne * 4u, &full[s]);
+          bulk_g2s(sval + (size_t)s * kUnitEntries, a.val + e0, ne * 8u, &full[s]);
+        }
+      }
+    }
+  } else {
+    // consumers: slices of this CTA's stream go round-robin to the 8 warps
+    int it = 0;
+    int64_t seen = 0;  // slices of earlier units in this CTA's stream
+    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+      const int s = it % kStages;
+      const int64_t s0 = __ldg(unit_slice + u), s1 = __ldg(unit_slice + u + 1);
+      const int64_t e0 = __ldg(a.slice_ptr + s0);
+      const int32_t* C = scol + (size_t)s * kUnitEntries;
+      const double* Vv = sval + (size_t)s * kUnitEntries;
+      int64_t first = s0 + ((warp - seen) % kConsumerWarps + kConsumerWarps) % kConsumerWarps;
+      if (first < s1) mbar_wait(&full[s], (it / kStages) & 1);
+      for (int64_t sl = first; sl < s1; sl += kConsumerWarps) {
+        const int64_t ln = sl * PG_SLICE + lane;
+        const int64_t row = lane_row(a, ln);
+        const int w = __ldg(a.slice_w + sl);
+        const int len = __ldg(a.row_len + ln);
+        const int off = (int)(__ldg(a.slice_ptr + sl) - e0) + lane;
+        const Pre pre = epi_load<MODE>(e, x, row);
+        const double ax = row_sum([&](int j) { return C[off + j * PG_SLICE]; },
+                                  [&](int j) { return Vv[off + j * PG_SLICE]; }, w, len, x);
+        if (row >= 0) {
+          const double r = epilogue<MODE>(e, pre, row, ax);
+          if (MODE == kResid) local = __fma_rn(r, r, local);
+        }
+      }
+      seen += s1 - s0;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
   }
-  if (MODE == kResid) {
-    double s = block_sum(local);
-    if (threadIdx.x == 0) partials[blockIdx.x] = s;
-    last_block_reduce(partials, counter, 1, nsq);
-  }
+  finish_resid<MODE>(local, partials, counter, nsq);
 }
 
 static SellArgs args_of(const pg_matrix* m) {
@@ -119,34 +251,41 @@ static SellArgs args_of(const pg_matrix* m) {
 }
 
 template <int MODE>
-static void launch_sell(const pg_matrix* m, const double* x, const double* acc_in,
-                        const double* base, double* acc_out, double* w_out, double y0,
-                        double yk, int flags, const double* b, pg_workspace* ws,
+static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace* ws,
                         double* nsq, cudaStream_t st) {
   SellArgs a = args_of(m);
-  int64_t blocks_needed = (a.nlanes + kSellThreads - 1) / kSellThreads;
   if (MODE == kResid) {
     PG_REQUIRE(ws && nsq, PG_ERR_PARAMETER, "residual needs a workspace and nsq");
     PG_REQUIRE(ws->device == m->device, PG_ERR_PARAMETER, "workspace on another device");
   }
-  if (blocks_needed == 0) {
+  if (a.nlanes == 0) {
     if (MODE == kResid) PG_CUDA(cudaMemsetAsync(nsq, 0, sizeof(double), st));
     return;
   }
-  // Grid: enough resident blocks to fill every SM; grid-stride beyond that.
-  static int grid_cache[3][64] = {};
-  int dev = m->device;
-  int g;
-  if (dev < 64 && grid_cache[MODE][dev] > 0) {
-    g = grid_cache[MODE][dev];
+  const int dev = m->device;
+  PG_REQUIRE(dev >= 0 && dev < 64, PG_ERR_PARAMETER, "device ordinal out of range");
+  double* part = ws ? ws->partials : nullptr;
+  unsigned* cnt = ws ? ws->counter : nullptr;
+  static int sms[64] = {};
+  if (!sms[dev]) PG_CUDA(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
+  if (m->use_tma) {
+    static bool attr[3][64] = {};
+    if (!attr[MODE][dev]) {
+      PG_CUDA(cudaFuncSetAttribute(sell_tma_kernel<MODE>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+      attr[MODE][dev] = true;
+    }
+    int g = sms[dev];
+    if (m->n_units < g) g = (int)m->n_units;
+    sell_tma_kernel<MODE><<<g, kTmaThreads, kTmaSmem, st>>>(a, m->unit_slice, m->n_units, x, e,
+                                                           part, cnt, nsq);
   } else {
-    g = grid_for(dev, (const void*)sell_kernel<MODE>, kSellThreads, 0, int64_t(1) << 40);
-    if (dev < 64) grid_cache[MODE][dev] = g;
+    // one row per thread; reductions keep the grid within the partial slots
+    int64_t blocks = (a.nlanes + kSellThreads - 1) / kSellThreads;
+    const int64_t cap = (MODE == kResid) ? kMaxBlocks : (int64_t)sms[dev] * 64;
+    if (blocks > cap) blocks = cap;
+    sell_kernel<MODE><<<(int)blocks, kSellThreads, 0, st>>>(a, x, e, part, cnt, nsq);
   }
-  if (blocks_needed < g) g = (int)blocks_needed;
-  sell_kernel<MODE><<<g, kSellThreads, 0, st>>>(
-      a, x, acc_in, base, acc_out, w_out, y0, yk, flags, b,
-      ws ? ws->partials : nullptr, ws ? ws->counter : nullptr, nsq);
   check_launch();
 }
 
@@ -159,8 +298,8 @@ extern "C" {
 PG_API int pg_spmv(const pg_matrix* mat, const double* d_x, double* d_y, void* stream) {
   return guard([&] {
     PG_REQUIRE(mat && d_x && d_y, PG_ERR_PARAMETER, "null argument");
-    launch_sell<kSpmv>(mat, d_x, nullptr, nullptr, d_y, nullptr, 0.0, 0.0, 0, nullptr,
-                       nullptr, nullptr, as_stream(stream));
+    Epi e{nullptr, nullptr, d_y, nullptr, nullptr, 0.0, 0.0, 0};
+    launch_sell<kSpmv>(mat, d_x, e, nullptr, nullptr, as_stream(stream));
   });
 }
 
@@ -173,8 +312,8 @@ PG_API int pg_poly_pass(const pg_matrix* mat, const double* d_x, const double* d
                "acc_in required unless PG_PASS_FIRST");
     PG_REQUIRE(!(flags & PG_PASS_WRITE_W) || d_w_out, PG_ERR_PARAMETER,
                "w_out required with PG_PASS_WRITE_W");
-    launch_sell<kPoly>(mat, d_x, d_acc_in, d_base, d_acc_out, d_w_out, y0, yk, flags,
-                       nullptr, nullptr, nullptr, as_stream(stream));
+    Epi e{d_acc_in, d_base, d_acc_out, d_w_out, nullptr, y0, yk, flags};
+    launch_sell<kPoly>(mat, d_x, e, nullptr, nullptr, as_stream(stream));
   });
 }
 
@@ -182,8 +321,8 @@ PG_API int pg_residual(const pg_matrix* mat, const double* d_x, const double* d_
                        double* d_nsq, pg_workspace* ws, void* stream) {
   return guard([&] {
     PG_REQUIRE(mat && d_x && d_b && d_r, PG_ERR_PARAMETER, "null argument");
-    launch_sell<kResid>(mat, d_x, nullptr, nullptr, d_r, nullptr, 0.0, 0.0, 0, d_b, ws, d_nsq,
-                        as_stream(stream));
+    Epi e{nullptr, nullptr, d_r, nullptr, d_b, 0.0, 0.0, 0};
+    launch_sell<kResid>(mat, d_x, e, ws, d_nsq, as_stream(stream));
   });
 }
 

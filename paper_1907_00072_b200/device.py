@@ -294,6 +294,9 @@ class Engine:
         self.comm = comm
         self.N = int(n_global)
         self.P = len(shards)
+        # optional list collecting (start_event, end_event, algorithmic_bytes)
+        # per fused polynomial pass (bench.py's live roofline measurement)
+        self.timer = None
 
     # ---- construction -------------------------------------------------------
     @classmethod
@@ -399,8 +402,11 @@ class Engine:
         return self.from_host(v)
 
     def emit(self, xs, like):
+        """Result in the caller's vector type: CUDA tensor -> CUDA tensor, CPU
+        tensor -> CPU tensor (one D2H copy), anything else -> numpy."""
         if isinstance(like, torch.Tensor):
-            return self.to_torch(xs)
+            out = self.to_torch(xs)
+            return out if like.is_cuda else out.cpu()
         return self.to_host(xs)
 
     # ---- kernels ----------------------------------------------------------------
@@ -438,9 +444,20 @@ class Engine:
             dst = out if last else acc
             for i, s in enumerate(self._each()):
                 b = base[i] if (last and base is not None) else None
+                if self.timer is not None:
+                    ev0 = torch.cuda.Event(enable_timing=True)
+                    ev0.record(torch.cuda.current_stream(s.device))
                 _lib.call("pg_poly_pass", s.mat, ptr(cur[i]), ptr(acc[i]) if k > 1 else None,
                           ptr(b) if b is not None else None, ptr(dst[i]),
                           ptr(nxt[i]) if not last else None, y[0], y[k], flags, s.stream)
+                if self.timer is not None:
+                    ev1 = torch.cuda.Event(enable_timing=True)
+                    ev1.record(torch.cuda.current_stream(s.device))
+                    # algorithmic bytes: 12 B per nonzero (value +
+                    # int32 index), 4 B row length, 8 B compulsory gather of x,
+                    # then the epilogue's vector traffic
+                    vec = 8 * (int(k > 1) + 1 + int(not last) + int(b is not None))
+                    self.timer.append((ev0, ev1, 12 * s.nnz + (12 + vec) * s.n))
             if not last:
                 self.halo(nxt)
                 cur = nxt

@@ -327,7 +327,13 @@ def test_small_configs_with_degree_policy(golden, cfg, kw):
     b = wl.make_rhs(conf, h)
     res, sc, ref, t, poly, c = _solve_pair(h, b, conf["degree"], conf["m"], conf["tol"])
     _agree(res, sc, ref, t, conf["tol"], c)
-    assert abs(poly.degree - rec["effective_degree"]) <= 2
+    # the degree decision: the device's compensated Gram takes the decision of
+    # a correctly rounded Gram; the reference's OpenBLAS Gram may land +-3 away
+    # (small4: reference 12, exact 15) -- DESIGN.md §5
+    v = wl.make_v0(h.nrows)
+    P = orc.power_columns(_oracle(h), v / np.linalg.norm(v), conf["degree"] + 1)
+    exact_d = orc.auto_deg_from_gram(orc.gram_exact(P), conf["degree"])[0]
+    assert abs(poly.degree - exact_d) <= 1
     if poly.degree == rec["effective_degree"]:
         assert abs(res.iterations - rec["iterations"]) <= 2
 
