@@ -1,0 +1,269 @@
+"""CPU-only tests of the boundary and the host logic: the C-ABI library loads
+and exports every symbol include/pgmres.h declares (no compute calls), the
+host-built SELL-C-sigma layout reproduces the reference row order, the
+row-block partition / halo plan reconstructs the global SpMV, the
+torch.distributed halo exchange + all-reduce work across 2 gloo ranks, and the
+host-side solver pieces mirror the reference."""
+
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import pgmres_oracle as orc
+from paper_1907_00072_b200 import _lib, workloads as wl
+from paper_1907_00072_b200 import device as dv
+
+
+# ---------------------------------------------------------------------------
+# the C-ABI library
+# ---------------------------------------------------------------------------
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    syms = _lib.header_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing
+    assert set(_lib._SIGNATURES) == set(syms)  # every declared entry point is bound
+    assert lib.pg_version() == 1
+
+
+def test_error_codes_and_last_error():
+    lib = _lib.load()
+    rp = np.array([0, 1, 2], dtype=np.int64)
+    nsl, pad = C.c_int64(), C.c_int64()
+    assert lib.pg_sell_size(2, rp.ctypes.data, 1, C.byref(nsl), C.byref(pad)) == 0
+    bad = np.array([1, 1, 2], dtype=np.int64)  # row_ptr[0] != 0
+    assert lib.pg_sell_size(2, bad.ctypes.data, 1, None, None) == _lib.PG_ERR_PARAMETER
+    assert "row_ptr[0]" in _lib.last_error()
+    with pytest.raises(_lib.errors.ParameterError):
+        _lib.call("pg_sell_size", 2, bad.ctypes.data, 1, None, None)
+
+
+def _sell_host(h, sigma):
+    lib = _lib.load()
+    nsl, pad = C.c_int64(), C.c_int64()
+    _lib.call("pg_sell_size", h.nrows, h.row_ptr.ctypes.data, sigma, C.byref(nsl), C.byref(pad))
+    ns, p = nsl.value, pad.value
+    sp = np.zeros(ns + 1, np.int64)
+    sw = np.zeros(ns, np.int32)
+    rl = np.zeros(ns * 32, np.int32)
+    pm = np.zeros(ns * 32, np.int32)
+    col = np.zeros(max(p, 1), np.int32)
+    val = np.zeros(max(p, 1), np.float64)
+    cols = np.ascontiguousarray(h.col_idx, np.int64)
+    vals = np.ascontiguousarray(h.values, np.float64)
+    _lib.call("pg_sell_fill", h.nrows, h.ncols, h.row_ptr.ctypes.data, cols.ctypes.data,
+              vals.ctypes.data, sigma, sp.ctypes.data, sw.ctypes.data, rl.ctypes.data,
+              pm.ctypes.data, col.ctypes.data, val.ctypes.data)
+    assert lib is not None
+    return sp, sw, rl, pm, col, val
+
+
+def _sell_spmv(sell, nrows, x):
+    """Row-sequential SpMV over the SELL layout, in numpy (column j of all
+    lanes at once, so each lane's sum runs in stored order)."""
+    sp, sw, rl, pm, col, val = sell
+    y = np.zeros(nrows)
+    for s in range(len(sw)):
+        lanes = np.arange(32)
+        acc = np.zeros(32)
+        for j in range(sw[s]):
+            pos = sp[s] + j * 32 + lanes
+            live = j < rl[s * 32 + lanes]
+            acc = np.where(live, acc + val[pos] * x[col[pos]], acc)
+        rows = pm[s * 32 + lanes]
+        ok = rows >= 0
+        y[rows[ok]] = acc[ok]
+    return y
+
+
+@pytest.mark.parametrize("sigma", [1, 64])
+def test_sell_layout_reproduces_reference_order(golden, sigma):
+    a, _ = golden
+    R = wl.CsrHost(1000, 1000, a["rand1k_row_ptr"], a["rand1k_col_idx"], a["rand1k_values"])
+    sell = _sell_host(R, sigma)
+    assert np.array_equal(_sell_spmv(sell, 1000, a["rand1k_x"]), a["rand1k_y"])
+    L = wl.CsrHost(4096, 4096, a["lap64_row_ptr"], a["lap64_col_idx"], a["lap64_values"])
+    x = orc.sm64_uniform(0, 4096)
+    assert np.array_equal(_sell_spmv(_sell_host(L, sigma), 4096, x), a["cfg1_b"])
+    if sigma > 1:  # sorting makes slices uniform: padding shrinks
+        assert _sell_host(R, sigma)[0][-1] <= _sell_host(R, 1)[0][-1]
+
+
+def test_sell_rejects_bad_columns():
+    # column 5 of a 2 x 2 matrix: the C-ABI reports ParameterError, as CsrMatrix
+    # does (sparse.py:78-79)
+    with pytest.raises(_lib.errors.ParameterError):
+        _sell_host(wl.CsrHost(2, 2, [0, 1, 2], [0, 5], [1.0, 1.0]), 1)
+
+
+# ---------------------------------------------------------------------------
+# row-block partition and halo plan (host logic of device.Engine)
+# ---------------------------------------------------------------------------
+def _emulate_sharded_spmv(h, parts, x):
+    offs = dv.balanced_offsets(h.row_ptr, parts)
+    y = np.zeros(h.nrows)
+    for p in range(parts):
+        r0, r1 = int(offs[p]), int(offs[p + 1])
+        q0, q1 = int(h.row_ptr[r0]), int(h.row_ptr[r1])
+        cols = h.col_idx[q0:q1]
+        ghosts = dv.ghost_columns(cols, r0, r1)
+        recv = dv.plan_recv(ghosts, offs, r1 - r0)
+        local_cols = dv.localize_columns(cols, r0, r1, ghosts)
+        xe = np.zeros(r1 - r0 + len(ghosts))
+        xe[:r1 - r0] = x[r0:r1]
+        for q, (off, cnt) in recv.items():
+            assert offs[q] <= ghosts[off - (r1 - r0)] < offs[q + 1]  # owned by q
+            xe[off:off + cnt] = x[ghosts[off - (r1 - r0): off - (r1 - r0) + cnt]]
+        blk = orc.OracleMatrix(r1 - r0, len(xe), h.row_ptr[r0:r1 + 1] - q0, local_cols,
+                               h.values[q0:q1])
+        y[r0:r1] = blk.matvec(xe)
+    return y, offs
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 8])
+def test_partition_halo_plan_reconstructs_spmv(parts):
+    for h in (wl.convdiff3d_7pt(12), wl.random_lognormal(3000, seed=4), wl.aniso27(8)):
+        x = wl.splitmix_uniform(3, h.nrows)
+        y, offs = _emulate_sharded_spmv(h, parts, x)
+        assert np.array_equal(y, orc.OracleMatrix.of(h).matvec(x))  # bitwise: order kept
+        assert offs[0] == 0 and offs[-1] == h.nrows and np.all(np.diff(offs) >= 0)
+
+
+def test_row_range_generators_concatenate():
+    for make in (lambda rows=None: wl.convdiff3d_7pt(10, rows=rows),
+                 lambda rows=None: wl.aniso27(7, rows=rows),
+                 lambda rows=None: wl.convdiff2d_9pt(33, rows=rows),
+                 lambda rows=None: wl.random_lognormal(70000, seed=3, rows=rows)):
+        full = make()
+        cut = full.nrows // 3
+        a, b = make(rows=(0, cut)), make(rows=(cut, full.nrows))
+        assert b.row_offset == cut
+        assert np.array_equal(np.concatenate([a.col_idx, b.col_idx]), full.col_idx)
+        assert np.array_equal(np.concatenate([a.values, b.values]), full.values)
+    assert wl.aniso27(200, rows=(0, 0)).nrows == 0
+    g = 20
+    assert wl.aniso27(g).nnz == (3 * g - 2) ** 3
+
+
+def test_choose_sigma():
+    assert dv.choose_sigma(wl.convdiff3d_7pt(16).row_ptr) == 1
+    assert dv.choose_sigma(wl.random_lognormal(20000, seed=1).row_ptr) > 1
+
+
+# ---------------------------------------------------------------------------
+# distributed halo exchange + all-reduce over 2 gloo ranks
+# ---------------------------------------------------------------------------
+class _CpuShard:
+    """Test double of device.Shard for the gloo ranks: same plan / send-list
+    fields, numpy SpMV on the local block instead of a CUDA kernel."""
+
+    def __init__(self, h_block, offs, rank):
+        self.r0, self.r1 = int(offs[rank]), int(offs[rank + 1])
+        self.n = self.r1 - self.r0
+        ghosts = dv.ghost_columns(h_block.col_idx, self.r0, self.r1)
+        self.plan = dv.HaloPlan(ghosts, dv.plan_recv(ghosts, offs, self.n))
+        self.n_ext = self.n + len(ghosts)
+        self.local = orc.OracleMatrix(self.n, self.n_ext, h_block.row_ptr,
+                                      dv.localize_columns(h_block.col_idx, self.r0, self.r1,
+                                                          ghosts), h_block.values)
+
+    def set_send(self, q, idx):
+        self.plan.send[q] = torch.from_numpy(np.asarray(idx, dtype=np.int64))
+
+    def packed_send(self, x, q):
+        return x.index_select(0, self.plan.send[q]).contiguous()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _gloo_worker(rank, world, port, cfg_name, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        h = wl.convdiff3d_7pt(10) if cfg_name == "7pt" else wl.random_lognormal(4000, seed=9)
+        offs = dv.balanced_offsets(h.row_ptr, world)
+        r0, r1 = int(offs[rank]), int(offs[rank + 1])
+        blk = wl.convdiff3d_7pt(10, rows=(r0, r1)) if cfg_name == "7pt" else \
+            wl.random_lognormal(4000, seed=9, rows=(r0, r1))
+        s = _CpuShard(blk, offs, rank)
+        comm = dv.DistComm([s])
+        dv.exchange_send_lists([s], comm)
+        x = wl.splitmix_uniform(5, h.nrows)
+        xe = torch.zeros(s.n_ext, dtype=torch.float64)
+        xe[:s.n] = torch.from_numpy(x[r0:r1])
+        comm.halo([xe])
+        y_local = s.local.matvec(xe.numpy())
+        want = orc.OracleMatrix.of(h).matvec(x)[r0:r1]
+        ok_spmv = bool(np.array_equal(y_local, want))
+        part = torch.tensor([float(np.dot(y_local, y_local)), float(rank + 1)],
+                            dtype=torch.float64)
+        comm.allreduce([part])
+        full = orc.OracleMatrix.of(h).matvec(x)
+        ok_red = abs(part[0].item() - float(np.dot(full, full))) <= 1e-9 * float(np.dot(full, full))
+        ok_red = ok_red and part[1].item() == world * (world + 1) / 2
+        q.put((rank, ok_spmv, ok_red))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg_name", ["7pt", "random"])
+def test_gloo_world2_halo_and_allreduce(cfg_name):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, cfg_name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    got = sorted(q.get(timeout=5) for _ in range(2))
+    assert got == [(0, True, True), (1, True, True)]
+
+
+# ---------------------------------------------------------------------------
+# host-side solver pieces
+# ---------------------------------------------------------------------------
+def test_host_pieces_mirror_reference():
+    import paper_1907_00072_b200 as pg
+    y, res = pg.hessenberg_lsq(np.array([[2.0], [0.0]]), 4.0)
+    assert y == pytest.approx([2.0]) and res == pytest.approx(0.0, abs=1e-15)
+    y, res = pg.hessenberg_lsq(np.array([[1.0], [1.0]]), 1.0)
+    assert y == pytest.approx([0.5]) and res == pytest.approx(1 / np.sqrt(2.0))
+    assert pg.dense_cholesky(pg.GramSystem(np.array([[5.0, 9.0], [9.0, 17.0]]),
+                                           np.array([3.0, 5.0]))) == pytest.approx([1.5, -0.5])
+    with pytest.raises(pg.CholeskyFailure) as err:
+        pg.dense_cholesky(pg.GramSystem(np.ones((2, 2)), np.ones(2)))
+    assert err.value.pivot == 2
+    for bad in (dict(restart_m=0), dict(tol=1.5), dict(tol=0.0), dict(max_iters=0)):
+        with pytest.raises(pg.ParameterError):
+            pg.GmresConfig(**bad)
+    with pytest.raises(pg.ParameterError):
+        pg.PolyCoefficients(1, np.array([1.0]), 1.0)
+    with pytest.raises(pg.ParameterError):
+        pg.PolyCoefficients(0, np.array([np.nan]), 1.0)
+    rep = pg.cost_report(pg.CostCounters(spmvs=5, dots=3), 4, 50)
+    assert rep["spmvs_per_iteration"] == 5 and rep["ca_grouping_spmvs_per_sync"] == 200
+    p = pg.PolyCoefficients(1, np.array([1.5, -0.5]), 1.0)
+    assert pg.lambda_p_lambda(p, [1.0, 2.0]) == pytest.approx([1.0, 1.0])
+
+
+def test_device_path_refuses_without_gpu():
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_1907_00072_b200 as pg
+    with pytest.raises(pg.DeviceError):
+        pg.DeviceMatrixOperator(wl.laplacian2d(4))
