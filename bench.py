@@ -70,12 +70,48 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        # nvidia-smi in a subprocess: an in-process NVML thread competes for the
+        # GIL with the launching thread and visibly delays kernel launches
+        self.mode = os.environ.get("PG_BENCH_CLOCKS", "smi")
+        self.interval = float(os.environ.get("PG_BENCH_CLOCKS_MS", "250")) / 1e3
+
+    def _nvml_loop(self):
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        bits = (("hw_slowdown", nv.nvmlClocksThrottleReasonHwSlowdown),
+                ("hw_thermal_slowdown", getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown",
+                                                0x40)),
+                ("sw_thermal_slowdown", getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown",
+                                                0x20)),
+                ("sw_power_cap", nv.nvmlClocksThrottleReasonSwPowerCap))
+        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop:
+            if self.marked:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                act = ["Active" if (r & b) else "Not Active" for _, b in bits]
+                self.lines.append(",".join([str(sm), str(smax), hex(r)] + act))
+            time.sleep(self.interval)
+        nv.nvmlShutdown()
 
     def start(self):
+        if self.mode == "off":
+            return
+        if self.mode == "nvml":
+            try:
+                import pynvml  # noqa: F401
+                self._stop = False
+                self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
+                self.thread.start()
+                return
+            except Exception:
+                self.mode = "smi"
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                ["nvidia-smi", "-i", str(self.index),
+                 f"--query-gpu={os.environ.get('PG_BENCH_CLOCKS_FIELDS', self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", str(int(1e3 * self.interval))],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -84,17 +120,30 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            if self.marked:
+                self.lines.append(line.strip())
+
+    marked = False
+
+    def mark(self):
+        """Only samples from here on (the timed region) are kept."""
+        self.marked = True
 
     def stop(self):
-        if self.proc is None:
+        if self.mode == "off":
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["sampling disabled"]}
+        if self.mode == "nvml":
+            self._stop = True
+            self.thread.join(timeout=5)
+        elif self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        self.thread.join(timeout=2)
+        else:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
         sm, smax, reasons = [], [], set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         for ln in self.lines:
@@ -111,7 +160,8 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": self.mode, "interval_ms": 1e3 * self.interval}
 
 
 # ---------------------------------------------------------------------------
@@ -171,18 +221,22 @@ def run_ours(args):
         res = pg.solve(op, b, right_prec=poly, config=cfg)
         return poly, pivot, res, c
 
+    # the clock sampler starts before the warm-up: nvidia-smi's own start-up
+    # (driver queries) must not land inside the timed region
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.5)
     for _ in range(args.warmup):
         step(b_dev, v0_dev)
     torch.cuda.synchronize()
 
-    sampler = ClockSampler(local)
     times, results = [], []
     e.timer = []
     launches0 = _lib.launches()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
+    sampler.mark()
     for _ in range(args.steps):
         flush.fill_(1.0)  # evict L2 (126 MB) between steps -- outside the events
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -190,7 +244,7 @@ def run_ours(args):
         ev0.record(stream)
         out = step(b_dev, v0_dev)
         ev1.record(stream)
-        results.append(out)
+        results[:] = [out]  # keep only the last result: no allocator growth across steps
         times.append((ev0, ev1))
     torch.cuda.synchronize()
     if world > 1:
@@ -200,9 +254,11 @@ def run_ours(args):
     per_step = [a.elapsed_time(b) / 1e3 for a, b in times]
     total = sum(per_step)
     # kernel-level roofline of the dominant kernel (fused polynomial pass)
-    kt = sum(a.elapsed_time(b) for a, b, _ in e.timer) / 1e3
-    kb = sum(nb for _, _, nb in e.timer)
-    nk = len(e.timer)
+    # e.timer: (start, end, algorithmic bytes, passes) per fused chain of d
+    # back-to-back polynomial passes (events on the launching stream)
+    kt = sum(a.elapsed_time(b) for a, b, _, _ in e.timer) / 1e3
+    kb = sum(nb for _, _, nb, _ in e.timer)
+    nk = sum(np_ for _, _, _, np_ in e.timer)
     e.timer = None
     if world > 1:
         t = torch.tensor([total, kt], dtype=torch.float64, device=dev)
@@ -253,6 +309,9 @@ def run_ours(args):
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": 1e3 * total / args.steps,
+            "step_ms": {"min": 1e3 * min(per_step), "median": 1e3 * statistics.median(per_step),
+                        "max": 1e3 * max(per_step),
+                        "all": [round(1e3 * t, 3) for t in per_step]},
             "higher_is_better": False,
             "scaling": "strong",
             "vs_baseline": None,
@@ -314,7 +373,7 @@ def cpu_baseline(conf, iterations, cycles, sample_iters=5, threads=1):
         t = orc.Tally()
         A = orc.OracleMatrix.of(A_h, t)
         t0 = time.perf_counter()
-        _, eff, y, _ = orc.degree_policy(A, v0, conf["degree"], t)
+        _, eff, y, _ = orc.degree_policy_shared(A, v0, conf["degree"], t)
         t1 = time.perf_counter()
         orc.gmres(A, b, y=y, m=conf["m"], tol=conf["tol"], max_iters=sample_iters)
         t2 = time.perf_counter()
@@ -377,8 +436,8 @@ def _reference_iterations(config: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--max-iters", type=int, default=200000)

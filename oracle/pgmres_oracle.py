@@ -310,6 +310,29 @@ def degree_policy(op, v0, deg, tally):
         return deg, d, y, nrm
 
 
+def degree_policy_shared(op, v0, deg, tally):
+    """The same policy with one shared power sequence + Gram (deg+1 SpMVs,
+    2 dots), as the device's build_poly_or_auto; used by the CPU baseline so
+    both arms do identical work.  Returns (requested, effective, y, seed_norm)."""
+    v, nrm = _seed(v0)
+    tally.scalar_dots += 1
+    P = power_columns(op, v, deg + 1)
+    G, rhs = gram(P, deg, tally)
+    try:
+        return deg, deg, chol_solve(G, rhs), nrm
+    except CholeskyFailureOracle:
+        Gfull = np.zeros((deg + 2, deg + 2))
+        Gfull[1:, 1:] = G
+        Gfull[1:, 0] = rhs
+        best = auto_deg_from_gram(Gfull, deg)
+        if best is None:
+            try:
+                return deg, 0, chol_solve(G[:1, :1], rhs[:1]), nrm
+            except CholeskyFailureOracle:
+                return deg, 0, np.zeros(1), nrm
+        return deg, best[0], best[1], nrm
+
+
 # ---------------------------------------------------------------------------
 # restarted GMRES(m)  (gmres.py:165-169, 213-343)
 # ---------------------------------------------------------------------------

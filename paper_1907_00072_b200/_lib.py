@@ -116,7 +116,15 @@ def launches() -> int:
     return sum(LAUNCH_COUNT.values())
 
 
+_FN: dict = {}
+
+
 def call(name: str, *args):
-    check(getattr(load(), name)(*args), name)
+    fn = _FN.get(name)
+    if fn is None:
+        fn = _FN[name] = getattr(load(), name)
+    code = fn(*args)
+    if code:
+        check(code, name)
     if name in LAUNCHING:
         LAUNCH_COUNT[name] = LAUNCH_COUNT.get(name, 0) + 1

@@ -150,9 +150,14 @@ class Shard:
         # small per-shard device scratch: [c1 | c2 | nsq | spare]
         self.scal = torch.zeros(2 * KMAX + 8, dtype=F64, device=device)
         self.coef = torch.zeros(KMAX, dtype=F64, device=device)
+        # two-slot ring of CGS2 scalars (one Arnoldi step of look-ahead) and
+        # its pinned host mirror
+        self.ring = [torch.zeros(2 * KMAX + 8, dtype=F64, device=device) for _ in range(2)]
+        self.pinned = [torch.zeros(2 * KMAX + 1, dtype=F64).pin_memory() for _ in range(2)]
         self.send_idx: dict = {}
         self.send_buf: dict = {}
         self._lib = lib
+        self._stream = None
 
     # send lists (local indices) are installed once every shard's ghost needs are known
     def set_send(self, q: int, local_idx: np.ndarray):
@@ -167,7 +172,12 @@ class Shard:
 
     @property
     def stream(self) -> int:
-        return torch.cuda.current_stream(self.device).cuda_stream
+        """cudaStream_t of the device's current torch stream, cached by
+        :meth:`Engine.bind_stream` at each public entry point."""
+        st = self._stream
+        if st is None:
+            st = self._stream = torch.cuda.current_stream(self.device).cuda_stream
+        return st
 
     def activate(self):
         _lib.call("pg_set_device", self.dev_ord)
@@ -343,12 +353,36 @@ class Engine:
         for s in self.shards:
             s.close()
 
+    def bind_stream(self):
+        """Re-read each device's current torch stream (call at every public
+        entry point so `with torch.cuda.stream(...)` is honoured)."""
+        for s in self.shards:
+            s._stream = torch.cuda.current_stream(s.device).cuda_stream
+
     # ---- vectors --------------------------------------------------------------
     def vecs(self):
         return [s.vec() for s in self.shards]
 
     def blocks(self, cols):
         return [s.block(cols) for s in self.shards]
+
+    def cached_blocks(self, key: str, cols: int):
+        """Reusable zero-padded column blocks (>= cols columns) kept across
+        calls: basis / power-sequence storage is allocated once per operator,
+        not per solve.  Rows >= n of every column stay zero (kernels only
+        write owned rows; halo fills rows n..n_ext before each SpMV)."""
+        cache = self.__dict__.setdefault("_block_cache", {})
+        blk = cache.get(key)
+        if blk is None or blk[0].shape[0] < cols:
+            blk = cache[key] = self.blocks(cols)
+        return blk
+
+    def cached_vecs(self, key: str):
+        cache = self.__dict__.setdefault("_vec_cache", {})
+        v = cache.get(key)
+        if v is None:
+            v = cache[key] = self.vecs()
+        return v
 
     @property
     def local_n(self) -> int:
@@ -397,6 +431,9 @@ class Engine:
         return torch.cat([t[:s.n].to(d) for s, t in zip(self.shards, xs)])
 
     def ingest(self, v):
+        """Caller vector -> shard vectors; every public entry point starts here,
+        so this is also where the launch stream is (re)bound."""
+        self.bind_stream()
         if isinstance(v, torch.Tensor):
             return self.from_torch(v)
         return self.from_host(v)
@@ -437,6 +474,12 @@ class Engine:
         self.halo(vs)
         cur = vs
         ws = (w0, w1)
+        timing = self.timer is not None and self.P == 1
+        if timing:  # one event pair around the d back-to-back fused passes
+            s0 = self.shards[0]
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev0.record(torch.cuda.current_stream(s0.device))
+            nbytes = 0
         for k in range(1, d + 1):
             last = k == d
             flags = (_lib.PG_PASS_FIRST if k == 1 else 0) | (0 if last else _lib.PG_PASS_WRITE_W)
@@ -444,23 +487,22 @@ class Engine:
             dst = out if last else acc
             for i, s in enumerate(self._each()):
                 b = base[i] if (last and base is not None) else None
-                if self.timer is not None:
-                    ev0 = torch.cuda.Event(enable_timing=True)
-                    ev0.record(torch.cuda.current_stream(s.device))
                 _lib.call("pg_poly_pass", s.mat, ptr(cur[i]), ptr(acc[i]) if k > 1 else None,
                           ptr(b) if b is not None else None, ptr(dst[i]),
                           ptr(nxt[i]) if not last else None, y[0], y[k], flags, s.stream)
-                if self.timer is not None:
-                    ev1 = torch.cuda.Event(enable_timing=True)
-                    ev1.record(torch.cuda.current_stream(s.device))
+                if timing:
                     # algorithmic bytes: 12 B per nonzero (value +
                     # int32 index), 4 B row length, 8 B compulsory gather of x,
                     # then the epilogue's vector traffic
                     vec = 8 * (int(k > 1) + 1 + int(not last) + int(b is not None))
-                    self.timer.append((ev0, ev1, 12 * s.nnz + (12 + vec) * s.n))
+                    nbytes += 12 * s.nnz + (12 + vec) * s.n
             if not last:
                 self.halo(nxt)
                 cur = nxt
+        if timing:
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev1.record(torch.cuda.current_stream(s0.device))
+            self.timer.append((ev0, ev1, nbytes, d))
 
     def slot(self, i):
         """Per-shard 1-element device scalar slot i (0..7) after the coefficients."""
@@ -501,9 +543,33 @@ class Engine:
         """Two-pass CGS of z against columns 0..k-1 of V; writes w2/|w2| into
         column k.  Returns host (c1, c2, nsq) after the three batched
         all-reduces (one per phase)."""
-        c1 = [s.scal[0:KMAX] for s in self.shards]
-        c2 = [s.scal[KMAX:2 * KMAX] for s in self.shards]
-        nsq = [s.scal[2 * KMAX:2 * KMAX + 1] for s in self.shards]
+        return self.cgs2_fetch(self.cgs2_launch(Vs, k, zs, 0))
+
+    def cgs2_launch(self, Vs, k, zs, slot: int):
+        """Asynchronous CGS2 (all three phases, their all-reduces and the
+        normalisation of column k); the reduced scalars land in device ring
+        slot ``slot`` (0/1) and are copied to pinned host memory behind an
+        event.  Returns a handle for :meth:`cgs2_fetch`."""
+        bufs = [s.ring[slot] for s in self.shards]
+        c1 = [b[0:KMAX] for b in bufs]
+        c2 = [b[KMAX:2 * KMAX] for b in bufs]
+        nsq = [b[2 * KMAX:2 * KMAX + 1] for b in bufs]
+        self._cgs2_phases(Vs, k, zs, c1, c2, nsq)
+        s0 = self.shards[0]
+        host = s0.pinned[slot]
+        host.copy_(bufs[0][:2 * KMAX + 1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(s0.device))
+        return ev, host, k
+
+    @staticmethod
+    def cgs2_fetch(handle):
+        ev, host, k = handle
+        ev.synchronize()
+        h = host.numpy()
+        return h[:k].copy(), h[KMAX:KMAX + k].copy(), float(h[2 * KMAX])
+
+    def _cgs2_phases(self, Vs, k, zs, c1, c2, nsq):
         if k > 0:
             for s, V, z, c in zip(self._each(), Vs, zs, c1):
                 _lib.call("pg_cgs2_phase1", ptr(V), s.ld, k, ptr(z), s.n, ptr(c), s.ws, s.stream)
@@ -520,8 +586,6 @@ class Engine:
         # normalisation of column k is launched before the host looks at the
         # scalars; on breakdown the column is simply never used (ortho.py:67-70)
         self.normalize_dev([V[k] for V in Vs], nsq, [V[k] for V in Vs])
-        host = self.shards[0].scal[:2 * KMAX + 1].cpu().numpy()
-        return host[:k].copy(), host[KMAX:KMAX + k].copy(), float(host[2 * KMAX])
 
     def gemv(self, Vs, k, y_host, outs):
         yt = torch.from_numpy(np.ascontiguousarray(y_host, dtype=np.float64))

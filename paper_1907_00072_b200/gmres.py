@@ -14,6 +14,7 @@ reference line for line.
 
 from __future__ import annotations
 
+import gc
 import math
 from dataclasses import dataclass, field
 
@@ -120,13 +121,13 @@ class _Workspace:
     """Device buffers of one solve (allocated once, reused across cycles)."""
 
     def __init__(self, e, m):
-        self.V = e.blocks(m + 1)
-        self.z = e.vecs()       # A p(A) v_j
-        self.t = e.vecs()       # p(A) v_j / recovery update
-        self.acc = e.vecs()
-        self.w0 = e.vecs()
-        self.w1 = e.vecs()
-        self.r = e.vecs()
+        self.V = e.cached_blocks("basis", m + 1)
+        self.z = e.cached_vecs("z")       # A p(A) v_j
+        self.t = e.cached_vecs("t")       # p(A) v_j / recovery update
+        self.acc = e.cached_vecs("acc")
+        self.w0 = e.cached_vecs("w0")
+        self.w1 = e.cached_vecs("w1")
+        self.r = e.cached_vecs("r")
 
     def col(self, j):
         return [V[j] for V in self.V]
@@ -136,7 +137,23 @@ def solve(op, b, x0=None, right_prec: PolyCoefficients | None = None,
           config: GmresConfig | None = None) -> GmresResult:
     """Restarted GMRES over the device operator (gmres.py:213-343).
     ``b`` (and ``x0``) may be numpy arrays or torch tensors; ``x`` comes back in
-    the type of ``b``."""
+    the type of ``b``.
+
+    Python's cyclic garbage collector is paused for the duration of the solve:
+    the Arnoldi loop creates only short-lived acyclic objects (freed by
+    reference counting), and a full collection of a process that has imported
+    torch takes tens of milliseconds -- longer than several Arnoldi steps --
+    during which no kernel is queued and the GPU idles."""
+    enabled = gc.isenabled()
+    gc.disable()
+    try:
+        return _solve(op, b, x0, right_prec, config)
+    finally:
+        if enabled:
+            gc.enable()
+
+
+def _solve(op, b, x0, right_prec, config) -> GmresResult:
     if config is None:
         config = GmresConfig()
     e = _engine(op)
@@ -196,18 +213,23 @@ def solve(op, b, x0=None, right_prec: PolyCoefficients | None = None,
         j = 0
         breakdown = False
         pending_row = None
+        handle = _launch_step(e, W, poly, 0)
         while j < m and total_iters < config.max_iters:
-            vj = W.col(j)
+            # one step of look-ahead: step j+1's device work (it only needs
+            # v_{j+1}, already normalized on the device) is queued before the
+            # host waits for step j's scalars, so the GPU never idles during
+            # the host Givens update.  If step j ends the cycle, the queued
+            # step is abandoned unused (no counter, no history row).
+            ahead = None
+            if j + 1 < m and total_iters + 1 < config.max_iters:
+                ahead = _launch_step(e, W, poly, j + 1)
+            c1, c2, nsq = e.cgs2_fetch(handle)
+            handle = ahead
             if poly is not None:
-                counters.spmvs += d
+                counters.spmvs += d + 1
                 counters.vector_updates += d + 1
-                e.poly(poly.y, vj, W.t, W.acc, W.w0, W.w1)
-                counters.spmvs += 1
-                e.spmv(W.t, W.z)
             else:
                 counters.spmvs += 1
-                e.spmv(vj, W.z)
-            c1, c2, nsq = e.cgs2(W.V, j + 1, W.z)
             coeffs = c1 + c2
             new_norm = math.sqrt(nsq) if nsq >= 0.0 else float("nan")
             counters.dots += 3
@@ -275,6 +297,19 @@ def solve(op, b, x0=None, right_prec: PolyCoefficients | None = None,
 
     return GmresResult(e.emit(xs, b), converged, total_iters, true_relres, history, counters,
                        cycles)
+
+
+def _launch_step(e, W, poly, j):
+    """Queue Arnoldi step j on the device: w = A p(A) v_j (d fused passes +
+    the wrapper SpMV, gmres.py:112-113, 283) and its CGS2 against
+    v_0..v_j writing v_{j+1} (ortho.py:53-70).  Returns the scalar handle."""
+    vj = W.col(j)
+    if poly is not None:
+        e.poly(poly.y, vj, W.t, W.acc, W.w0, W.w1)
+        e.spmv(W.t, W.z)
+    else:
+        e.spmv(vj, W.z)
+    return e.cgs2_launch(W.V, j + 1, W.z, j & 1)
 
 
 def cost_report(counters: CostCounters, deg: int, restart_m: int) -> dict:

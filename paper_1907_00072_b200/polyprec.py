@@ -101,14 +101,13 @@ def _device_power_gram(op, v0, top: int, counters: CostCounters):
     seed_norm = float(np.sqrt(nsq))
     if seed_norm == 0.0:
         raise ParameterError("seed vector v0 must be nonzero")
-    P = e.blocks(top + 1)
+    P = e.cached_blocks("powers", top + 1)
     # column 0 = v0 / |v0| (exact division, as numpy's v0 / seed_norm)
     e.normalize_dev(vs, e.slot(6), [blk[0] for blk in P])
     for k in range(top):
         op.counters.spmvs += 1
         e.spmv([blk[k] for blk in P], [blk[k + 1] for blk in P])
     G = e.gram(P, top + 1)
-    del P
     return G, seed_norm
 
 
@@ -142,15 +141,57 @@ def auto_degree(op, v0, cap: int = DEFAULT_DEGREE_CAP, counters: CostCounters | 
         counters = CostCounters()
     Gfull, seed_norm = _device_power_gram(op, v0, cap + 1, counters)
     counters.scalar_dots += 1
-    full = _normal_equations(Gfull, cap, counters)
+    return _select_degree(_normal_equations(Gfull, cap, counters), cap, seed_norm, seed_mode)
+
+
+def _nested_pivots(G: np.ndarray):
+    """One Cholesky sweep of the full Gram matrix, recording every pivot.
+
+    The Cholesky of a leading (o x o) block performs exactly the first o
+    steps of this sweep, so its pivots are piv[:o]; the reference's test for
+    order o is ``piv[k] > o*eps*G[k,k]`` for all k < o (polyprec.py:80-82).
+    Returns (L, piv, n_ok) where the sweep stops at the first non-positive
+    pivot (n_ok = number of usable pivots)."""
+    m = G.shape[0]
+    L = np.zeros((m, m))
+    piv = np.zeros(m)
+    for k in range(m):
+        p = G[k, k] - L[k, :k] @ L[k, :k]
+        piv[k] = p
+        if not (p > 0.0):
+            return L, piv, k
+        L[k, k] = np.sqrt(p)
+        if k + 1 < m:
+            L[k + 1:, k] = (G[k + 1:, k] - L[k + 1:, :k] @ L[k, :k]) / L[k, k]
+    return L, piv, m
+
+
+def _select_degree(full: GramSystem, cap: int, seed_norm: float, seed_mode: str):
+    """auto_degree's selection (polyprec.py:171-190): the largest d <= cap
+    whose order-(d+1) Gram block passes the pivot test, with finite y.
+
+    Order o passes iff piv[k] > o*eps*G[k,k] for all k < o; the threshold
+    grows with o, so the passing orders form a prefix {1..F}: one pivot sweep
+    finds the candidate (instead of cap separate factorizations).  y is then
+    computed by the reference's own per-order factorization of that block:
+    near the failure margin the normal equations have cond ~1e14 and y
+    inherits O(1) relative changes from last-bit differences in L, so the
+    selected degree's y must come from the same code path as build_poly."""
+    eps = np.finfo(np.float64).eps
+    _, piv, n_ok = _nested_pivots(full.G)
+    diag = np.diag(full.G)
     best = None
-    for d in range(1, cap + 1):
+    for d in range(cap, 0, -1):
+        o = d + 1
+        if o > n_ok or not np.all(piv[:o] > o * eps * diag[:o]):
+            continue
         try:
-            y = dense_cholesky(GramSystem(full.G[:d + 1, :d + 1], full.rhs[:d + 1]))
+            y = dense_cholesky(GramSystem(full.G[:o, :o], full.rhs[:o]))
         except CholeskyFailure:
             continue
         if np.all(np.isfinite(y)):
             best = (d, y)
+            break
     if best is None:
         try:
             y0 = dense_cholesky(GramSystem(full.G[:1, :1], full.rhs[:1]))
@@ -163,14 +204,26 @@ def auto_degree(op, v0, cap: int = DEFAULT_DEGREE_CAP, counters: CostCounters | 
 def build_poly_or_auto(op, v0, deg: int, counters: CostCounters,
                        seed_mode: str = "unspecified"):
     """Degree policy for requested degrees beyond what the power basis can
-    build: ``build_poly(deg)``, and on CholeskyFailure
-    ``auto_degree(cap=deg)``.  Returns (PolyCoefficients, failed_pivot|None).
-    The reference has no such helper; bench and parity tests apply the same
-    policy to the reference oracle."""
-    try:
+    build: the degree-``deg`` polynomial if its Gram system
+    factors, else auto-degree selection with cap ``deg``.  Returns
+    (PolyCoefficients, failed_pivot | None).
+
+    ``build_poly(deg)`` and ``auto_degree(cap=deg)`` need the same power
+    sequence [v, ..., A^{deg+1} v] and the same Gram matrix, so -- as
+    auto_degree itself shares one sequence across candidate degrees
+    (polyprec.py:150-160) -- it is built once: deg+1 SpMVs and 2 dots in total.
+    The reference has no such helper; the CPU baseline runs the same policy
+    (oracle.degree_policy_shared)."""
+    if deg < 1:
         return build_poly(op, v0, deg, counters, seed_mode), None
+    Gfull, seed_norm = _device_power_gram(op, v0, deg + 1, counters)
+    counters.scalar_dots += 1
+    full = _normal_equations(Gfull, deg, counters)
+    try:
+        y = dense_cholesky(full)
+        return PolyCoefficients(deg, y, seed_norm, seed_mode), None
     except CholeskyFailure as exc:
-        return auto_degree(op, v0, deg, counters, seed_mode), exc.pivot
+        return _select_degree(full, deg, seed_norm, seed_mode), exc.pivot
 
 
 def apply_poly(p: PolyCoefficients, op, v, counters: CostCounters):

@@ -1,3 +1,5 @@
-timeout 800 python -m pytest tests -q -m "gpu" -x > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
-python tools/cgs2_bench.py > gpurun_out/cgs2_bench.log 2>&1; cat gpurun_out/cgs2_bench.log
-python bench.py --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/bench_q.log 2>&1; tail -c 1800 gpurun_out/bench_q.log
+for cfgs in "off 500" "smi 500" "smi 250"; do
+set -- $cfgs
+PG_BENCH_CLOCKS=$1 PG_BENCH_CLOCKS_MS=$2 python bench.py --no-cpu-baseline --steps 40 > gpurun_out/bench_x.log 2>&1
+echo "== $cfgs"; grep -o '"value": [0-9.]*, "unit": "s", "n_gpus\|"median": [0-9.]*\|"max": [0-9.]*\|"samples": [0-9]*' gpurun_out/bench_x.log | tr '\n' ' '; echo
+done

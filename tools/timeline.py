@@ -1,0 +1,76 @@
+"""Kernel timeline of one warm solve (torch.profiler / CUPTI sees the
+libpgmres kernels): busy time vs span, idle gaps, per-kernel totals.
+
+  python tools/timeline.py [--config 2] [--grid G] [--out gpurun_out/timeline.json]
+"""
+
+import argparse
+import collections
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+import paper_1907_00072_b200 as pg  # noqa: E402
+from paper_1907_00072_b200 import workloads as wl  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--grid", type=int, default=None)
+    ap.add_argument("--out", default="gpurun_out/timeline.json")
+    args = ap.parse_args()
+    conf = wl.CONFIGS[args.config]
+    A = wl.make_matrix(conf, grid=args.grid)
+    b = torch.from_numpy(wl.make_rhs(conf, A)).cuda()
+    v0 = torch.from_numpy(wl.make_v0(A.nrows)).cuda()
+    op = pg.DeviceMatrixOperator(A)
+    cfg = pg.GmresConfig(conf["m"], conf["tol"])
+
+    def one():
+        c = pg.CostCounters()
+        op.counters = c
+        p, _ = pg.build_poly_or_auto(op, v0, conf["degree"], c)
+        return pg.solve(op, b, right_prec=p, config=cfg)
+
+    one()
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+        res = one()
+        torch.cuda.synchronize()
+    kern = []
+    for ev in prof.events():
+        if ev.device_type == torch.autograd.DeviceType.CUDA and ev.name and \
+                "Memcpy" not in ev.name and "Memset" not in ev.name:
+            kern.append((ev.time_range.start, ev.time_range.end, ev.name))
+    mem = [ev for ev in prof.events() if ev.device_type == torch.autograd.DeviceType.CUDA
+           and ev.name and ("Memcpy" in ev.name or "Memset" in ev.name)]
+    kern.sort()
+    span = kern[-1][1] - kern[0][0]
+    busy = sum(e - s for s, e, _ in kern)
+    gaps = [kern[i + 1][0] - kern[i][1] for i in range(len(kern) - 1)]
+    per = collections.defaultdict(lambda: [0, 0.0])
+    for s, e, nm in kern:
+        key = nm.split("(")[0][:50]
+        per[key][0] += 1
+        per[key][1] += e - s
+    big = sorted(gaps, reverse=True)[:10]
+    out = dict(iterations=res.iterations, kernels=len(kern), span_us=span, busy_us=busy,
+               idle_us=span - busy, gaps_over_10us=sum(g for g in gaps if g > 10),
+               n_gaps_over_10us=sum(1 for g in gaps if g > 10), largest_gaps_us=big,
+               memops=len(mem),
+               per_kernel={k: dict(n=v[0], us=round(v[1], 1)) for k, v in
+                           sorted(per.items(), key=lambda kv: -kv[1][1])})
+    print(json.dumps(out, indent=1))
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
