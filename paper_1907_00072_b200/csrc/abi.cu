@@ -237,6 +237,13 @@ PG_API int pg_matrix_create(int device, int64_t nrows, int64_t ncols, const int6
       // one-row-per-thread kernel (all index/value loads issued before the
       // gathers) reaches a higher fraction of HBM
       m->use_tma = std::getenv("PG_SPMV_TMA") != nullptr;
+      // L2 evict_last policy on the matrix stream (opt-in, PG_SPMV_L2KEEP=1):
+      // measured slower on config 2 (the pinned lines crowd out the x gathers
+      // and vectors), so streaming evict_first loads are the default
+      {
+        const char* kv = std::getenv("PG_SPMV_L2KEEP");
+        m->l2_keep = kv ? (std::atoi(kv) != 0) : 0;
+      }
       int64_t acc = 0;
       for (int64_t s = 0; s < h.n_slices; ++s) {
         const int64_t ne = h.slice_ptr[s + 1] - h.slice_ptr[s];

@@ -67,6 +67,7 @@ struct pg_matrix {
   int32_t* unit_slice; // [n_units+1] first slice of each TMA streaming unit
   int64_t n_units;
   bool use_tma;        // every slice fits a ring stage (kUnitEntries)
+  int l2_keep;         // matrix loads carry an L2 evict_last policy
   size_t bytes;
 };
 

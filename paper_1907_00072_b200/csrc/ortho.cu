@@ -15,6 +15,8 @@
 // 16-byte cp.async copies, double buffered, so the next tile's HBM reads are
 // in flight while the current tile is reduced.
 
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace pg {
@@ -290,6 +292,182 @@ __global__ void __launch_bounds__(kRowThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-chunk CGS2 kernels (the default path).  A warp owns chunks of
+// kChunkRows = 32 * kR consecutive rows, lane l holding rows l, l+32, ...;
+// every column read is a coalesced 256 B segment and kCol columns x kR rows
+// of loads are issued before they are consumed.  No shared-memory staging,
+// small register footprint -> full occupancy, which is what an HBM-latency
+// bound kernel needs.  Column dots are reduced across the warp with a fixed
+// xor tree per chunk; lane (i mod 32) keeps column i's running sum.
+// ---------------------------------------------------------------------------
+constexpr int kR = 4;
+constexpr int kChunkRows = 32 * kR;
+constexpr int kCol = 4;
+constexpr int kChunkThreads = 256;
+
+struct ChunkRows {
+  int64_t r[kR];
+  bool ok[kR];
+};
+
+__device__ __forceinline__ ChunkRows chunk_rows(int64_t chunk, int lane, int64_t n) {
+  ChunkRows c;
+#pragma unroll
+  for (int q = 0; q < kR; ++q) {
+    c.r[q] = chunk * kChunkRows + lane + 32 * q;
+    c.ok[q] = c.r[q] < n;
+  }
+  return c;
+}
+
+// t[q] = sum_i V[r_q, i] * c[i] in sequential i order (FMA) -- the same order
+// as row_proj, so phase 2 and phase 3 recompute bit-identical w1.
+__device__ __forceinline__ void chunk_proj(const double* __restrict__ V, int64_t ld, int k,
+                                           const ChunkRows& cr, const double* c, double* t) {
+#pragma unroll
+  for (int q = 0; q < kR; ++q) t[q] = 0.0;
+  int i = 0;
+  for (; i + kCol <= k; i += kCol) {
+    double v[kCol][kR];
+#pragma unroll
+    for (int u = 0; u < kCol; ++u)
+#pragma unroll
+      for (int q = 0; q < kR; ++q)
+        v[u][q] = cr.ok[q] ? __ldg(V + (int64_t)(i + u) * ld + cr.r[q]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kCol; ++u)
+#pragma unroll
+      for (int q = 0; q < kR; ++q) t[q] = __fma_rn(v[u][q], c[i + u], t[q]);
+  }
+  for (; i < k; ++i)
+#pragma unroll
+    for (int q = 0; q < kR; ++q)
+      t[q] = __fma_rn(cr.ok[q] ? __ldg(V + (int64_t)i * ld + cr.r[q]) : 0.0, c[i], t[q]);
+}
+
+template <int MODE>  // 1: c = V^T z;  2: w1 = z - V c1 (row-local), c = V^T w1
+__global__ void __launch_bounds__(kChunkThreads)
+    chunk_dots_kernel(const double* __restrict__ V, int64_t ld, int k,
+                      const double* __restrict__ z, int64_t n, const double* __restrict__ c1,
+                      double* partials, unsigned int* counter, double* out) {
+  __shared__ double cs[PG_KMAX];
+  __shared__ double wsum[kChunkThreads / 32][PG_KMAX];
+  if (MODE == 2)
+    for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = c1[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+  const int64_t nw = (int64_t)gridDim.x * (kChunkThreads / 32);
+  double acc0 = 0.0, acc1 = 0.0;  // columns lane and lane + 32
+  for (int64_t ch = (int64_t)blockIdx.x * (kChunkThreads / 32) + warp; ch < nchunks; ch += nw) {
+    const ChunkRows cr = chunk_rows(ch, lane, n);
+    double w[kR];
+#pragma unroll
+    for (int q = 0; q < kR; ++q) w[q] = cr.ok[q] ? z[cr.r[q]] : 0.0;
+    if (MODE == 2) {
+      double t[kR];
+      chunk_proj(V, ld, k, cr, cs, t);
+#pragma unroll
+      for (int q = 0; q < kR; ++q) w[q] = __dsub_rn(w[q], t[q]);
+    }
+    int i = 0;
+    for (; i < k; i += kCol) {
+      double p[kCol];
+#pragma unroll
+      for (int u = 0; u < kCol; ++u) {
+        p[u] = 0.0;
+        if (i + u < k) {
+#pragma unroll
+          for (int q = 0; q < kR; ++q)
+            p[u] = __fma_rn(cr.ok[q] ? __ldg(V + (int64_t)(i + u) * ld + cr.r[q]) : 0.0, w[q],
+                            p[u]);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < kCol; ++u) p[u] += __shfl_xor_sync(0xffffffffu, p[u], o);
+#pragma unroll
+      for (int u = 0; u < kCol; ++u) {
+        const int col = i + u;
+        if (col < k && lane == (col & 31)) {
+          if (col < 32) acc0 += p[u];
+          else acc1 += p[u];
+        }
+      }
+    }
+  }
+  if (lane < k) wsum[warp][lane] = acc0;
+  if (lane + 32 < k) wsum[warp][lane + 32] = acc1;
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kChunkThreads / 32; ++w) s += wsum[w][i];
+    partials[(size_t)blockIdx.x * k + i] = s;
+  }
+  last_block_reduce(partials, counter, k, out);
+}
+
+// phase 3: w2 = (z - V c1) - V c2 -> out, sum w2^2 -> nsq
+__global__ void __launch_bounds__(kChunkThreads)
+    chunk_update_kernel(const double* __restrict__ V, int64_t ld, int k,
+                        const double* __restrict__ z, int64_t n, const double* __restrict__ c1,
+                        const double* __restrict__ c2, double* __restrict__ out,
+                        double* partials, unsigned int* counter, double* nsq) {
+  __shared__ double cs1[PG_KMAX], cs2[PG_KMAX];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    cs1[i] = c1[i];
+    cs2[i] = c2[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+  const int64_t nw = (int64_t)gridDim.x * (kChunkThreads / 32);
+  double local = 0.0;
+  for (int64_t ch = (int64_t)blockIdx.x * (kChunkThreads / 32) + warp; ch < nchunks; ch += nw) {
+    const ChunkRows cr = chunk_rows(ch, lane, n);
+    double t1[kR], t2[kR];
+#pragma unroll
+    for (int q = 0; q < kR; ++q) t1[q] = t2[q] = 0.0;
+    int i = 0;
+    for (; i + kCol <= k; i += kCol) {
+      double v[kCol][kR];
+#pragma unroll
+      for (int u = 0; u < kCol; ++u)
+#pragma unroll
+        for (int q = 0; q < kR; ++q)
+          v[u][q] = cr.ok[q] ? __ldcs(V + (int64_t)(i + u) * ld + cr.r[q]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kCol; ++u)
+#pragma unroll
+        for (int q = 0; q < kR; ++q) {
+          t1[q] = __fma_rn(v[u][q], cs1[i + u], t1[q]);
+          t2[q] = __fma_rn(v[u][q], cs2[i + u], t2[q]);
+        }
+    }
+    for (; i < k; ++i)
+#pragma unroll
+      for (int q = 0; q < kR; ++q) {
+        const double v = cr.ok[q] ? __ldcs(V + (int64_t)i * ld + cr.r[q]) : 0.0;
+        t1[q] = __fma_rn(v, cs1[i], t1[q]);
+        t2[q] = __fma_rn(v, cs2[i], t2[q]);
+      }
+#pragma unroll
+    for (int q = 0; q < kR; ++q) {
+      if (cr.ok[q]) {
+        const double w2 = __dsub_rn(__dsub_rn(z[cr.r[q]], t1[q]), t2[q]);
+        out[cr.r[q]] = w2;
+        local = __fma_rn(w2, w2, local);
+      }
+    }
+  }
+  const double s = block_sum(local);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  last_block_reduce(partials, counter, 1, nsq);
+}
+
 __global__ void dot_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                            double* partials, unsigned int* counter, double* out) {
   double local = 0.0;
@@ -355,6 +533,47 @@ static size_t tile_smem(int mode, int k) {
   return b;
 }
 
+// Resident-grid size for a chunk kernel (cached per kernel and device),
+// limited by the work: one warp per 128-row chunk at most.
+static int chunk_grid(const void* kernel, int slot, int dev, int64_t n) {
+  static int cache[4][64] = {};
+  PG_REQUIRE(dev >= 0 && dev < 64, PG_ERR_PARAMETER, "device ordinal out of range");
+  int g = cache[slot][dev];
+  if (g == 0) g = cache[slot][dev] = grid_for(dev, kernel, kChunkThreads, 0, int64_t(1) << 40);
+  const int64_t need = ((n + kChunkRows - 1) / kChunkRows + 7) / 8;
+  if (need < g) g = (int)(need < 1 ? 1 : need);
+  return g;
+}
+
+// Kernel choice per basis width (tools/cgs2_bench.py on B200): the warp-chunk
+// kernels win while the basis is narrow (k <= 12: fixed launch / reduction
+// costs dominate and their full occupancy hides them); past that the
+// shared-memory tile kernels (phases 1-2) and the row-streaming phase 3 reach
+// a higher fraction of HBM.  PG_CGS2_TILE=1 / PG_CGS2_CHUNK_KMAX override.
+static bool use_tile_cgs2(int k) {
+  static int force_tile = -1, chunk_kmax = -1;
+  if (force_tile < 0) {
+    force_tile = std::getenv("PG_CGS2_TILE") != nullptr;
+    const char* s = std::getenv("PG_CGS2_CHUNK_KMAX");
+    chunk_kmax = s ? std::atoi(s) : 12;
+  }
+  return force_tile == 1 || k > chunk_kmax;
+}
+
+template <int MODE>
+static void launch_chunk_dots(const double* V, int64_t ld, int k, const double* z, int64_t n,
+                              const double* c1, double* out, pg_workspace* ws, cudaStream_t st) {
+  check_ws(ws);
+  if (n == 0) {
+    PG_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * k, st));
+    return;
+  }
+  const int g = chunk_grid((const void*)chunk_dots_kernel<MODE>, MODE, ws->device, n);
+  chunk_dots_kernel<MODE><<<g, kChunkThreads, 0, st>>>(V, ld, k, z, n, c1, ws->partials,
+                                                       ws->counter, out);
+  check_launch();
+}
+
 template <int MODE>
 static void launch_tile(const double* V, int64_t ld, int k, const double* z, int64_t n,
                         const double* c1, double* out, pg_workspace* ws, cudaStream_t st) {
@@ -408,7 +627,10 @@ PG_API int pg_cgs2_phase1(const double* d_V, int64_t ld, int k, const double* d_
   return guard([&] {
     check_tall(d_V, ld, k, n, 1);
     PG_REQUIRE(d_z && d_c1, PG_ERR_PARAMETER, "null argument");
-    launch_tile<kDots>(d_V, ld, k, d_z, n, nullptr, d_c1, ws, as_stream(stream));
+    if (use_tile_cgs2(k))
+      launch_tile<kDots>(d_V, ld, k, d_z, n, nullptr, d_c1, ws, as_stream(stream));
+    else
+      launch_chunk_dots<1>(d_V, ld, k, d_z, n, nullptr, d_c1, ws, as_stream(stream));
   });
 }
 
@@ -417,7 +639,10 @@ PG_API int pg_cgs2_phase2(const double* d_V, int64_t ld, int k, const double* d_
   return guard([&] {
     check_tall(d_V, ld, k, n, 1);
     PG_REQUIRE(d_z && d_c1 && d_c2, PG_ERR_PARAMETER, "null argument");
-    launch_tile<kUpdDots>(d_V, ld, k, d_z, n, d_c1, d_c2, ws, as_stream(stream));
+    if (use_tile_cgs2(k))
+      launch_tile<kUpdDots>(d_V, ld, k, d_z, n, d_c1, d_c2, ws, as_stream(stream));
+    else
+      launch_chunk_dots<2>(d_V, ld, k, d_z, n, d_c1, d_c2, ws, as_stream(stream));
   });
 }
 
@@ -434,9 +659,15 @@ PG_API int pg_cgs2_phase3(const double* d_V, int64_t ld, int k, const double* d_
       PG_CUDA(cudaMemsetAsync(d_nsq, 0, sizeof(double), st));
       return;
     }
-    const int g = simple_grid(n, kRowThreads, ws);
-    rows_kernel<true><<<g, kRowThreads, 0, st>>>(d_V, ld, k, d_z, n, d_c1, d_c2, d_w2,
-                                                  ws->partials, ws->counter, d_nsq);
+    if (use_tile_cgs2(k)) {
+      const int g = simple_grid(n, kRowThreads, ws);
+      rows_kernel<true><<<g, kRowThreads, 0, st>>>(d_V, ld, k, d_z, n, d_c1, d_c2, d_w2,
+                                                    ws->partials, ws->counter, d_nsq);
+    } else {
+      const int g = chunk_grid((const void*)chunk_update_kernel, 3, ws->device, n);
+      chunk_update_kernel<<<g, kChunkThreads, 0, st>>>(d_V, ld, k, d_z, n, d_c1, d_c2, d_w2,
+                                                       ws->partials, ws->counter, d_nsq);
+    }
     check_launch();
   });
 }

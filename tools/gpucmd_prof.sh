@@ -1,0 +1,5 @@
+# launch list + full captures of the fused polynomial pass and the CGS2 kernels (cfg2 solve)
+python tools/profile_solve.py > gpurun_out/prof_plain.log 2>&1 && \
+ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg2.csv python tools/profile_solve.py > gpurun_out/ncu_launch.log 2>&1; tail -2 gpurun_out/ncu_launch.log
+ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:sell_kernel -s 40 -c 3 -o gpurun_out/prof_poly python tools/profile_solve.py > gpurun_out/ncu_full.log 2>&1; tail -2 gpurun_out/ncu_full.log
+ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"tile_kernel|rows_kernel" -s 120 -c 3 -o gpurun_out/prof_cgs2 python tools/profile_solve.py > gpurun_out/ncu_full2.log 2>&1; tail -2 gpurun_out/ncu_full2.log
