@@ -69,9 +69,11 @@ def header_symbols(path: str = HEADER_PATH):
 
 def load():
     """Load (once) and return the library; raises if it is missing."""
-    global _lib
+    global _lib, LIB_PATH
     if _lib is not None:
         return _lib
+    # PG_LIB_PATH: load an alternative build (kernel-variant A/B experiments)
+    LIB_PATH = os.environ.get("PG_LIB_PATH", LIB_PATH)
     if not os.path.exists(LIB_PATH):
         raise errors.DeviceError(
             f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "

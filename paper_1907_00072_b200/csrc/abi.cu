@@ -242,7 +242,7 @@ PG_API int pg_matrix_create(int device, int64_t nrows, int64_t ncols, const int6
       // and vectors), so streaming evict_first loads are the default
       {
         const char* kv = std::getenv("PG_SPMV_L2KEEP");
-        m->l2_keep = kv ? (std::atoi(kv) != 0) : 0;
+        m->l2_keep = kv ? std::atoi(kv) : 0;
       }
       int64_t acc = 0;
       for (int64_t s = 0; s < h.n_slices; ++s) {

@@ -29,7 +29,18 @@ namespace pg {
 enum SellMode { kSpmv = 0, kPoly = 1, kResid = 2 };
 
 constexpr int kSellThreads = 256;
-constexpr int kUnroll = 8;
+// Occupancy floor and row-chunk unroll of the plain kernel, chosen by sweep
+// on B200 (tools/spmv_bench.py over build variants): (4 blocks, unroll 4)
+// gives cfg2 5.40, cfg4 6.19, cfg5 5.26, cfg3 2.41 TB/s; forcing 6+ blocks
+// (<= 40 registers) spills and loses 30-40%.
+#ifndef PG_SELL_MIN_BLOCKS
+#define PG_SELL_MIN_BLOCKS 4
+#endif
+constexpr int kSellMinBlocks = PG_SELL_MIN_BLOCKS;
+#ifndef PG_SELL_UNROLL
+#define PG_SELL_UNROLL 4
+#endif
+constexpr int kUnroll = PG_SELL_UNROLL;
 constexpr int kConsumerWarps = 16;
 constexpr int kTmaThreads = (kConsumerWarps + 1) * 32;
 constexpr int kStages = 6;
@@ -56,15 +67,18 @@ __device__ __forceinline__ uint64_t l2_policy_keep() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
   return p;
 }
-__device__ __forceinline__ int ld_mat(const int32_t* p, bool keep, uint64_t pol) {
-  if (!keep) return __ldcs(p);
+// mode 0: streaming (evict-first), 1: L2 evict_last policy, 2: default caching
+__device__ __forceinline__ int ld_mat(const int32_t* p, int mode, uint64_t pol) {
+  if (mode == 0) return __ldcs(p);
+  if (mode == 2) return __ldg(p);
   int v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;\n"
                : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
-__device__ __forceinline__ double ld_mat(const double* p, bool keep, uint64_t pol) {
-  if (!keep) return __ldcs(p);
+__device__ __forceinline__ double ld_mat(const double* p, int mode, uint64_t pol) {
+  if (mode == 0) return __ldcs(p);
+  if (mode == 2) return __ldg(p);
   double v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n"
                : "=d"(v) : "l"(p), "l"(pol));
@@ -163,7 +177,7 @@ __device__ __forceinline__ void finish_resid(double local, double* partials, uns
 
 // ------------------------------------------------------------ plain kernel --
 template <int MODE>
-__global__ void __launch_bounds__(kSellThreads)
+__global__ void __launch_bounds__(kSellThreads, kSellMinBlocks)
     sell_kernel(SellArgs a, const double* __restrict__ x, Epi e, double* partials,
                 unsigned int* counter, double* nsq) {
   double local = 0.0;
@@ -179,8 +193,8 @@ __global__ void __launch_bounds__(kSellThreads)
     const int32_t* __restrict__ cpp = a.col + base;
     const double* __restrict__ vpp = a.val + base;
     const Pre pre = epi_load<MODE>(e, x, row);
-    const bool keep = a.l2_keep != 0;
-    const uint64_t pol = keep ? l2_policy_keep() : 0;
+    const int keep = a.l2_keep;
+    const uint64_t pol = keep == 1 ? l2_policy_keep() : 0;
     const double ax = row_sum(
         [&](int j) { return ld_mat(cpp + (int64_t)j * PG_SLICE, keep, pol); },
         [&](int j) { return ld_mat(vpp + (int64_t)j * PG_SLICE, keep, pol); }, w, len, x);

@@ -1,2 +1,3 @@
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 800 python -m pytest tests -q -m "gpu" > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log; grep -E "^E |^FAILED" gpurun_out/pytest_gpu.log | head -8
+for d in mb4_u8 mb6_u8 mb8_u4 mb6_u4 mb4_u4 mb8_u2; do
+echo "== $d"; PG_LIB_PATH=$PWD/variants_tmp/$d/libpgmres.so python tools/spmv_bench.py 2>&1 | grep plain | cut -c1-110
+done
