@@ -183,7 +183,9 @@ class Shard:
         _lib.call("pg_set_device", self.dev_ord)
 
     def vec(self) -> torch.Tensor:
-        return torch.zeros(self.n_ext, dtype=F64, device=self.device)
+        """Shard vector: owned rows, ghost slots, zero padding up to ``ld`` (the
+        tile / ring kernels stream whole 16-byte pairs of rows)."""
+        return torch.zeros(self.ld, dtype=F64, device=self.device)
 
     def block(self, cols: int) -> torch.Tensor:
         """Column-major n x cols block: row-major (cols, ld) tensor."""
