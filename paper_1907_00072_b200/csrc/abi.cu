@@ -19,6 +19,15 @@ static thread_local std::string g_last_error;
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = std::getenv("PG_PDL");
+    v = s ? (std::atoi(s) != 0) : 1;
+  }
+  return v == 1;
+}
+
 int grid_for(int device, const void* kernel, int block, size_t smem, int64_t work_blocks) {
   int sms = 0, per_sm = 0;
   PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));

@@ -139,6 +139,40 @@ __device__ inline double block_sum(double v) {
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch.  Every libpgmres kernel starts with
+//   griddepcontrol.launch_dependents  -- the next kernel in the stream may be
+//                                        scheduled once all our CTAs are resident
+//   griddepcontrol.wait               -- block until the previous grid has
+//                                        completed and its writes are visible
+// and is launched with cudaLaunchAttributeProgrammaticStreamSerialization, so
+// the launch latency and CTA rasterisation of kernel N+1 overlap kernel N's
+// tail.  Results are unchanged: no kernel touches global memory before the
+// wait.  PG_PDL=0 disables it.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  PG_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 int grid_for(int device, const void* kernel, int block, size_t smem, int64_t work_blocks);
 
 }  // namespace pg

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(kTileThreads)
     tile_kernel(const double* __restrict__ V, int64_t ld, int k, const double* __restrict__ z,
                 int64_t n, const double* __restrict__ c1, double* partials,
                 unsigned int* counter, double* out) {
+  pdl_entry();
   extern __shared__ __align__(16) double smem[];
   __shared__ double c1s[PG_KMAX];
   const bool has_z = (MODE != kGram);
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
     ring_kernel(const double* __restrict__ V, int64_t ld, int k, const double* __restrict__ z,
                 int64_t n, const double* __restrict__ c1, int stages, double* partials,
                 unsigned int* counter, double* out) {
+  pdl_entry();
   extern __shared__ __align__(128) unsigned char ring_raw[];
   double* sbuf = reinterpret_cast<double*>(ring_raw);
   __shared__ __align__(8) uint64_t full[kRingMaxStages];
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(kRowThreads)
     rows_kernel(const double* __restrict__ V, int64_t ld, int k, const double* __restrict__ z,
                 int64_t n, const double* __restrict__ c1, const double* __restrict__ c2,
                 double* __restrict__ out, double* partials, unsigned int* counter, double* nsq) {
+  pdl_entry();
   __shared__ double cs1[PG_KMAX], cs2[PG_KMAX];
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     cs1[i] = c1[i];
@@ -475,6 +478,7 @@ __global__ void __launch_bounds__(kChunkThreads)
     chunk_dots_kernel(const double* __restrict__ V, int64_t ld, int k,
                       const double* __restrict__ z, int64_t n, const double* __restrict__ c1,
                       double* partials, unsigned int* counter, double* out) {
+  pdl_entry();
   __shared__ double cs[PG_KMAX];
   __shared__ double wsum[kChunkThreads / 32][PG_KMAX];
   if (MODE == 2)
@@ -540,6 +544,7 @@ __global__ void __launch_bounds__(kChunkThreads)
                         const double* __restrict__ z, int64_t n, const double* __restrict__ c1,
                         const double* __restrict__ c2, double* __restrict__ out,
                         double* partials, unsigned int* counter, double* nsq) {
+  pdl_entry();
   __shared__ double cs1[PG_KMAX], cs2[PG_KMAX];
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     cs1[i] = c1[i];
@@ -594,6 +599,7 @@ __global__ void __launch_bounds__(kChunkThreads)
 
 __global__ void dot_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                            double* partials, unsigned int* counter, double* out) {
+  pdl_entry();
   double local = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -605,6 +611,7 @@ __global__ void dot_kernel(const double* __restrict__ x, const double* __restric
 
 __global__ void normalize_kernel(const double* __restrict__ x, const double* __restrict__ nsq,
                                  int64_t n, double* __restrict__ out) {
+  pdl_entry();
   const double nrm = sqrt(*nsq);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -613,6 +620,7 @@ __global__ void normalize_kernel(const double* __restrict__ x, const double* __r
 
 __global__ void scale_add_kernel(const double* base, double a, const double* v, int64_t n,
                                  double* out) {
+  pdl_entry();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const double t = __dmul_rn(a, v[i]);
@@ -622,6 +630,7 @@ __global__ void scale_add_kernel(const double* base, double a, const double* v, 
 
 __global__ void gather_kernel(const double* __restrict__ x, const int32_t* __restrict__ idx,
                               int64_t m, double* __restrict__ out) {
+  pdl_entry();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride)
     out[i] = x[idx[i]];
@@ -731,8 +740,7 @@ static void launch_ring(const double* V, int64_t ld, int k, const double* z, int
   }
   int g = ws->num_sms;
   if (ntiles < g) g = (int)ntiles;
-  ring_kernel<MODE><<<g, kRingThreads, stage_bytes * stages, st>>>(
-      V, ld, k, z, n, c1, stages, ws->partials, ws->counter, out);
+  launch_k(ring_kernel<MODE>, g, kRingThreads, stage_bytes * stages, st, V, ld, k, z, n, c1, stages, ws->partials, ws->counter, out);
   check_launch();
 }
 
@@ -745,7 +753,7 @@ static void launch_chunk_dots(const double* V, int64_t ld, int k, const double* 
     return;
   }
   const int g = chunk_grid((const void*)chunk_dots_kernel<MODE>, MODE, ws->device, n);
-  chunk_dots_kernel<MODE><<<g, kChunkThreads, 0, st>>>(V, ld, k, z, n, c1, ws->partials,
+  launch_k(chunk_dots_kernel<MODE>, g, kChunkThreads, 0, st, V, ld, k, z, n, c1, ws->partials,
                                                        ws->counter, out);
   check_launch();
 }
@@ -787,13 +795,13 @@ static void launch_tile(const double* V, int64_t ld, int k, const double* z, int
   }
   if (ntiles < g) g = (int)ntiles;
   if (stages == 4)
-    tile_kernel<MODE, 4><<<g, kTileThreads, smem, st>>>(V, ld, k, z, n, c1, ws->partials,
+    launch_k(tile_kernel<MODE, 4>, g, kTileThreads, smem, st, V, ld, k, z, n, c1, ws->partials,
                                                         ws->counter, out);
   else if (stages == 3)
-    tile_kernel<MODE, 3><<<g, kTileThreads, smem, st>>>(V, ld, k, z, n, c1, ws->partials,
+    launch_k(tile_kernel<MODE, 3>, g, kTileThreads, smem, st, V, ld, k, z, n, c1, ws->partials,
                                                         ws->counter, out);
   else
-    tile_kernel<MODE, 2><<<g, kTileThreads, smem, st>>>(V, ld, k, z, n, c1, ws->partials,
+    launch_k(tile_kernel<MODE, 2>, g, kTileThreads, smem, st, V, ld, k, z, n, c1, ws->partials,
                                                         ws->counter, out);
   check_launch();
 }
@@ -856,11 +864,11 @@ PG_API int pg_cgs2_phase3(const double* d_V, int64_t ld, int k, const double* d_
     }
     if (use_tile_cgs2(k)) {
       const int g = simple_grid(n, kRowThreads, ws);
-      rows_kernel<true><<<g, kRowThreads, 0, st>>>(d_V, ld, k, d_z, n, d_c1, d_c2, d_w2,
+      launch_k(rows_kernel<true>, g, kRowThreads, 0, st, d_V, ld, k, d_z, n, d_c1, d_c2, d_w2,
                                                     ws->partials, ws->counter, d_nsq);
     } else {
       const int g = chunk_grid((const void*)chunk_update_kernel, 3, ws->device, n);
-      chunk_update_kernel<<<g, kChunkThreads, 0, st>>>(d_V, ld, k, d_z, n, d_c1, d_c2, d_w2,
+      launch_k(chunk_update_kernel, g, kChunkThreads, 0, st, d_V, ld, k, d_z, n, d_c1, d_c2, d_w2,
                                                        ws->partials, ws->counter, d_nsq);
     }
     check_launch();
@@ -873,7 +881,7 @@ PG_API int pg_normalize(const double* d_x, const double* d_nsq, int64_t n, doubl
     PG_REQUIRE(d_x && d_nsq && d_out, PG_ERR_PARAMETER, "null argument");
     if (n == 0) return;
     const int g = simple_grid(n, 256, nullptr);
-    normalize_kernel<<<g, 256, 0, as_stream(stream)>>>(d_x, d_nsq, n, d_out);
+    launch_k(normalize_kernel, g, 256, 0, as_stream(stream), d_x, d_nsq, n, d_out);
     check_launch();
   });
 }
@@ -894,8 +902,7 @@ PG_API int pg_gemv(const double* d_V, int64_t ld, int k, const double* d_y, int6
     PG_REQUIRE(d_out && (k == 0 || d_y), PG_ERR_PARAMETER, "null argument");
     if (n == 0) return;
     const int g = simple_grid(n, kRowThreads, nullptr);
-    rows_kernel<false><<<g, kRowThreads, 0, as_stream(stream)>>>(
-        d_V, ld, k, nullptr, n, d_y, nullptr, d_out, nullptr, nullptr, nullptr);
+    launch_k(rows_kernel<false>, g, kRowThreads, 0, as_stream(stream), d_V, ld, k, nullptr, n, d_y, nullptr, d_out, nullptr, nullptr, nullptr);
     check_launch();
   });
 }
@@ -911,7 +918,7 @@ PG_API int pg_dot(const double* d_x, const double* d_y, int64_t n, double* d_out
       return;
     }
     const int g = simple_grid(n, 256, ws);
-    dot_kernel<<<g, 256, 0, st>>>(d_x, d_y, n, ws->partials, ws->counter, d_out);
+    launch_k(dot_kernel, g, 256, 0, st, d_x, d_y, n, ws->partials, ws->counter, d_out);
     check_launch();
   });
 }
@@ -922,7 +929,7 @@ PG_API int pg_scale_add(const double* d_base, double a, const double* d_v, int64
     PG_REQUIRE(d_v && d_out, PG_ERR_PARAMETER, "null argument");
     if (n == 0) return;
     const int g = simple_grid(n, 256, nullptr);
-    scale_add_kernel<<<g, 256, 0, as_stream(stream)>>>(d_base, a, d_v, n, d_out);
+    launch_k(scale_add_kernel, g, 256, 0, as_stream(stream), d_base, a, d_v, n, d_out);
     check_launch();
   });
 }
@@ -933,7 +940,7 @@ PG_API int pg_gather(const double* d_x, const int32_t* d_idx, int64_t m, double*
     if (m == 0) return;
     PG_REQUIRE(d_x && d_idx && d_out, PG_ERR_PARAMETER, "null argument");
     const int g = simple_grid(m, 256, nullptr);
-    gather_kernel<<<g, 256, 0, as_stream(stream)>>>(d_x, d_idx, m, d_out);
+    launch_k(gather_kernel, g, 256, 0, as_stream(stream), d_x, d_idx, m, d_out);
     check_launch();
   });
 }

@@ -180,6 +180,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kSellThreads, kSellMinBlocks)
     sell_kernel(SellArgs a, const double* __restrict__ x, Epi e, double* partials,
                 unsigned int* counter, double* nsq) {
+  pdl_entry();
   double local = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t lane = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lane < a.nlanes;
@@ -210,6 +211,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     sell_tma_kernel(SellArgs a, const int32_t* __restrict__ unit_slice, int64_t n_units,
                     const double* __restrict__ x, Epi e, double* partials,
                     unsigned int* counter, double* nsq) {
+  pdl_entry();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   int32_t* scol = reinterpret_cast<int32_t*>(smem_raw);
   double* sval = reinterpret_cast<double*>(smem_raw + (size_t)kStages * kUnitEntries * 4);
@@ -319,14 +321,14 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
     }
     int g = sms[dev];
     if (m->n_units < g) g = (int)m->n_units;
-    sell_tma_kernel<MODE><<<g, kTmaThreads, kTmaSmem, st>>>(a, m->unit_slice, m->n_units, x, e,
+    launch_k(sell_tma_kernel<MODE>, g, kTmaThreads, kTmaSmem, st, a, m->unit_slice, m->n_units, x, e,
                                                            part, cnt, nsq);
   } else {
     // one row per thread; reductions keep the grid within the partial slots
     int64_t blocks = (a.nlanes + kSellThreads - 1) / kSellThreads;
     const int64_t cap = (MODE == kResid) ? kMaxBlocks : (int64_t)sms[dev] * 64;
     if (blocks > cap) blocks = cap;
-    sell_kernel<MODE><<<(int)blocks, kSellThreads, 0, st>>>(a, x, e, part, cnt, nsq);
+    launch_k(sell_kernel<MODE>, (int)blocks, kSellThreads, 0, st, a, x, e, part, cnt, nsq);
   }
   check_launch();
 }

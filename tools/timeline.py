@@ -59,7 +59,10 @@ def main():
         key = nm.split("(")[0][:50]
         per[key][0] += 1
         per[key][1] += e - s
-    big = sorted(gaps, reverse=True)[:10]
+    order = sorted(range(len(gaps)), key=lambda i: -gaps[i])[:12]
+    big = [dict(gap_us=round(gaps[i], 1), at_kernel=i,
+                before=kern[i][2].split("(")[0][-30:], after=kern[i + 1][2].split("(")[0][-30:])
+           for i in order]
     out = dict(iterations=res.iterations, kernels=len(kern), span_us=span, busy_us=busy,
                idle_us=span - busy, gaps_over_10us=sum(g for g in gaps if g > 10),
                n_gaps_over_10us=sum(1 for g in gaps if g > 10), largest_gaps_us=big,
