@@ -82,8 +82,9 @@ PG_API int pg_matrix_create(int device, int64_t nrows, int64_t ncols,
                             const int64_t* row_ptr, const int64_t* col_idx,
                             const double* values, int sigma, pg_matrix** out);
 PG_API int pg_matrix_destroy(pg_matrix* mat);
-/* stats[8] = {nrows, ncols, nnz, padded_nnz, n_slices, device_bytes,
- *             max_width, sigma} */
+/* stats[10] = {nrows, ncols, nnz, padded_nnz, n_slices, device_bytes,
+ *              max_width, sigma, bytes per column entry (1 = dictionary-
+ *              compressed offsets, 4 = int32), bytes per value (1 or 8)} */
 PG_API int pg_matrix_stats(const pg_matrix* mat, int64_t* stats);
 
 /* ---- reduction workspace (one per stream) --------------------------------
@@ -150,6 +151,25 @@ PG_API int pg_scale_add(const double* d_base, double a, const double* d_v, int64
                         double* d_out, void* stream);
 PG_API int pg_gather(const double* d_x, const int32_t* d_idx, int64_t m, double* d_out,
                      void* stream);
+
+/* ---- host routines (CPU, synchronous) --------------------------------------
+ * The small dense steps the reference keeps on the host, natively:
+ * pg_host_cholesky_solve: dense_cholesky (polyprec.py:60-93) of the leading
+ *   order x order block of row-major G (leading dimension ldg); *failed_pivot
+ *   = 0 and y filled on success, else the 1-based pivot failing
+ *   pivot <= order*eps*G[k,k].
+ * pg_host_degree_select: auto_degree's choice (polyprec.py:171-182): largest
+ *   d <= cap whose order-(d+1) system factors with finite y; *degree = -1 if
+ *   none.  G, rhs are the cap+1 normal-equation blocks.
+ * pg_host_backsolve: y = R[:j,:j]^{-1} g (gmres.py:319-325), R row-major with
+ *   leading dimension ldr; *zero_col = index of a zero diagonal (-1 if none;
+ *   the caller raises SingularHessenbergError). */
+PG_API int pg_host_cholesky_solve(int order, const double* G, int ldg, const double* rhs,
+                                  double* y, int* failed_pivot);
+PG_API int pg_host_degree_select(int cap, const double* G, int ldg, const double* rhs,
+                                 double* y, int* degree);
+PG_API int pg_host_backsolve(int j, const double* R, int ldr, const double* g, double* y,
+                             int* zero_col);
 
 #ifdef __cplusplus
 }

@@ -245,6 +245,34 @@ def gram_exact(powers):
     return G
 
 
+def chol_pivot_exact(G):
+    """1-based failing pivot (0 = success) of the Cholesky of G with every
+    inner product exactly rounded (math.fsum) and the reference's floor
+    ``pivot <= order*eps*G[k,k]`` -- the exact-arithmetic pass/fail decision
+    (the plain numpy loop decides the trailing pivots by its own rounding)."""
+    G = np.asarray(G, dtype=np.float64)
+    o = G.shape[0]
+    eps = np.finfo(np.float64).eps
+    L = [[0.0] * o for _ in range(o)]
+    for k in range(o):
+        piv = math.fsum([float(G[k, k])] + [-L[k][t] * L[k][t] for t in range(k)])
+        if piv <= o * eps * G[k, k]:
+            return k + 1
+        L[k][k] = math.sqrt(piv)
+        for i in range(k + 1, o):
+            L[i][k] = math.fsum([float(G[i, k])] + [-L[i][t] * L[k][t] for t in range(k)]) / L[k][k]
+    return 0
+
+
+def auto_deg_exact(Gfull, cap):
+    """Exact-arithmetic auto_degree decision on a (correctly rounded) Gram."""
+    G = Gfull[1:cap + 2, 1:cap + 2]
+    for d in range(cap, 0, -1):
+        if chol_pivot_exact(G[:d + 1, :d + 1]) == 0:
+            return d
+    return 0
+
+
 def auto_deg_from_gram(Gfull, cap):
     """auto_degree's selection loop (polyprec.py:171-190) on a given full
     Gram of [v, Av, ..., A^{cap+1} v]."""

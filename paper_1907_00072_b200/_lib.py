@@ -56,6 +56,9 @@ _SIGNATURES = {
     "pg_dot": ([_p, _p, _i64, _p, _p, _p], C.c_int),
     "pg_scale_add": ([_p, _d, _p, _i64, _p, _p], C.c_int),
     "pg_gather": ([_p, _p, _i64, _p, _p], C.c_int),
+    "pg_host_cholesky_solve": ([_i32, _p, _i32, _p, _p, C.POINTER(C.c_int)], C.c_int),
+    "pg_host_degree_select": ([_i32, _p, _i32, _p, _p, C.POINTER(C.c_int)], C.c_int),
+    "pg_host_backsolve": ([_i32, _p, _i32, _p, _p, C.POINTER(C.c_int)], C.c_int),
 }
 
 _lib = None
@@ -119,6 +122,43 @@ def launches() -> int:
 
 
 _FN: dict = {}
+
+
+def host_cholesky(G, rhs):
+    """(y, failed_pivot) of the order-len(rhs) Gram system (native)."""
+    import numpy as np
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+    o = len(rhs)
+    y = np.zeros(o)
+    piv = C.c_int(0)
+    call("pg_host_cholesky_solve", o, G.ctypes.data, G.shape[1], rhs.ctypes.data, y.ctypes.data,
+         C.byref(piv))
+    return y, piv.value
+
+
+def host_degree_select(G, rhs, cap):
+    """(degree, y) chosen like auto_degree from the cap+1 blocks; degree -1 if none."""
+    import numpy as np
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+    y = np.zeros(cap + 1)
+    d = C.c_int(-1)
+    call("pg_host_degree_select", cap, G.ctypes.data, G.shape[1], rhs.ctypes.data,
+         y.ctypes.data, C.byref(d))
+    return d.value, (y[:d.value + 1].copy() if d.value >= 0 else None)
+
+
+def host_backsolve(R, g, j):
+    """y = R[:j,:j]^{-1} g[:j]; returns (y, zero_col) (zero_col = -1 if none)."""
+    import numpy as np
+    R = np.ascontiguousarray(R, dtype=np.float64)
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    y = np.zeros(max(j, 1))
+    zc = C.c_int(-1)
+    call("pg_host_backsolve", j, R.ctypes.data, R.shape[1], g.ctypes.data, y.ctypes.data,
+         C.byref(zc))
+    return y[:j], zc.value
 
 
 def call(name: str, *args):

@@ -64,6 +64,12 @@ struct pg_matrix {
   int32_t* perm;       // [n_slices*32] local row of lane (nullptr if sigma<=1)
   int32_t* col;        // [padded]  SELL column indices (int32)
   double* val;         // [padded]  SELL values
+  int64_t* slice_ptr8; // [n_slices+1] slice offsets of the packed 1-byte streams
+  uint8_t* col8;       // packed dictionary index of (col - row), or null
+  int32_t* dtab;       // [256]    column-offset dictionary
+  uint8_t* val8;       // [padded] dictionary index of the value bits, or null
+  double* vtab;        // [256]    value dictionary
+  int n_dcol, n_dval;  // dictionary sizes (0 = stream not compressed)
   int32_t* unit_slice; // [n_units+1] first slice of each TMA streaming unit
   int64_t n_units;
   bool use_tma;        // every slice fits a ring stage (kUnitEntries)

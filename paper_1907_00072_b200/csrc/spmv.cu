@@ -21,6 +21,8 @@
 //  * sell_kernel: plain grid of one-row-per-thread loads, for matrices with a
 //    slice too wide for a ring stage.
 
+#include <cstdlib>
+
 #include "internal.cuh"
 #include "pipeline.cuh"
 
@@ -56,6 +58,11 @@ struct SellArgs {
   int64_t nrows;
   int64_t nlanes;
   int l2_keep;  // matrix stream marked L2 evict_last (resident across a pass chain)
+  const int64_t* __restrict__ slice_ptr8;  // packed 1-byte stream offsets
+  const uint8_t* __restrict__ col8;  // dictionary-compressed streams (abi.cu)
+  const int32_t* __restrict__ dtab;
+  const uint8_t* __restrict__ val8;
+  const double* __restrict__ vtab;
 };
 
 // Matrix-stream loads.  With l2_keep the index/value lines carry an L2
@@ -139,16 +146,19 @@ __device__ __forceinline__ double epilogue(const Epi& e, const Pre& p, int64_t r
   }
 }
 
-// Sequential row sum over entries held at p_col[j*32], p_val[j*32].
-template <class ColPtr, class ValPtr>
-__device__ __forceinline__ double row_sum(ColPtr cp, ValPtr vp, int w, int len,
+// Sequential row sum over the row's entries.  cp(j) loads the raw column
+// entry j (an int32 column, or a 1-byte dictionary index), dec(raw) turns it
+// into a column, vp(j) loads value j.
+template <class ColPtr, class Dec, class ValPtr>
+__device__ __forceinline__ double row_sum(ColPtr cp, Dec dec, ValPtr vp, int w, int len,
                                           const double* __restrict__ x) {
   double acc = 0.0;
   for (int j = 0; j < w; j += kUnroll) {
     double v[kUnroll], xv[kUnroll];
     int c[kUnroll];
-    // all index / value loads of the chunk first (bounded by the uniform slice
-    // width), then all gathers (bounded by this row's length)
+    // all raw index / value loads of the chunk first (bounded by the uniform
+    // slice width), then the dictionary decode, then all gathers (bounded by
+    // this row's length): no global load waits behind a dependent one
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       if (j + u < w) {
@@ -157,9 +167,49 @@ __device__ __forceinline__ double row_sum(ColPtr cp, ValPtr vp, int w, int len,
       }
     }
 #pragma unroll
+    for (int u = 0; u < kUnroll; ++u) c[u] = dec(c[u]);
+#pragma unroll
     for (int u = 0; u < kUnroll; ++u) xv[u] = (j + u < len) ? __ldg(x + c[u]) : 0.0;
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
+      if (j + u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+  }
+  return acc;
+}
+
+// Row sum over dictionary-compressed streams: one 32-bit load per lane per 4
+// entries of each packed 1-byte stream (CM: column offsets, VM: values);
+// uncompressed streams keep their regular SELL positions.  Same sequential
+// order and separately rounded products as row_sum.
+template <int CM, int VM>
+__device__ __forceinline__ double row_sum_dict(const SellArgs& a, int64_t base, int64_t base8,
+                                               int row, int w, int len,
+                                               const double* __restrict__ x,
+                                               const int32_t* s_dtab, const double* s_vtab) {
+  const uint32_t* __restrict__ cw = reinterpret_cast<const uint32_t*>(a.col8 + base8);
+  const uint32_t* __restrict__ vw = reinterpret_cast<const uint32_t*>(a.val8 + base8);
+  double acc = 0.0;
+  for (int j = 0; j < w; j += 4) {
+    const int q = j >> 2;
+    uint32_t cbits = 0, vbits = 0;
+    int c[4];
+    double v[4], xv[4];
+    if (CM) cbits = __ldcs(cw + q * PG_SLICE);
+    if (VM) vbits = __ldcs(vw + q * PG_SLICE);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (!CM) c[u] = (j + u < w) ? __ldcs(a.col + base + (int64_t)(j + u) * PG_SLICE) : 0;
+      if (!VM) v[u] = (j + u < w) ? __ldcs(a.val + base + (int64_t)(j + u) * PG_SLICE) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (CM) c[u] = row + s_dtab[(cbits >> (8 * u)) & 255u];
+      if (VM) v[u] = s_vtab[(vbits >> (8 * u)) & 255u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xv[u] = (j + u < len) ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
       if (j + u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
   }
   return acc;
@@ -176,11 +226,20 @@ __device__ __forceinline__ void finish_resid(double local, double* partials, uns
 }
 
 // ------------------------------------------------------------ plain kernel --
-template <int MODE>
+// CM / VM: 1 = the column / value stream is dictionary-compressed (1-byte
+// indices into the per-matrix tables, staged in shared memory per block).
+template <int MODE, int CM, int VM>
 __global__ void __launch_bounds__(kSellThreads, kSellMinBlocks)
     sell_kernel(SellArgs a, const double* __restrict__ x, Epi e, double* partials,
                 unsigned int* counter, double* nsq) {
   pdl_entry();
+  __shared__ int32_t s_dtab[CM ? 256 : 1];
+  __shared__ double s_vtab[VM ? 256 : 1];
+  if (CM)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_dtab[i] = __ldg(a.dtab + i);
+  if (VM)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_vtab[i] = __ldg(a.vtab + i);
+  if (CM || VM) __syncthreads();
   double local = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t lane = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lane < a.nlanes;
@@ -191,14 +250,20 @@ __global__ void __launch_bounds__(kSellThreads, kSellMinBlocks)
     const int w = __ldg(a.slice_w + s);
     const int len = __ldg(a.row_len + lane);
     const int64_t base = __ldg(a.slice_ptr + s) + (lane & 31);
-    const int32_t* __restrict__ cpp = a.col + base;
-    const double* __restrict__ vpp = a.val + base;
     const Pre pre = epi_load<MODE>(e, x, row);
     const int keep = a.l2_keep;
     const uint64_t pol = keep == 1 ? l2_policy_keep() : 0;
-    const double ax = row_sum(
-        [&](int j) { return ld_mat(cpp + (int64_t)j * PG_SLICE, keep, pol); },
-        [&](int j) { return ld_mat(vpp + (int64_t)j * PG_SLICE, keep, pol); }, w, len, x);
+    double ax;
+    if (CM || VM) {
+      const int64_t base8 = __ldg(a.slice_ptr8 + s) + 4 * (lane & 31);
+      ax = row_sum_dict<CM, VM>(a, base, base8, (int)row, w, len, x, s_dtab, s_vtab);
+    } else {
+      ax = row_sum(
+          [&](int j) { return ld_mat(a.col + base + (int64_t)j * PG_SLICE, keep, pol); },
+          [](int raw) { return raw; },
+          [&](int j) { return ld_mat(a.val + base + (int64_t)j * PG_SLICE, keep, pol); }, w,
+          len, x);
+    }
     const double r = epilogue<MODE>(e, pre, row, ax);
     if (MODE == kResid) local = __fma_rn(r, r, local);
   }
@@ -266,6 +331,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const int off = (int)(__ldg(a.slice_ptr + sl) - e0) + lane;
         const Pre pre = epi_load<MODE>(e, x, row);
         const double ax = row_sum([&](int j) { return C[off + j * PG_SLICE]; },
+                                  [](int raw) { return raw; },
                                   [&](int j) { return Vv[off + j * PG_SLICE]; }, w, len, x);
         if (row >= 0) {
           const double r = epilogue<MODE>(e, pre, row, ax);
@@ -291,6 +357,11 @@ static SellArgs args_of(const pg_matrix* m) {
   a.nrows = m->nrows;
   a.nlanes = m->n_slices * PG_SLICE;
   a.l2_keep = m->l2_keep;
+  a.slice_ptr8 = m->slice_ptr8;
+  a.col8 = m->col8;
+  a.dtab = m->dtab;
+  a.val8 = m->val8;
+  a.vtab = m->vtab;
   return a;
 }
 
@@ -312,7 +383,7 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
   unsigned* cnt = ws ? ws->counter : nullptr;
   static int sms[64] = {};
   if (!sms[dev]) PG_CUDA(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
-  if (m->use_tma) {
+  if (m->use_tma && !m->col8 && !m->val8) {  // the ring streams the uncompressed arrays
     static bool attr[3][64] = {};
     if (!attr[MODE][dev]) {
       PG_CUDA(cudaFuncSetAttribute(sell_tma_kernel<MODE>,
@@ -326,9 +397,26 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
   } else {
     // one row per thread; reductions keep the grid within the partial slots
     int64_t blocks = (a.nlanes + kSellThreads - 1) / kSellThreads;
-    const int64_t cap = (MODE == kResid) ? kMaxBlocks : (int64_t)sms[dev] * 64;
+    const int cm = m->col8 != nullptr, vm = m->val8 != nullptr;
+    // compressed streams: a resident grid (grid-stride over rows) so each
+    // block stages the dictionaries once, not once per 256 rows
+    static int per_sm_env = -1;
+    if (per_sm_env < 0) {
+      const char* s = std::getenv("PG_SPMV_DICT_BLOCKS_PER_SM");
+      per_sm_env = s ? std::atoi(s) : 4;  // measured best (4 / 16 / 64 swept)
+    }
+    const int64_t cap = (MODE == kResid) ? kMaxBlocks
+                        : (cm || vm)     ? (int64_t)sms[dev] * per_sm_env
+                                         : (int64_t)sms[dev] * 64;
     if (blocks > cap) blocks = cap;
-    launch_k(sell_kernel<MODE>, (int)blocks, kSellThreads, 0, st, a, x, e, part, cnt, nsq);
+    if (cm && vm)
+      launch_k(sell_kernel<MODE, 1, 1>, (int)blocks, kSellThreads, 0, st, a, x, e, part, cnt, nsq);
+    else if (cm)
+      launch_k(sell_kernel<MODE, 1, 0>, (int)blocks, kSellThreads, 0, st, a, x, e, part, cnt, nsq);
+    else if (vm)
+      launch_k(sell_kernel<MODE, 0, 1>, (int)blocks, kSellThreads, 0, st, a, x, e, part, cnt, nsq);
+    else
+      launch_k(sell_kernel<MODE, 0, 0>, (int)blocks, kSellThreads, 0, st, a, x, e, part, cnt, nsq);
   }
   check_launch();
 }

@@ -143,10 +143,13 @@ class Shard:
         _lib.call("pg_workspace_create", self.dev_ord, _lib.C.byref(w))
         self.ws = w
         self.nnz = int(row_ptr[-1])
-        st = (_lib.C.c_int64 * 8)()
+        st = (_lib.C.c_int64 * 10)()
         _lib.call("pg_matrix_stats", self.mat, st)
         self.stats = dict(zip(("nrows", "ncols", "nnz", "padded_nnz", "n_slices",
-                               "device_bytes", "max_width", "sigma"), list(st)))
+                               "device_bytes", "max_width", "sigma", "col_bytes",
+                               "val_bytes"), list(st)))
+        # bytes streamed per stored matrix entry (dictionary compression: 1+1)
+        self.entry_bytes = int(st[8]) + int(st[9])
         # small per-shard device scratch: [c1 | c2 | nsq | spare]
         self.scal = torch.zeros(2 * KMAX + 8, dtype=F64, device=device)
         self.coef = torch.zeros(KMAX, dtype=F64, device=device)
@@ -493,11 +496,12 @@ class Engine:
                           ptr(b) if b is not None else None, ptr(dst[i]),
                           ptr(nxt[i]) if not last else None, y[0], y[k], flags, s.stream)
                 if timing:
-                    # algorithmic bytes: 12 B per nonzero (value +
-                    # int32 index), 4 B row length, 8 B compulsory gather of x,
+                    # algorithmic bytes: per nonzero the stored
+                    # entry (12 B: f64 value + int32 index; 2 B with dictionary
+                    # compression), 4 B row length, 8 B compulsory gather of x,
                     # then the epilogue's vector traffic
                     vec = 8 * (int(k > 1) + 1 + int(not last) + int(b is not None))
-                    nbytes += 12 * s.nnz + (12 + vec) * s.n
+                    nbytes += s.entry_bytes * s.nnz + (12 + vec) * s.n
             if not last:
                 self.halo(nxt)
                 cur = nxt
@@ -520,12 +524,17 @@ class Engine:
         self.comm.allreduce(nsq)
         return float(nsq[0].item())
 
-    def dot(self, xs, ys, slot=5) -> float:
+    def dot(self, xs, ys, slot=5, fetch=True):
+        """Global x.y into device slot ``slot``; returns it as a host float
+        unless ``fetch`` is False (then read later with :meth:`read_slot`)."""
         outs = self.slot(slot)
         for s, x, y, o in zip(self._each(), xs, ys, outs):
             _lib.call("pg_dot", ptr(x), ptr(y), s.n, ptr(o), s.ws, s.stream)
         self.comm.allreduce(outs)
-        return float(outs[0].item())
+        return float(outs[0].item()) if fetch else None
+
+    def read_slot(self, slot) -> float:
+        return float(self.slot(slot)[0].item())
 
     def normalize_dev(self, xs, nsq_slices, outs, n_rows=None):
         for s, x, q, o in zip(self._each(), xs, nsq_slices, outs):

@@ -21,6 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from . import _lib
 from .counters import CostCounters
 from .device import KMAX
 from .errors import (
@@ -171,18 +172,28 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
         raise ParameterError(f"restart_m must be at most {KMAX - 1} on the device path")
     tol = config.tol
 
+    poly = right_prec if right_prec else None  # reference truthiness (gmres.py:261)
     bs = e.ingest(b)
-    norm_b = math.sqrt(e.dot(bs, bs, slot=4))
+    W = _Workspace(e, m)
+    xs = e.vecs()
+    early = None
+    if x0 is None:
+        # |b|^2 stays on the device (slot 4) while the first cycle is queued:
+        # r = b, v_0 = r/|b| and Arnoldi step 0 need no host value, so the
+        # host round trip for |b| overlaps step 0 (gmres.py:241-247,277).
+        e.dot(bs, bs, slot=4, fetch=False)
+        e.copy(bs, W.r)
+        e.normalize_dev(W.r, e.slot(4), W.col(0))
+        early = _launch_step(e, W, poly, 0)
+        norm_b = math.sqrt(e.read_slot(4))
+    else:
+        norm_b = math.sqrt(e.dot(bs, bs, slot=4))
     counters.scalar_dots += 1
     if norm_b == 0.0:
         return GmresResult(e.emit(e.vecs(), b), True, 0, 0.0, [], counters, 0)
 
-    W = _Workspace(e, m)
-    xs = e.vecs()
     if x0 is None:
-        e.copy(bs, W.r)
         beta = norm_b
-        beta_nsq_dev = None
     else:
         xs = e.ingest(x0)
         if any(bool(torch.any(x[:s.n] != 0.0)) for s, x in zip(e.shards, xs)):
@@ -193,7 +204,6 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
             beta = math.sqrt(e.dot(bs, bs, slot=4))
         counters.scalar_dots += 1
 
-    poly = right_prec if right_prec else None  # reference truthiness (gmres.py:261)
     d = poly.degree if poly is not None else 0
 
     history: list = []
@@ -207,13 +217,16 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
     g = np.empty(m + 1)
 
     while not converged and total_iters < config.max_iters:
-        # V[:, 0] = r / beta: beta = sqrt(nsq) with nsq still in device slot 4
-        e.normalize_dev(W.r, e.slot(4), W.col(0))
+        if early is not None:  # first cycle already queued above
+            handle, early = early, None
+        else:
+            # V[:, 0] = r / beta: beta = sqrt(nsq) with nsq still in device slot 4
+            e.normalize_dev(W.r, e.slot(4), W.col(0))
+            handle = _launch_step(e, W, poly, 0)
         g[0] = beta
         j = 0
         breakdown = False
         pending_row = None
-        handle = _launch_step(e, W, poly, 0)
         while j < m and total_iters < config.max_iters:
             # one step of look-ahead: step j+1's device work (it only needs
             # v_{j+1}, already normalized on the device) is queued before the
@@ -270,11 +283,9 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
                 pending_row = None
 
         # cycle end (gmres.py:318-341)
-        y = np.empty(j)
-        for i in range(j - 1, -1, -1):
-            if Hrot[i, i] == 0.0:
-                raise SingularHessenbergError(f"zero rotated diagonal at column {i}")
-            y[i] = (g[i] - Hrot[i, i + 1:j] @ y[i + 1:]) / Hrot[i, i]
+        y, zero_col = _lib.host_backsolve(Hrot, g, j)  # native loop of gmres.py:319-325
+        if zero_col >= 0:
+            raise SingularHessenbergError(f"zero rotated diagonal at column {zero_col}")
         e.gemv(W.V, j, y, W.t)
         counters.vector_updates += j
         if poly is not None:

@@ -19,6 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import _lib
 from .counters import CostCounters
 from .device import KMAX
 from .errors import CholeskyFailure, DimensionMismatchError, ParameterError
@@ -126,7 +127,10 @@ def build_poly(op, v0, deg: int, counters: CostCounters,
         raise ParameterError("polynomial degree must be non-negative")
     Gfull, seed_norm = _device_power_gram(op, v0, deg + 1, counters)
     counters.scalar_dots += 1
-    y = dense_cholesky(_normal_equations(Gfull, deg, counters))
+    full = _normal_equations(Gfull, deg, counters)
+    y, pivot = _lib.host_cholesky(full.G, full.rhs)
+    if pivot:
+        raise CholeskyFailure(pivot)
     return PolyCoefficients(deg, y, seed_norm, seed_mode)
 
 
@@ -144,61 +148,18 @@ def auto_degree(op, v0, cap: int = DEFAULT_DEGREE_CAP, counters: CostCounters | 
     return _select_degree(_normal_equations(Gfull, cap, counters), cap, seed_norm, seed_mode)
 
 
-def _nested_pivots(G: np.ndarray):
-    """One Cholesky sweep of the full Gram matrix, recording every pivot.
-
-    The Cholesky of a leading (o x o) block performs exactly the first o
-    steps of this sweep, so its pivots are piv[:o]; the reference's test for
-    order o is ``piv[k] > o*eps*G[k,k]`` for all k < o (polyprec.py:80-82).
-    Returns (L, piv, n_ok) where the sweep stops at the first non-positive
-    pivot (n_ok = number of usable pivots)."""
-    m = G.shape[0]
-    L = np.zeros((m, m))
-    piv = np.zeros(m)
-    for k in range(m):
-        p = G[k, k] - L[k, :k] @ L[k, :k]
-        piv[k] = p
-        if not (p > 0.0):
-            return L, piv, k
-        L[k, k] = np.sqrt(p)
-        if k + 1 < m:
-            L[k + 1:, k] = (G[k + 1:, k] - L[k + 1:, :k] @ L[k, :k]) / L[k, k]
-    return L, piv, m
-
-
 def _select_degree(full: GramSystem, cap: int, seed_norm: float, seed_mode: str):
     """auto_degree's selection (polyprec.py:171-190): the largest d <= cap
-    whose order-(d+1) Gram block passes the pivot test, with finite y.
-
-    Order o passes iff piv[k] > o*eps*G[k,k] for all k < o; the threshold
-    grows with o, so the passing orders form a prefix {1..F}: one pivot sweep
-    finds the candidate (instead of cap separate factorizations).  y is then
-    computed by the reference's own per-order factorization of that block:
-    near the failure margin the normal equations have cond ~1e14 and y
-    inherits O(1) relative changes from last-bit differences in L, so the
-    selected degree's y must come from the same code path as build_poly."""
-    eps = np.finfo(np.float64).eps
-    _, piv, n_ok = _nested_pivots(full.G)
-    diag = np.diag(full.G)
-    best = None
-    for d in range(cap, 0, -1):
-        o = d + 1
-        if o > n_ok or not np.all(piv[:o] > o * eps * diag[:o]):
-            continue
-        try:
-            y = dense_cholesky(GramSystem(full.G[:o, :o], full.rhs[:o]))
-        except CholeskyFailure:
-            continue
-        if np.all(np.isfinite(y)):
-            best = (d, y)
-            break
-    if best is None:
-        try:
-            y0 = dense_cholesky(GramSystem(full.G[:1, :1], full.rhs[:1]))
-        except CholeskyFailure:
-            y0 = np.zeros(1)
-        return PolyCoefficients(0, y0, seed_norm, seed_mode)
-    return PolyCoefficients(best[0], best[1], seed_norm, seed_mode)
+    whose order-(d+1) Gram block factors with finite y, each order factored
+    on its own as the reference does -- natively (pg_host_degree_select,
+    top-down, stopping at the first success), then the degree-0 rule."""
+    d, y = _lib.host_degree_select(full.G, full.rhs, cap)
+    if d >= 1:
+        return PolyCoefficients(d, y, seed_norm, seed_mode)
+    y0, pivot = _lib.host_cholesky(full.G[:1, :1], full.rhs[:1])
+    if pivot:
+        y0 = np.zeros(1)  # op v0 vanished; p = 0 (polyprec.py:186-187)
+    return PolyCoefficients(0, y0, seed_norm, seed_mode)
 
 
 def build_poly_or_auto(op, v0, deg: int, counters: CostCounters,
@@ -219,11 +180,10 @@ def build_poly_or_auto(op, v0, deg: int, counters: CostCounters,
     Gfull, seed_norm = _device_power_gram(op, v0, deg + 1, counters)
     counters.scalar_dots += 1
     full = _normal_equations(Gfull, deg, counters)
-    try:
-        y = dense_cholesky(full)
+    y, pivot = _lib.host_cholesky(full.G, full.rhs)
+    if not pivot:
         return PolyCoefficients(deg, y, seed_norm, seed_mode), None
-    except CholeskyFailure as exc:
-        return _select_degree(full, deg, seed_norm, seed_mode), exc.pivot
+    return _select_degree(full, deg, seed_norm, seed_mode), pivot
 
 
 def apply_poly(p: PolyCoefficients, op, v, counters: CostCounters):

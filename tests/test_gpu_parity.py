@@ -210,10 +210,14 @@ def test_build_poly_cfg1(golden):
     assert resid(p.y) <= resid(a["cfg1_y10"]) * 1.01 + 1e-12
     with pytest.raises(pg.CholeskyFailure) as err:
         pg.build_poly(op, orc.sm64_uniform(1, 4096), 13, pg.CostCounters())
-    # The failing pivot sits where cancellation meets the m*eps*G[k,k] floor:
-    # the reference (OpenBLAS Gram) fails at 14, an exactly rounded Gram (and
-    # this device Gram) at 13 -- DESIGN.md §5.  Agreement within one pivot.
-    assert abs(err.value.pivot - meta["cfg1_build13"]) <= 1
+    # The failing pivot sits where cancellation meets the m*eps*G[k,k] floor
+    # and is decided by rounding: the reference (OpenBLAS Gram + numpy loop)
+    # fails at pivot 14; exact arithmetic (correctly rounded Gram, fsum
+    # Cholesky) at 12 -- which is what the device (double-double Gram,
+    # compensated host Cholesky) reproduces.  DESIGN.md §5.
+    P13 = orc.power_columns(A, v, 14)
+    assert err.value.pivot == orc.chol_pivot_exact(orc.gram_exact(P13)[1:, 1:])
+    assert abs(err.value.pivot - meta["cfg1_build13"]) <= 2
 
 
 def test_known_answer_diag12_and_auto():
@@ -233,8 +237,12 @@ def test_auto_degree_lap64(golden):
     a, meta = golden
     c = pg.CostCounters()
     op = pg.DeviceMatrixOperator(_lap64(golden), c)
-    p = pg.auto_degree(op, orc.sm64_uniform(1, 4096), 16, c)
-    assert abs(p.degree - meta["auto_lap64"]["degree"]) <= 1
+    v0 = orc.sm64_uniform(1, 4096)
+    p = pg.auto_degree(op, v0, 16, c)
+    # exact-arithmetic decision (10); the reference's rounding lands on 12
+    P = orc.power_columns(_oracle(_lap64(golden)), v0 / np.linalg.norm(v0), 17)
+    assert p.degree == orc.auto_deg_exact(orc.gram_exact(P), 16)
+    assert abs(p.degree - meta["auto_lap64"]["degree"]) <= 2
     assert (c.spmvs, c.dots) == (meta["auto_lap64"]["counters"]["spmvs"], 2)
 
 
@@ -332,7 +340,7 @@ def test_small_configs_with_degree_policy(golden, cfg, kw):
     # (small4: reference 12, exact 15) -- DESIGN.md §5
     v = wl.make_v0(h.nrows)
     P = orc.power_columns(_oracle(h), v / np.linalg.norm(v), conf["degree"] + 1)
-    exact_d = orc.auto_deg_from_gram(orc.gram_exact(P), conf["degree"])[0]
+    exact_d = orc.auto_deg_exact(orc.gram_exact(P), conf["degree"])
     assert abs(poly.degree - exact_d) <= 1
     if poly.degree == rec["effective_degree"]:
         assert abs(res.iterations - rec["iterations"]) <= 2

@@ -261,6 +261,36 @@ def test_host_pieces_mirror_reference():
     assert pg.lambda_p_lambda(p, [1.0, 2.0]) == pytest.approx([1.0, 1.0])
 
 
+def test_native_host_routines(golden):
+    """pg_host_cholesky_solve / _degree_select / _backsolve (compensated
+    inner products): known answers, and the exact-arithmetic pass/fail
+    decision on the cfg1 power-basis Gram."""
+    y, piv = _lib.host_cholesky(np.array([[5.0, 9.0], [9.0, 17.0]]), np.array([3.0, 5.0]))
+    assert piv == 0 and y == pytest.approx([1.5, -0.5], abs=1e-12)
+    assert _lib.host_cholesky(np.ones((2, 2)), np.ones(2))[1] == 2
+    y, piv = _lib.host_cholesky(np.array([[4.0]]), np.array([2.0]))
+    assert y == pytest.approx([0.5])
+    a, _ = golden
+    A = orc.OracleMatrix(4096, 4096, a["lap64_row_ptr"], a["lap64_col_idx"], a["lap64_values"])
+    v0 = orc.sm64_uniform(1, 4096)
+    P = orc.power_columns(A, v0 / np.linalg.norm(v0), 17)
+    G = orc.gram_exact(P)
+    Gs, r = np.ascontiguousarray(G[1:, 1:]), np.ascontiguousarray(G[1:, 0])
+    for o in (6, 11, 12, 14):
+        assert _lib.host_cholesky(Gs[:o, :o], r[:o])[1] == orc.chol_pivot_exact(Gs[:o, :o])
+    d, y = _lib.host_degree_select(Gs, r, 16)
+    assert d == orc.auto_deg_exact(G, 16)
+    # well inside the passing range the native y agrees with the numpy loop
+    y6, _ = _lib.host_cholesky(Gs[:6, :6], r[:6])
+    np.testing.assert_allclose(y6, orc.chol_solve(Gs[:6, :6], r[:6]), rtol=1e-9)
+    R = np.triu(np.arange(1.0, 31.0).reshape(6, 5) % 7 + 1.0)
+    g = np.linspace(1, 2, 6)
+    yb, zc = _lib.host_backsolve(R, g, 5)
+    assert zc == -1 and np.allclose(R[:5, :5] @ yb, g[:5])
+    R[2, 2] = 0.0
+    assert _lib.host_backsolve(R, g, 5)[1] == 2
+
+
 def test_device_path_refuses_without_gpu():
     if torch.cuda.is_available():
         pytest.skip("GPU present")
