@@ -254,19 +254,21 @@ def run_ours(args):
     per_step = [a.elapsed_time(b) / 1e3 for a, b in times]
     total = sum(per_step)
     # kernel-level roofline of the dominant kernel (fused polynomial pass)
-    # e.timer: (start, end, algorithmic bytes, passes) per fused chain of d
-    # back-to-back polynomial passes (events on the launching stream)
-    kt = sum(a.elapsed_time(b) for a, b, _, _ in e.timer) / 1e3
-    kb = sum(nb for _, _, nb, _ in e.timer)
-    nk = sum(np_ for _, _, _, np_ in e.timer)
+    # e.timer: (start, end, algorithmic bytes of the stored format, passes,
+    # uncompressed-equivalent bytes) per fused chain of d back-to-back
+    # polynomial passes (events on the launching stream)
+    kt = sum(t[0].elapsed_time(t[1]) for t in e.timer) / 1e3
+    kb = sum(t[2] for t in e.timer)
+    nk = sum(t[3] for t in e.timer)
+    kb12 = sum(t[4] for t in e.timer)
     e.timer = None
     if world > 1:
         t = torch.tensor([total, kt], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total, kt = float(t[0]), float(t[1])
-        kb_t = torch.tensor([kb], dtype=torch.float64, device=dev)
+        kb_t = torch.tensor([kb, kb12], dtype=torch.float64, device=dev)
         dist.all_reduce(kb_t)
-        kb = float(kb_t[0])
+        kb, kb12 = float(kb_t[0]), float(kb_t[1])
 
     poly, pivot, res, c = results[-1]
 
@@ -344,6 +346,10 @@ def run_ours(args):
                 "kernel_s_per_step": kt / args.steps,
                 "share_of_step": kt / total if total else None,
                 "algorithmic_bytes_per_launch": kb / max(nk, 1),
+                "matrix_format": ("dictionary SELL (1 B offset + 1 B value index)"
+                                  if st.get("val_bytes") == 1 else
+                                  "SELL-C-sigma (int32 column + f64 value)"),
+                "uncompressed_equivalent_gbs": (kb12 / kt / 1e9) if kt > 0 else None,
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": 16 * N,

@@ -484,7 +484,7 @@ class Engine:
             s0 = self.shards[0]
             ev0 = torch.cuda.Event(enable_timing=True)
             ev0.record(torch.cuda.current_stream(s0.device))
-            nbytes = 0
+            nbytes = nbytes12 = 0
         for k in range(1, d + 1):
             last = k == d
             flags = (_lib.PG_PASS_FIRST if k == 1 else 0) | (0 if last else _lib.PG_PASS_WRITE_W)
@@ -502,13 +502,14 @@ class Engine:
                     # then the epilogue's vector traffic
                     vec = 8 * (int(k > 1) + 1 + int(not last) + int(b is not None))
                     nbytes += s.entry_bytes * s.nnz + (12 + vec) * s.n
+                    nbytes12 += 12 * s.nnz + (12 + vec) * s.n
             if not last:
                 self.halo(nxt)
                 cur = nxt
         if timing:
             ev1 = torch.cuda.Event(enable_timing=True)
             ev1.record(torch.cuda.current_stream(s0.device))
-            self.timer.append((ev0, ev1, nbytes, d))
+            self.timer.append((ev0, ev1, nbytes, d, nbytes12))
 
     def slot(self, i):
         """Per-shard 1-element device scalar slot i (0..7) after the coefficients."""
