@@ -177,10 +177,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one GPU per rank over NCCL; --dist-backend gloo lets several ranks share
+    # fewer GPUs (host-staged exchanges, for validating the distributed path)
+    ndev = torch.cuda.device_count()
+    local_dev = local if args.dist_backend == "nccl" else local % max(ndev, 1)
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     conf = wl.CONFIGS[args.config]
     N = wl.config_n(conf)
 
@@ -449,6 +456,7 @@ def main():
     ap.add_argument("--max-iters", type=int, default=200000)
     ap.add_argument("--cpu-sample-iters", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

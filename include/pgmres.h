@@ -135,8 +135,10 @@ PG_API int pg_normalize(const double* d_x, const double* d_nsq, int64_t n, doubl
                         void* stream);
 
 /* ---- polynomial construction / recovery helpers ---------------------------
- * pg_gram: G = P^T P for the ncols columns of P (full symmetric ncols x ncols,
- * row-major) -- the Gram blocks of _normal_equations (polyprec.py:115-122).
+ * pg_gram: G = P^T P for the ncols columns of P -- the Gram blocks of
+ * _normal_equations (polyprec.py:115-122) -- accumulated in double-double;
+ * d_G receives 2*ncols^2 doubles: G rounded (full symmetric, row-major) then
+ * the rounding remainder, so shards can be combined in double-double.
  * pg_gemv: out = V[:, :k] y (gmres.py:326), y a device array of k doubles.
  * pg_dot: d_out[0] = sum x*y (np.linalg.norm's squared sum, gmres.py:241).
  * pg_scale_add: out = (base ? base + a*v : a*v) (polyprec.py:205, gmres.py:330).

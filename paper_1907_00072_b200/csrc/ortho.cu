@@ -223,8 +223,14 @@ __global__ void __launch_bounds__(kTileThreads)
       int i = 0, rem = p;
       while (rem >= k - i) { rem -= k - i; ++i; }
       const int j = i + rem;
-      out[i * k + j] = hi + lo;
-      out[j * k + i] = hi + lo;
+      // G = hi_r + lo_r exactly-ish: hi_r is G rounded to double, lo_r the
+      // remainder, so shards can be combined in double-double (Engine.gram)
+      const double hr = hi + lo;
+      const double lr = (hi - hr) + lo;
+      out[i * k + j] = hr;
+      out[j * k + i] = hr;
+      out[k * k + i * k + j] = lr;
+      out[k * k + j * k + i] = lr;
     }
     if (threadIdx.x == 0) *counter = 0u;
   } else {
@@ -785,7 +791,7 @@ static void launch_tile(const double* V, int64_t ld, int k, const double* z, int
   }
   const int64_t ntiles = (n + kTileRows - 1) / kTileRows;
   if (ntiles == 0) {
-    PG_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * (MODE == kGram ? k * k : k), st));
+    PG_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * (MODE == kGram ? 2 * k * k : k), st));
     return;
   }
   int g = grid_cache[MODE][k][dev];

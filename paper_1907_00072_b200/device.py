@@ -263,22 +263,42 @@ class DistComm:
         self.shards = shards
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # gloo moves CPU tensors only: device buffers are staged through the
+        # host (host-logic tests, and several ranks sharing one GPU in the GPU
+        # tests -- host-mediated, so no kernel ever waits on another rank)
+        self.staged = dist.get_backend(group) == "gloo"
 
     def halo(self, xs):
         dist = self.dist
         s = self.shards[0]
         x = xs[0]
-        ops = []
+        ops, landing = [], []
         for q in sorted(s.plan.send):
-            ops.append(dist.P2POp(dist.isend, s.packed_send(x, q), q, self.group))
+            buf = s.packed_send(x, q)
+            if self.staged and buf.is_cuda:
+                buf = buf.cpu()
+            ops.append(dist.P2POp(dist.isend, buf, q, self.group))
         for q, (off, cnt) in sorted(s.plan.recv.items()):
-            ops.append(dist.P2POp(dist.irecv, x[off:off + cnt], q, self.group))
+            dst = x[off:off + cnt]
+            if self.staged and dst.is_cuda:
+                tmp = torch.empty(cnt, dtype=dst.dtype)
+                landing.append((dst, tmp))
+                dst = tmp
+            ops.append(dist.P2POp(dist.irecv, dst, q, self.group))
         if ops:
             for r in dist.batch_isend_irecv(ops):
                 r.wait()
+        for dst, tmp in landing:
+            dst.copy_(tmp)
 
     def allreduce(self, bufs):
-        self.dist.all_reduce(bufs[0], group=self.group)
+        b = bufs[0]
+        if self.staged and b.is_cuda:
+            h = b.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            b.copy_(h)
+        else:
+            self.dist.all_reduce(b, group=self.group)
 
 
 def exchange_send_lists(shards, comm):
@@ -606,11 +626,30 @@ class Engine:
             _lib.call("pg_gemv", ptr(V), s.ld, k, ptr(s.coef), s.n, ptr(o), s.stream)
 
     def gram(self, Ps, ncols) -> np.ndarray:
-        outs = [torch.zeros(ncols * ncols, dtype=F64, device=s.device) for s in self.shards]
+        """Global Gram matrix of the first ncols columns.  Each shard returns
+        its double-double partial (hi | lo); partials are summed in
+        double-double in shard order on the host (all_gather when distributed),
+        so G -- and with it the Cholesky degree decision -- does not depend on
+        the number of shards."""
+        kk = ncols * ncols
+        outs = [torch.zeros(2 * kk, dtype=F64, device=s.device) for s in self.shards]
         for s, P, o in zip(self._each(), Ps, outs):
             _lib.call("pg_gram", ptr(P), s.ld, ncols, s.n, ptr(o), s.ws, s.stream)
-        self.comm.allreduce(outs)
-        return outs[0].cpu().numpy().reshape(ncols, ncols)
+        parts = [o.cpu().numpy() for o in outs]
+        if self.comm.distributed:
+            src = torch.from_numpy(parts[0]) if self.comm.staged else outs[0]
+            gathered = [torch.zeros_like(src) for _ in range(self.comm.world)]
+            self.comm.dist.all_gather(gathered, src, group=self.comm.group)
+            parts = [g.cpu().numpy() for g in gathered]
+        hi = np.zeros(kk)
+        lo = np.zeros(kk)
+        for p in parts:  # TwoSum accumulation of every shard's (hi, lo)
+            for x in (p[:kk], p[kk:]):
+                s = hi + x
+                bb = s - hi
+                lo = lo + ((hi - (s - bb)) + (x - bb))
+                hi = s
+        return (hi + lo).reshape(ncols, ncols)
 
     def copy(self, src, dst):
         for s, a, b in zip(self.shards, src, dst):
