@@ -189,13 +189,28 @@ __device__ __forceinline__ double row_sum_dict(const SellArgs& a, int64_t base, 
   const uint32_t* __restrict__ cw = reinterpret_cast<const uint32_t*>(a.col8 + base8);
   const uint32_t* __restrict__ vw = reinterpret_cast<const uint32_t*>(a.val8 + base8);
   double acc = 0.0;
+  // index words are software-pipelined two 4-entry chunks ahead: the stall
+  // profile of the non-pipelined loop was dominated by waits on these loads
+  uint32_t cn0 = 0, vn0 = 0, cn1 = 0, vn1 = 0;
+  if (CM) {
+    if (0 < w) cn0 = __ldcs(cw);
+    if (4 < w) cn1 = __ldcs(cw + PG_SLICE);
+  }
+  if (VM) {
+    if (0 < w) vn0 = __ldcs(vw);
+    if (4 < w) vn1 = __ldcs(vw + PG_SLICE);
+  }
   for (int j = 0; j < w; j += 4) {
     const int q = j >> 2;
-    uint32_t cbits = 0, vbits = 0;
+    const uint32_t cbits = cn0, vbits = vn0;
+    cn0 = cn1;
+    vn0 = vn1;
+    if (j + 8 < w) {
+      if (CM) cn1 = __ldcs(cw + (q + 2) * PG_SLICE);
+      if (VM) vn1 = __ldcs(vw + (q + 2) * PG_SLICE);
+    }
     int c[4];
     double v[4], xv[4];
-    if (CM) cbits = __ldcs(cw + q * PG_SLICE);
-    if (VM) vbits = __ldcs(vw + q * PG_SLICE);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (!CM) c[u] = (j + u < w) ? __ldcs(a.col + base + (int64_t)(j + u) * PG_SLICE) : 0;
@@ -228,8 +243,12 @@ __device__ __forceinline__ void finish_resid(double local, double* partials, uns
 // ------------------------------------------------------------ plain kernel --
 // CM / VM: 1 = the column / value stream is dictionary-compressed (1-byte
 // indices into the per-matrix tables, staged in shared memory per block).
+#ifndef PG_SELL_DICT_MIN_BLOCKS
+#define PG_SELL_DICT_MIN_BLOCKS 4
+#endif
 template <int MODE, int CM, int VM>
-__global__ void __launch_bounds__(kSellThreads, kSellMinBlocks)
+__global__ void __launch_bounds__(kSellThreads,
+                                  (CM || VM) ? PG_SELL_DICT_MIN_BLOCKS : kSellMinBlocks)
     sell_kernel(SellArgs a, const double* __restrict__ x, Epi e, double* partials,
                 unsigned int* counter, double* nsq) {
   pdl_entry();

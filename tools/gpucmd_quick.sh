@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests -q -m "gpu" > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log; grep -E "^E |^FAILED|Error" gpurun_out/pytest_gpu.log | head -12
-python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 2 --warmup 1 --no-cpu-baseline --dist-backend gloo > gpurun_out/bench_dist.log 2>&1; echo rc=$?; grep -o '"degree_effective": [0-9]*\|"iterations": [0-9]*' gpurun_out/bench_dist.log
-python bench.py --no-cpu-baseline > gpurun_out/bench_q.log 2>&1; grep -o '"value": [0-9.]*, "unit": "s", "n_gpus\|"median": [0-9.]*\|"frac": [0-9.]*\|"degree_effective": [0-9]*\|"iterations": [0-9]*' gpurun_out/bench_q.log | tr '\n' ' '; echo
+timeout 900 python -m pytest tests -q -m "gpu" -k "spmv or poly" > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
+python tools/spmv_bench.py 2>&1 | grep plain | head -3 | cut -c1-90
