@@ -672,12 +672,22 @@ static size_t tile_smem(int mode, int k, int stages) {
   return b;
 }
 
-// Ring depth.  Phase 1 (pure dots) wants the deepest ring that fits one CTA;
-// phase 2 also runs a serial k-long row projection per tile, so it keeps two
-// CTAs per SM (more warps to hide it) and takes the deepest ring that allows
-// that (cgs2_bench: k=51, n=8M phase 2 5.3 TB/s at 2x2 stages vs 3.3 at 1x4).
+// Ring depth: the deepest ring (<= 4 stages) that still lets `ctas` CTAs
+// share an SM.  Co-resident CTAs hide each other's reduction phases (phase 2
+// also runs a serial k-long row projection per tile): with 1 CTA x 4 stages
+// phase 2 at k=51, n=8M ran at 3.3 TB/s, with 2 x 2 at 5.3.
 static int tile_stages(int mode, int k) {
-  const size_t per_sm = (mode == kUpdDots) ? kTileSmemMax / 2 : kTileSmemMax;
+  // PG_TILE_CTAS_P{1,2,3}: CTAs per SM the ring is sized for (experiments)
+  static int ctas_env[4] = {-1, -1, -1, -1};
+  if (ctas_env[mode] < 0) {
+    const char* names[4] = {"", "PG_TILE_CTAS_P1", "PG_TILE_CTAS_P2", "PG_TILE_CTAS_P3"};
+    const char* s = std::getenv(names[mode]);
+    ctas_env[mode] = s ? std::atoi(s) : 0;
+  }
+  // sweep (tools/cgs2_sweep.py, n = 1e6 and 8e6): 3 co-resident CTAs up to
+  // k = 40, 2 beyond, for both dot phases; the Gram keeps one deep ring
+  int ctas = ctas_env[mode] > 0 ? ctas_env[mode] : (mode == kGram ? 1 : (k <= 40 ? 3 : 2));
+  const size_t per_sm = kTileSmemMax / ctas;
   for (int s = 4; s > 2; --s)
     if (tile_smem(mode, k, s) <= per_sm) return s;
   return 2;
