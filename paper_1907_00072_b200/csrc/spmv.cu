@@ -11,15 +11,18 @@
 // epilogue of the same pass: acc <- acc + y_k * (A w)[row], so a degree-d
 // application streams A exactly d times with no separate axpy kernels.
 //
-// Two kernels share that row arithmetic:
-//  * sell_tma_kernel (default): one persistent CTA per SM.  A producer warp
-//    streams "units" (runs of consecutive slices, <= kUnitEntries entries) of
-//    the index and value arrays into a kStages-deep shared-memory ring with
-//    cp.async.bulk + mbarrier transaction counts; 8 consumer warps take the
-//    slices round-robin, issue all x gathers of a row chunk at once and run
-//    the epilogue.  The matrix stream never waits on the gather latency.
-//  * sell_kernel: plain grid of one-row-per-thread loads, for matrices with a
-//    slice too wide for a ring stage.
+// Kernels sharing that row arithmetic:
+//  * sell_kernel<MODE, 0, 0> (default for general matrices): one row per
+//    thread; all index / value loads of a 4-entry chunk are issued before its
+//    gathers, and the epilogue operands before the row's gathers.
+//  * sell_kernel<MODE, 1, 1> (default when both streams fit a 256-entry
+//    dictionary -- constant-coefficient stencils): 1-byte column-offset and
+//    value indices packed 4 per 32-bit lane word (abi.cu), decoded through
+//    shared-memory tables; ~2 B of matrix stream per entry instead of 12.
+//  * sell_tma_kernel (opt-in, PG_SPMV_TMA=1): one persistent CTA per SM, a
+//    producer warp streams runs of slices into a shared-memory ring with
+//    cp.async.bulk + mbarrier; measured slower than sell_kernel (the gathers,
+//    not the matrix stream, bound it), kept for reference.
 
 #include <cstdlib>
 
