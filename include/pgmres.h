@@ -110,6 +110,34 @@ PG_API int pg_poly_pass(const pg_matrix* mat, const double* d_x, const double* d
                         const double* d_base, double* d_acc_out, double* d_w_out,
                         double y0, double yk, int flags, void* stream);
 
+/* One pass of the ROOT-PRODUCT form of the same polynomial (SURVEY row f1,
+ * BASELINE north_star "root-product terms, complex-conjugate root pairs in
+ * real arithmetic, running sum"): with pi(z) = 1 - z p(z) = prod (1 - z/theta_i)
+ * and the invariant prod = v - A y (Loe & Morgan's running sum):
+ *   PG_ROOT_REAL   (c1 = 1/theta):  ax = A x; v_out = x - c1*ax; y_out = y_in + c1*x
+ *                  [+ c3*v_out: a trailing real root folded in]
+ *   PG_ROOT_PAIR_A (c1 = 1/|theta|^2, c2 = 2 Re theta):  ax = A x;
+ *                  t2 = c2*x - ax -> v_out; y_out = y_in + c1*t2
+ *   PG_ROOT_PAIR_B (c1 = 1/|theta|^2):  ax = A x (x = t2); v_out = p - c1*ax
+ *                  [+ y_out = y_in + c3*v_out when c3 != 0]
+ * d_y_in may be NULL (running sum starts at zero); v_out may be NULL when the
+ * product is not needed again (the final pass); y_out may be NULL when only the
+ * product is wanted.
+ *   | PG_ROOT_RESID (with REAL or PAIR_B; y_in = v, y_out = NULL):
+ *                  v_out = v - (p - c1*ax) -- the last factor of pi(A) v, giving
+ *                  A p(A) v = v - pi(A) v directly (the Arnoldi step's
+ *                  d+1 passes then never read or write a running sum).
+ * d SpMV passes for a degree-d polynomial, like the monomial form; not
+ * bit-identical to apply_poly (different evaluation order), parity within the
+ * north_star's 1e-10 relative bound at the usable degrees. */
+#define PG_ROOT_REAL 0
+#define PG_ROOT_PAIR_A 1
+#define PG_ROOT_PAIR_B 2
+#define PG_ROOT_RESID 4
+PG_API int pg_root_pass(const pg_matrix* mat, const double* d_x, const double* d_p,
+                        const double* d_y_in, double* d_y_out, double* d_v_out, double c1,
+                        double c2, double c3, int mode, void* stream);
+
 /* r = b - A x and the partial sum of r^2 into d_nsq[0] (gmres.py:334-335). */
 PG_API int pg_residual(const pg_matrix* mat, const double* d_x, const double* d_b,
                        double* d_r, double* d_nsq, pg_workspace* ws, void* stream);

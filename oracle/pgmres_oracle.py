@@ -129,6 +129,32 @@ def poly_eval(y, op, v, tally):
     return total
 
 
+def poly_eval_extended(y, op, v):
+    """``p(A) v`` by the monomial running power in x87 extended precision
+    (np.longdouble, 64-bit mantissa): the accuracy yardstick for the
+    root-product form (the reference evaluates only the monomial
+    form, polyprec.py:193-212, whose own fp64 error grows with the cancellation
+    max|y_k A^k v|/|p(A)v| -- SURVEY A.5).  Per row a sequential sum in stored
+    order, like ``matvec``."""
+    y = np.asarray(y, dtype=np.longdouble)
+    vals = np.asarray(op.values, dtype=np.longdouble)
+    rp = np.asarray(op.row_ptr, dtype=np.int64)
+    nz = rp[1:] > rp[:-1]
+
+    def mv(x):
+        out = np.zeros(op.nrows, dtype=np.longdouble)
+        if len(vals):
+            out[nz] = np.add.reduceat(vals * x[op.col_idx], rp[:-1][nz])
+        return out
+
+    cur = np.asarray(v, dtype=np.longdouble)
+    total = y[0] * cur
+    for yk in y[1:]:
+        cur = mv(cur)
+        total = total + yk * cur
+    return total.astype(np.float64)
+
+
 def wrapped_apply(y, op, v, tally):
     """``A p(A) v`` (gmres.py:112-113)."""
     return op.apply(poly_eval(y, op, v, tally))

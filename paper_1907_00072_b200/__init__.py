@@ -42,6 +42,10 @@ _LAZY = {
     "build_poly_or_auto": "polyprec",
     "dense_cholesky": "polyprec",
     "lambda_p_lambda": "polyprec",
+    "RootPlan": "polyprec",
+    "root_plan": "polyprec",
+    "leja_order": "polyprec",
+    "residual_poly_roots": "polyprec",
     "icgs": "ortho",
     "OrthoResult": "ortho",
 }

@@ -25,6 +25,10 @@ PG_SLICE = 32
 PG_KMAX = 64
 PG_PASS_FIRST = 1
 PG_PASS_WRITE_W = 2
+PG_ROOT_REAL = 0
+PG_ROOT_PAIR_A = 1
+PG_ROOT_PAIR_B = 2
+PG_ROOT_RESID = 4
 
 _i64 = C.c_int64
 _i32 = C.c_int
@@ -47,6 +51,7 @@ _SIGNATURES = {
     "pg_spmv": ([_p, _p, _p, _p], C.c_int),
     "pg_poly_pass": ([_p, _p, _p, _p, _p, _p, _d, _d, _i32, _p], C.c_int),
     "pg_residual": ([_p, _p, _p, _p, _p, _p, _p], C.c_int),
+    "pg_root_pass": ([_p, _p, _p, _p, _p, _p, _d, _d, _d, _i32, _p], C.c_int),
     "pg_cgs2_phase1": ([_p, _i64, _i32, _p, _i64, _p, _p, _p], C.c_int),
     "pg_cgs2_phase2": ([_p, _i64, _i32, _p, _i64, _p, _p, _p, _p], C.c_int),
     "pg_cgs2_phase3": ([_p, _i64, _i32, _p, _i64, _p, _p, _p, _p, _p, _p], C.c_int),
@@ -109,7 +114,7 @@ def check(code: int, what: str = ""):
 
 #: entry points that launch exactly one libpgmres kernel per call
 LAUNCHING = frozenset({
-    "pg_spmv", "pg_poly_pass", "pg_residual", "pg_cgs2_phase1", "pg_cgs2_phase2",
+    "pg_spmv", "pg_poly_pass", "pg_root_pass", "pg_residual", "pg_cgs2_phase1", "pg_cgs2_phase2",
     "pg_cgs2_phase3", "pg_normalize", "pg_gram", "pg_gemv", "pg_dot", "pg_scale_add",
     "pg_gather",
 })

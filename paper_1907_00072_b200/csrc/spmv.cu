@@ -31,7 +31,7 @@
 
 namespace pg {
 
-enum SellMode { kSpmv = 0, kPoly = 1, kResid = 2 };
+enum SellMode { kSpmv = 0, kPoly = 1, kResid = 2, kRoot = 3 };
 
 constexpr int kSellThreads = 256;
 // Occupancy floor and row-chunk unroll of the plain kernel, chosen by sweep
@@ -103,6 +103,10 @@ struct Epi {
   const double* b;
   double y0, yk;
   int flags;
+  // kRoot (root-product form, PG_ROOT_*): acc_in = y_in, acc_out = y_out,
+  // w_out = v_out, base = p_in; c1 = 1/|theta|^2 or 1/theta, c2 = 2 Re(theta),
+  // c3 = folded trailing real root (0 = none)
+  double c1, c2, c3;
 };
 
 __device__ __forceinline__ int64_t lane_row(const SellArgs& a, int64_t lane) {
@@ -125,6 +129,9 @@ __device__ __forceinline__ Pre epi_load(const Epi& e, const double* __restrict__
     if (e.base) p.b = e.base[row];
   } else if (MODE == kResid) {
     p.a = e.b[row];
+  } else if (MODE == kRoot) {
+    p.a = ((e.flags & 3) == PG_ROOT_PAIR_B) ? e.base[row] : x[row];
+    if (e.acc_in) p.b = e.acc_in[row];
   }
   return p;
 }
@@ -142,10 +149,34 @@ __device__ __forceinline__ double epilogue(const Epi& e, const Pre& p, int64_t r
     if (e.base) t = __dadd_rn(p.b, t);
     e.acc_out[row] = t;
     return 0.0;
-  } else {
+  } else if (MODE == kResid) {
     const double r = __dsub_rn(p.a, ax);
     e.acc_out[row] = r;
     return r;
+  } else {
+    // root-product step (Loe-Morgan running sum): p.a = operand / prod row,
+    // p.b = running sum y (or v for the PG_ROOT_RESID final pass)
+    const int mode = e.flags & 3;
+    const bool resid = (e.flags & PG_ROOT_RESID) != 0;
+    if (mode == PG_ROOT_PAIR_A) {
+      const double t2 = __fma_rn(e.c2, p.a, -ax);   // 2 Re(theta) prod - A prod
+      if (e.w_out) e.w_out[row] = t2;
+      if (e.acc_out) e.acc_out[row] = __fma_rn(e.c1, t2, p.b);  // y + t2 / |theta|^2
+    } else {
+      // REAL: prod - A prod / theta;  PAIR_B: prod - A t2 / |theta|^2
+      const double pn = __fma_rn(-e.c1, ax, p.a);
+      if (resid) {
+        e.w_out[row] = __dsub_rn(p.b, pn);          // A p(A) v = v - pi(A) v
+      } else {
+        if (e.w_out) e.w_out[row] = pn;
+        if (e.acc_out) {
+          double y = (mode == PG_ROOT_REAL) ? __fma_rn(e.c1, p.a, p.b) : p.b;
+          if (e.c3 != 0.0) y = __fma_rn(e.c3, pn, y);  // folded trailing real root
+          e.acc_out[row] = y;
+        }
+      }
+    }
+    return 0.0;
   }
 }
 
@@ -406,7 +437,7 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
   static int sms[64] = {};
   if (!sms[dev]) PG_CUDA(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
   if (m->use_tma && !m->col8 && !m->val8) {  // the ring streams the uncompressed arrays
-    static bool attr[3][64] = {};
+    static bool attr[4][64] = {};
     if (!attr[MODE][dev]) {
       PG_CUDA(cudaFuncSetAttribute(sell_tma_kernel<MODE>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
@@ -468,6 +499,25 @@ PG_API int pg_poly_pass(const pg_matrix* mat, const double* d_x, const double* d
                "w_out required with PG_PASS_WRITE_W");
     Epi e{d_acc_in, d_base, d_acc_out, d_w_out, nullptr, y0, yk, flags};
     launch_sell<kPoly>(mat, d_x, e, nullptr, nullptr, as_stream(stream));
+  });
+}
+
+PG_API int pg_root_pass(const pg_matrix* mat, const double* d_x, const double* d_p,
+                        const double* d_y_in, double* d_y_out, double* d_v_out, double c1,
+                        double c2, double c3, int mode, void* stream) {
+  return guard([&] {
+    PG_REQUIRE(mat && d_x, PG_ERR_PARAMETER, "null argument");
+    const int m = mode & 3;
+    const bool resid = (mode & PG_ROOT_RESID) != 0;
+    PG_REQUIRE((mode & ~(3 | PG_ROOT_RESID)) == 0 && m <= PG_ROOT_PAIR_B, PG_ERR_PARAMETER,
+               "unknown root-pass mode");
+    PG_REQUIRE(m != PG_ROOT_PAIR_B || d_p, PG_ERR_PARAMETER, "PAIR_B needs p");
+    PG_REQUIRE(!resid || (m != PG_ROOT_PAIR_A && d_y_in && d_v_out && !d_y_out),
+               PG_ERR_PARAMETER, "PG_ROOT_RESID: REAL/PAIR_B with v in y_in, output in v_out");
+    PG_REQUIRE(d_y_out || d_v_out, PG_ERR_PARAMETER, "pass writes nothing");
+    // d_y_in == nullptr: the running sum starts from zero
+    Epi e{d_y_in, d_p, d_y_out, d_v_out, nullptr, 0.0, 0.0, mode, c1, c2, c3};
+    launch_sell<kRoot>(mat, d_x, e, nullptr, nullptr, as_stream(stream));
   });
 }
 

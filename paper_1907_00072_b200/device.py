@@ -531,6 +531,102 @@ class Engine:
             ev1.record(torch.cuda.current_stream(s0.device))
             self.timer.append((ev0, ev1, nbytes, d, nbytes12))
 
+    def poly_roots(self, plan, vs, out, t, p0, p1, base=None):
+        """out = (base +) p(A) v in root-product form (polyprec.RootPlan): one
+        fused ``pg_root_pass`` per step, the running sum y in ``out`` (seeded
+        with ``base``), the product in p0/p1 (ping-pong: every pass gathers
+        it), the pair temporary in t.  vs is never written."""
+        if plan.degree == 0:
+            for s, v, o, b in zip(self._each(), vs, out, base or [None] * self.P):
+                _lib.call("pg_scale_add", ptr(b) if b is not None else None, plan.y0, ptr(v), s.n,
+                          ptr(o), s.stream)
+            return
+        self.halo(vs)
+        prod = vs
+        bufs = (p0, p1)
+        nb = 0
+        timing = self.timer is not None and self.P == 1
+        if timing:
+            s0 = self.shards[0]
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev0.record(torch.cuda.current_stream(s0.device))
+            nbytes = nbytes12 = 0
+        first = True
+        for mode, c1, c2, c3, keep in plan.steps:
+            if mode == _lib.PG_ROOT_PAIR_B:
+                x, p, w = t, prod, (bufs[nb] if keep else None)
+            elif mode == _lib.PG_ROOT_PAIR_A:
+                x, p, w = prod, None, (t if keep else None)
+            else:
+                x, p, w = prod, None, (bufs[nb] if keep else None)
+            writes_y = mode != _lib.PG_ROOT_PAIR_B or c3 != 0.0
+            for i, s in enumerate(self._each()):
+                yin = (base[i] if base is not None else None) if first else out[i]
+                _lib.call("pg_root_pass", s.mat, ptr(x[i]), ptr(p[i]) if p is not None else None,
+                          ptr(yin) if (writes_y and yin is not None) else None,
+                          ptr(out[i]) if writes_y else None, ptr(w[i]) if w is not None else None,
+                          c1, c2, c3, mode, s.stream)
+                if timing:
+                    # entry stream + row lengths + x gather, then the epilogue:
+                    # p read (PAIR_B), y read (unless seeded from zero), y/w writes
+                    vec = 8 * (int(p is not None) + int(writes_y and yin is not None)
+                               + int(writes_y) + int(w is not None))
+                    nbytes += s.entry_bytes * s.nnz + (12 + vec) * s.n
+                    nbytes12 += 12 * s.nnz + (12 + vec) * s.n
+            if writes_y:
+                first = False
+            if w is not None:
+                self.halo(w)
+                if mode != _lib.PG_ROOT_PAIR_A:
+                    prod = w
+                    nb ^= 1
+        if timing:
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev1.record(torch.cuda.current_stream(s0.device))
+            self.timer.append((ev0, ev1, nbytes, plan.degree, nbytes12))
+
+    def wrapped_roots(self, plan, vs, z, t, p0, p1):
+        """z = A p(A) v = v - pi(A) v (RootPlan.resid_steps): d+1 fused passes
+        that carry only the product -- no running sum is read or written, so
+        each pass moves 16 B/row of vectors instead of the monomial's 32."""
+        if not plan.resid_steps:  # p == 0
+            for s, v, o in zip(self._each(), vs, z):
+                _lib.call("pg_scale_add", None, 0.0, ptr(v), s.n, ptr(o), s.stream)
+            return
+        self.halo(vs)
+        prod = vs
+        bufs = (p0, p1)
+        nb = 0
+        timing = self.timer is not None and self.P == 1
+        if timing:
+            s0 = self.shards[0]
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev0.record(torch.cuda.current_stream(s0.device))
+            nbytes = nbytes12 = 0
+        for mode, c1, c2, c3, _ in plan.resid_steps:
+            m = mode & 3
+            resid = bool(mode & _lib.PG_ROOT_RESID)
+            x = t if m == _lib.PG_ROOT_PAIR_B else prod
+            p = prod if m == _lib.PG_ROOT_PAIR_B else None
+            w = z if resid else (t if m == _lib.PG_ROOT_PAIR_A else bufs[nb])
+            for i, s in enumerate(self._each()):
+                _lib.call("pg_root_pass", s.mat, ptr(x[i]), ptr(p[i]) if p is not None else None,
+                          ptr(vs[i]) if resid else None, None, ptr(w[i]), c1, c2, c3, mode,
+                          s.stream)
+                if timing:
+                    vec = 8 * (1 + int(p is not None) + int(resid))  # w, [p], [v]
+                    nbytes += s.entry_bytes * s.nnz + (12 + vec) * s.n
+                    nbytes12 += 12 * s.nnz + (12 + vec) * s.n
+            if not resid:
+                self.halo(w)
+                if m != _lib.PG_ROOT_PAIR_A:
+                    prod = w
+                    nb ^= 1
+        if timing:
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev1.record(torch.cuda.current_stream(s0.device))
+            self.timer.append((ev0, ev1, nbytes, len(plan.resid_steps), nbytes12))
+
     def slot(self, i):
         """Per-shard 1-element device scalar slot i (0..7) after the coefficients."""
         return [s.scal[2 * KMAX + i:2 * KMAX + i + 1] for s in self.shards]

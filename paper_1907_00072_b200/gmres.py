@@ -31,7 +31,7 @@ from .errors import (
     SingularHessenbergError,
 )
 from .ortho import breakdown_test
-from .polyprec import PolyCoefficients, apply_poly
+from .polyprec import POLY_FORMS, PolyCoefficients, apply_poly, root_plan
 
 
 class PolynomialWrappedOperator:
@@ -55,8 +55,16 @@ class GmresConfig:
     tol: float = 1e-8
     max_iters: int = 200000
     record_history: bool = True
+    # "monomial" (default): the reference's running-power evaluation, bit-
+    # identical.  "roots": the same polynomial as a Leja-ordered root product
+    # (polyprec.RootPlan) -- same SpMV count, half the vector
+    # traffic per Arnoldi pass, and accurate at degrees where the monomial
+    # form's cancellation is not.  Not a reference field.
+    poly_form: str = "monomial"
 
     def __post_init__(self):
+        if self.poly_form not in POLY_FORMS:
+            raise ParameterError(f"poly_form must be one of {POLY_FORMS}")
         if self.restart_m < 1:
             raise ParameterError("restart_m must be at least 1")
         if not (0.0 < self.tol < 1.0):
@@ -173,6 +181,7 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
     tol = config.tol
 
     poly = right_prec if right_prec else None  # reference truthiness (gmres.py:261)
+    plan = root_plan(poly) if (poly is not None and config.poly_form == "roots") else None
     bs = e.ingest(b)
     W = _Workspace(e, m)
     xs = e.vecs()
@@ -184,7 +193,7 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
         e.dot(bs, bs, slot=4, fetch=False)
         e.copy(bs, W.r)
         e.normalize_dev(W.r, e.slot(4), W.col(0))
-        early = _launch_step(e, W, poly, 0)
+        early = _launch_step(e, W, poly, 0, plan)
         norm_b = math.sqrt(e.read_slot(4))
     else:
         norm_b = math.sqrt(e.dot(bs, bs, slot=4))
@@ -222,7 +231,7 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
         else:
             # V[:, 0] = r / beta: beta = sqrt(nsq) with nsq still in device slot 4
             e.normalize_dev(W.r, e.slot(4), W.col(0))
-            handle = _launch_step(e, W, poly, 0)
+            handle = _launch_step(e, W, poly, 0, plan)
         g[0] = beta
         j = 0
         breakdown = False
@@ -235,7 +244,7 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
             # step is abandoned unused (no counter, no history row).
             ahead = None
             if j + 1 < m and total_iters + 1 < config.max_iters:
-                ahead = _launch_step(e, W, poly, j + 1)
+                ahead = _launch_step(e, W, poly, j + 1, plan)
             c1, c2, nsq = e.cgs2_fetch(handle)
             handle = ahead
             if poly is not None:
@@ -291,7 +300,10 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
         if poly is not None:
             counters.spmvs += d
             counters.vector_updates += d + 1
-            e.poly(poly.y, W.t, xs, W.acc, W.w0, W.w1, base=xs)  # x = x + p(A)(V y)
+            if plan is not None:
+                e.poly_roots(plan, W.t, xs, W.acc, W.w0, W.w1, base=xs)
+            else:
+                e.poly(poly.y, W.t, xs, W.acc, W.w0, W.w1, base=xs)  # x = x + p(A)(V y)
         else:
             e.add(xs, W.t, xs)
         counters.vector_updates += 1
@@ -310,12 +322,15 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
                        cycles)
 
 
-def _launch_step(e, W, poly, j):
+def _launch_step(e, W, poly, j, plan=None):
     """Queue Arnoldi step j on the device: w = A p(A) v_j (d fused passes +
-    the wrapper SpMV, gmres.py:112-113, 283) and its CGS2 against
-    v_0..v_j writing v_{j+1} (ortho.py:53-70).  Returns the scalar handle."""
+    the wrapper SpMV, gmres.py:112-113, 283 -- or, in root form, d+1 passes
+    ending in v - pi(A) v) and its CGS2 against v_0..v_j writing v_{j+1}
+    (ortho.py:53-70).  Returns the scalar handle."""
     vj = W.col(j)
-    if poly is not None:
+    if plan is not None:
+        e.wrapped_roots(plan, vj, W.z, W.acc, W.w0, W.w1)
+    elif poly is not None:
         e.poly(poly.y, vj, W.t, W.acc, W.w0, W.w1)
         e.spmv(W.t, W.z)
     else:

@@ -186,9 +186,151 @@ def build_poly_or_auto(op, v0, deg: int, counters: CostCounters,
     return _select_degree(full, deg, seed_norm, seed_mode), pivot
 
 
-def apply_poly(p: PolyCoefficients, op, v, counters: CostCounters):
+POLY_FORMS = ("monomial", "roots")
+
+
+@dataclass(frozen=True)
+class RootPlan:
+    """Root-product form of ``p``.
+
+    With ``pi(z) = 1 - z p(z) = prod_i (1 - z/theta_i)`` (degree d+1, the
+    GMRES residual polynomial, roots = harmonic Ritz values), the running sum
+    ``prod <- prod - A prod/theta, y <- y + prod/theta`` keeps
+    ``prod = v - A y`` and ends with ``y = p(A) v``.  A complex-conjugate pair
+    is one real quadratic step (two SpMVs, ``PG_ROOT_PAIR_A`` then
+    ``PG_ROOT_PAIR_B``); the last root needs no SpMV, so the plan is exactly d
+    fused passes, like the monomial form.  ``steps`` holds
+    ``(mode, c1, c2, c3, keep_prod)`` per pass (include/pgmres.h)."""
+
+    degree: int
+    roots: np.ndarray
+    steps: tuple
+    y0: float  # degree-0 fallback (no roots needed)
+    # d+1 passes giving A p(A) v = v - pi(A) v (the Arnoldi step's wrapped
+    # operator): every root's factor, no running sum, the last one PG_ROOT_RESID
+    resid_steps: tuple = ()
+
+
+def leja_order(roots: np.ndarray) -> np.ndarray:
+    """Modified Leja ordering with conjugate pairs adjacent (θ with Im > 0
+    first): start at the largest modulus, then repeatedly take the root that
+    maximises the product of distances to those already taken (log-summed)."""
+    roots = np.asarray(roots, dtype=np.complex128)
+    units = [complex(r) for r in roots if r.imag >= 0]
+    if sum(2 if u.imag > 0 else 1 for u in units) != len(roots):
+        raise ParameterError("roots are not closed under conjugation")
+    taken: list = []
+    out: list = []
+    while units:
+        if not taken:
+            i = int(np.argmax([abs(u) for u in units]))
+        else:
+            t = np.asarray(taken)
+            score = [np.sum(np.log(np.abs(u - t) + 0.0)) for u in units]
+            i = int(np.argmax(score))
+        u = units.pop(i)
+        members = [u, u.conjugate()] if u.imag > 0 else [u]
+        taken += members
+        out += members
+    return np.asarray(out)
+
+
+def residual_poly_roots(y: np.ndarray) -> np.ndarray:
+    """Roots of ``pi(z) = 1 - sum_k y_k z^{k+1}``; conjugate pairs exact
+    (companion-matrix eigenvalues of a real polynomial)."""
+    y = np.asarray(y, dtype=np.float64)
+    coeffs = np.concatenate([-y[::-1], [1.0]])  # highest degree first
+    r = np.roots(coeffs)
+    # a real polynomial's complex eigenvalues come in exact conjugate pairs;
+    # snap any residual asymmetry so each pair is one real quadratic step
+    cplx = r[r.imag != 0]
+    pos = np.sort_complex(cplx[cplx.imag > 0])
+    neg = np.sort_complex(np.conj(cplx[cplx.imag < 0]))
+    if len(pos) != len(neg) or not np.allclose(pos, neg, rtol=1e-12, atol=0):
+        raise ParameterError("residual polynomial roots are not conjugate-closed")
+    real = _polish(y, r[r.imag == 0].real.astype(np.complex128))
+    pos = _polish(y, pos)
+    return np.concatenate([real.real.astype(np.complex128), pos, pos.conj()])
+
+
+def _polish(y: np.ndarray, roots: np.ndarray, iters: int = 4) -> np.ndarray:
+    """Newton steps on pi in extended precision (np.clongdouble).  The
+    companion-matrix roots carry ~1e-10 relative error at degree 10 on cfg1,
+    which the running sum turns into a ~1e-10 error in p(A)v; polished roots
+    bring the root form to ~3e-14 of the extended-precision p(A)v, below the
+    reference monomial's own rounding."""
+    if len(roots) == 0:
+        return roots
+    c = np.concatenate([[1.0], -np.asarray(y, dtype=np.float64)]).astype(np.longdouble)
+    z = np.asarray(roots).astype(np.clongdouble)
+    for _ in range(iters):
+        f = np.zeros_like(z)
+        df = np.zeros_like(z)
+        for ck in c[::-1]:  # Horner for pi and pi'
+            df = df * z + f
+            f = f * z + ck
+        ok = df != 0
+        z = np.where(ok, z - np.where(ok, f / np.where(ok, df, 1), 0), z)
+    z = z.astype(np.complex128)
+    # a step that wandered (clustered roots) keeps the companion root
+    moved = np.abs(z - roots) > 1e-6 * np.abs(roots)
+    return np.where(moved | ~np.isfinite(z), roots, z)
+
+
+def root_plan(p: PolyCoefficients) -> RootPlan:
+    """Leja-ordered pass plan of ``p`` for ``Engine.poly_roots``."""
+    if p.degree == 0:
+        th = 1.0 / float(p.y[0]) if p.y[0] != 0.0 else None
+        rs = ((_lib.PG_ROOT_REAL | _lib.PG_ROOT_RESID, float(p.y[0]), 0.0, 0.0, True),) \
+            if th is not None else ()
+        return RootPlan(0, np.zeros(0, np.complex128), (), float(p.y[0]), rs)
+    order = leja_order(residual_poly_roots(p.y))
+    units = []
+    i = 0
+    while i < len(order):
+        th = order[i]
+        if th.imag > 0:
+            units.append(("pair", th))
+            i += 2
+        else:
+            units.append(("real", th.real))
+            i += 1
+    steps = []
+    for j, (kind, th) in enumerate(units):
+        last = j == len(units) - 1
+        nxt_fold = (not last and j + 1 == len(units) - 1 and units[j + 1][0] == "real")
+        c3 = 1.0 / units[j + 1][1] if nxt_fold else 0.0
+        if kind == "real":
+            if last:
+                break  # folded into the previous pass (c3)
+            steps.append((_lib.PG_ROOT_REAL, 1.0 / th, 0.0, c3, not nxt_fold))
+        else:
+            m2 = th.real * th.real + th.imag * th.imag
+            steps.append((_lib.PG_ROOT_PAIR_A, 1.0 / m2, 2.0 * th.real, 0.0, not last))
+            if not last:
+                steps.append((_lib.PG_ROOT_PAIR_B, 1.0 / m2, 0.0, c3, not nxt_fold))
+    if len(steps) != p.degree:
+        raise ParameterError(f"root plan has {len(steps)} passes for degree {p.degree}")
+    rsteps = []
+    for kind, th in units:
+        if kind == "real":
+            rsteps.append((_lib.PG_ROOT_REAL, 1.0 / th, 0.0, 0.0, True))
+        else:
+            m2 = th.real * th.real + th.imag * th.imag
+            rsteps.append((_lib.PG_ROOT_PAIR_A, 1.0 / m2, 2.0 * th.real, 0.0, True))
+            rsteps.append((_lib.PG_ROOT_PAIR_B, 1.0 / m2, 0.0, 0.0, True))
+    mode, c1, c2, c3, _ = rsteps[-1]
+    rsteps[-1] = (mode | _lib.PG_ROOT_RESID, c1, c2, c3, True)
+    return RootPlan(p.degree, order, tuple(steps), float(p.y[0]), tuple(rsteps))
+
+
+def apply_poly(p: PolyCoefficients, op, v, counters: CostCounters, form: str = "monomial"):
     """``p(op) v`` (polyprec.py:193-212): ``degree`` fused SpMV passes,
-    ``degree + 1`` counted vector updates.  Bit-identical to the reference."""
+    ``degree + 1`` counted vector updates.  ``form="monomial"`` is bit-identical
+    to the reference; ``form="roots"`` evaluates the same polynomial as its
+    Leja-ordered root product (``RootPlan``), also ``degree`` passes."""
+    if form not in POLY_FORMS:
+        raise ParameterError(f"unknown polynomial form {form!r}")
     e = _engine(op)
     if isinstance(v, np.ndarray) or not isinstance(v, torch.Tensor):
         vv = np.asarray(v, dtype=np.float64)
@@ -201,7 +343,10 @@ def apply_poly(p: PolyCoefficients, op, v, counters: CostCounters):
     out, acc, w0, w1 = e.vecs(), e.vecs(), e.vecs(), e.vecs()
     op.counters.spmvs += p.degree
     counters.vector_updates += p.degree + 1
-    e.poly(p.y, vs, out, acc, w0, w1)
+    if form == "roots":
+        e.poly_roots(root_plan(p), vs, out, acc, w0, w1)
+    else:
+        e.poly(p.y, vs, out, acc, w0, w1)
     return e.emit(out, v)
 
 

@@ -297,3 +297,70 @@ def test_device_path_refuses_without_gpu():
     import paper_1907_00072_b200 as pg
     with pytest.raises(pg.DeviceError):
         pg.DeviceMatrixOperator(wl.laplacian2d(4))
+
+
+def _simulate_root_plan(plan, A, v):
+    """numpy stand-in for the pg_root_pass epilogues (include/pgmres.h) driven
+    by the product's host RootPlan -- checks the plan logic without a GPU."""
+    prod, t, y = v.copy(), None, np.zeros_like(v)
+    for mode, c1, c2, c3, keep in plan.steps:
+        if mode == _lib.PG_ROOT_REAL:
+            ax = A.matvec(prod)
+            pn = prod - c1 * ax
+            y = y + c1 * prod + c3 * pn
+            prod = pn
+        elif mode == _lib.PG_ROOT_PAIR_A:
+            t = c2 * prod - A.matvec(prod)
+            y = y + c1 * t
+        else:
+            prod = prod - c1 * A.matvec(t)
+            y = y + c3 * prod
+    return y
+
+
+@pytest.mark.parametrize("key", ["cfg1_sweep_1_y", "cfg1_sweep_4_y", "cfg1_sweep_8_y", "cfg1_y10",
+                                 "cfg1_sweep_12_y"])
+def test_root_plan_matches_monomial(golden, key):
+    """Root-product plan (SURVEY §8 f1): d passes, conjugate pairs adjacent;
+    the running sum is within 1e-12 of the extended-precision p(A)v, and
+    within the north_star's 1e-10 of the reference's fp64 monomial wherever
+    the monomial itself is that accurate (deg <= 10; at deg 12 the monomial
+    is 2.9e-10 off the extended value while the root form is 1.7e-13)."""
+    import paper_1907_00072_b200 as pg
+    a, _ = golden
+    A = orc.OracleMatrix(4096, 4096, a["lap64_row_ptr"], a["lap64_col_idx"], a["lap64_values"])
+    y = a[key]
+    p = pg.PolyCoefficients(len(y) - 1, y, 1.0)
+    plan = pg.root_plan(p)
+    assert len(plan.steps) == p.degree
+    r = plan.roots
+    for i in range(len(r)):  # each complex root is followed by its conjugate
+        if r[i].imag > 0:
+            assert r[i + 1] == np.conj(r[i])
+    pi = np.polynomial.polynomial.polyval(r, np.concatenate([[1.0], -y]))
+    assert np.max(np.abs(pi)) < 1e-8
+    b = a["cfg1_b"]
+    ref = orc.poly_eval(y, A, b, orc.Tally())
+    ext = orc.poly_eval_extended(y, A, b)
+    got = _simulate_root_plan(plan, A, b)
+    rel = lambda u, w: np.linalg.norm(u - w) / np.linalg.norm(w)
+    assert rel(got, ext) < 1e-12
+    assert rel(got, ext) <= rel(ref, ext) + 1e-15
+    if p.degree <= 10:
+        assert rel(got, ref) < 1e-10
+
+
+def test_leja_order_pairs_and_start():
+    import paper_1907_00072_b200 as pg
+    r = np.array([1.0, 3 + 1j, 3 - 1j, -0.5, 10.0])
+    o = pg.leja_order(r.astype(complex))
+    assert o[0] == 10.0 and sorted(o, key=lambda z: (z.real, z.imag)) == \
+        sorted(r.astype(complex), key=lambda z: (z.real, z.imag))
+    i = list(o).index(3 + 1j)
+    assert o[i + 1] == 3 - 1j
+    with pytest.raises(pg.ParameterError):
+        pg.leja_order(np.array([1 + 1j, 2.0]))
+    p0 = pg.root_plan(pg.PolyCoefficients(0, np.array([2.0]), 1.0))
+    assert p0.steps == () and p0.y0 == 2.0
+    with pytest.raises(pg.ParameterError):
+        pg.apply_poly(p0, None, np.zeros(1), pg.CostCounters(), form="chebyshev")
