@@ -219,7 +219,7 @@ def run_ours(args):
     v0_dev = torch.from_numpy(v0_host).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
-    cfg = pg.GmresConfig(conf["m"], conf["tol"], args.max_iters)
+    cfg = pg.GmresConfig(conf["m"], conf["tol"], args.max_iters, poly_form=args.poly_form)
 
     def step(b, v0):
         c = pg.CostCounters()
@@ -331,7 +331,7 @@ def run_ours(args):
                 "n": N, "nnz": int(nnz_local) if world == 1 else None,
                 "restart_m": conf["m"], "tol": conf["tol"],
                 "degree_requested": conf["degree"], "degree_effective": poly.degree,
-                "build_poly_failed_pivot": pivot,
+                "build_poly_failed_pivot": pivot, "poly_form": args.poly_form,
                 "iterations": res.iterations, "cycles": res.cycles,
                 "converged": bool(res.converged), "final_relres": res.final_relres,
                 "spmvs": c.spmvs, "dots": c.dots,
@@ -457,6 +457,9 @@ def main():
     ap.add_argument("--cpu-sample-iters", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    # "monomial" = the reference's bit-identical evaluation (default, the
+    # headline); "roots" = the Leja root-product form
+    ap.add_argument("--poly-form", default="monomial", choices=["monomial", "roots"])
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -157,6 +157,9 @@ static void free_matrix(pg_matrix* m) {
   cudaFree(m->dtab);
   cudaFree(m->val8);
   cudaFree(m->vtab);
+  cudaFree(m->wtab);
+  cudaFree(m->pair8);
+  cudaFree(m->ptab);
   cudaSetDevice(cur);
   delete m;
 }
@@ -190,6 +193,65 @@ static bool dict_encode(const std::vector<K>& keys, std::vector<uint8_t>& idx,
 // The 1-byte streams use a packed slice layout: entry j of lane t of slice s
 // sits at slice_ptr8[s] + (j/4)*128 + 4t + (j%4), so one 32-bit load per lane
 // brings 4 entries (a warp-wide load is one contiguous 128 B segment).
+// Window plan (pg_matrix::wtab): natural row order only (the block's rows
+// must be contiguous), offsets clustered greedily -- a gap of >= kWinRows
+// between consecutive offsets starts a new group (merging would cost more
+// window than a second group's kWinRows rows).  Group starts are rounded down
+// to an even offset and lengths up to even, so every window copy is a
+// 16-byte aligned bulk copy.  No plan when the groups or a pipeline stage
+// exceed their budgets (the global-gather dictionary kernel runs).
+static std::vector<int32_t> build_window_plan(const std::vector<int64_t>& offs,
+                                              const std::vector<int64_t>& sp8, int64_t n_slices,
+                                              pg_matrix* m) {
+  const char* env = std::getenv("PG_SPMV_WIN");
+  if (env && std::atoi(env) == 0) return {};
+  if (m->sigma > 1 || offs.empty()) return {};
+  std::vector<int64_t> srt(offs);
+  std::sort(srt.begin(), srt.end());
+  std::vector<int64_t> lo, hi;
+  for (int64_t o : srt) {
+    if (lo.empty() || o - hi.back() >= kWinRows) {
+      lo.push_back(o);
+      hi.push_back(o);
+    } else {
+      hi.back() = o;
+    }
+  }
+  if ((int)lo.size() > kWinMaxGroups) return {};
+  int64_t total = 0;
+  std::vector<int64_t> len(lo.size());
+  for (size_t g = 0; g < lo.size(); ++g) {
+    if (lo[g] & 1) lo[g] -= 1;  // even start (floor for negatives too)
+    len[g] = kWinRows + (hi[g] - lo[g]);
+    len[g] += len[g] & 1;
+    total += len[g];
+  }
+  if (total > kWinMaxElems) return {};
+  const int64_t per_blk = kWinRows / PG_SLICE;
+  int64_t b8 = 0;
+  for (int64_t s0 = 0; s0 < n_slices; s0 += per_blk)
+    b8 = std::max(b8, sp8[std::min(s0 + per_blk, n_slices)] - sp8[s0]);
+  // window | pair stream | 2 epilogue operand slices | row lengths | widths
+  const int64_t stage = ((8 * total + 127) / 128) * 128 + b8 + 20 * kWinRows + 128;
+  if (stage > kWinMaxStageBytes) return {};
+  std::vector<int32_t> wtab(256, 0);
+  int32_t start = 0;
+  for (size_t g = 0; g < lo.size(); ++g) {
+    m->wlo[g] = (int32_t)lo[g];
+    m->wstart[g] = start;
+    m->wlen[g] = (int32_t)len[g];
+    start += m->wlen[g];
+  }
+  for (size_t i = 0; i < offs.size(); ++i) {
+    const size_t g = (size_t)(std::upper_bound(lo.begin(), lo.end(), offs[i]) - lo.begin()) - 1;
+    wtab[i] = (int32_t)(m->wstart[g] + (offs[i] - lo[g]));
+  }
+  m->n_wgrp = (int)lo.size();
+  m->win_elems = (int)total;
+  m->win_b8 = (int)b8;
+  return wtab;
+}
+
 static void build_dictionaries(const SellHost& h, const int32_t* col, const double* val,
                                pg_matrix* m) {
   const char* env = std::getenv("PG_SPMV_DICT");
@@ -214,6 +276,7 @@ static void build_dictionaries(const SellHost& h, const int32_t* col, const doub
     }
   }
   bool any = false;
+  std::vector<int32_t> wtab;  // window plan (empty: none)
   std::vector<uint8_t> c8, v8;
   std::vector<int64_t> dtab64;
   std::vector<uint64_t> vtab_bits;
@@ -233,11 +296,37 @@ static void build_dictionaries(const SellHost& h, const int32_t* col, const doub
       m->dtab = upload(dtab.data(), dtab.size(), m->bytes);
       m->n_dcol = (int)dtab64.size();
       any = true;
+      wtab = build_window_plan(dtab64, sp8, h.n_slices, m);
     }
   }
   {
     std::vector<double> vtab(256, 0.0);
     for (size_t i = 0; i < vtab_bits.size(); ++i) std::memcpy(&vtab[i], &vtab_bits[i], 8);
+    // pair dictionary: one byte per entry indexes (column offset, value) --
+    // 27 pairs for a 27-point stencil; read by the pair kernels (spmv.cu)
+    const char* penv = std::getenv("PG_SPMV_PAIR");
+    const char* renv = std::getenv("PG_SPMV_WIN_MIN_ROW");
+    // the windowed kernel pays off on long rows (27-point: 1.6x the pair
+    // kernel); short rows (7-point) keep the global-gather pair kernel
+    const int64_t min_row = renv ? std::atoll(renv) : 12;
+    if (m->nnz < min_row * m->nrows) wtab.clear();
+    if (m->col8 && !(penv && std::atoi(penv) == 0)) {
+      std::vector<uint16_t> pk(P);
+      for (size_t i = 0; i < P; ++i) pk[i] = (uint16_t)((c8[i] << 8) | v8[i]);
+      std::vector<uint8_t> p8;
+      std::vector<uint16_t> pkeys;
+      if (dict_encode(pk, p8, pkeys, std::hash<uint16_t>())) {
+        std::vector<PairEnt> ptab(256);
+        for (size_t k = 0; k < pkeys.size(); ++k) {
+          ptab[k].v = vtab[pkeys[k] & 255];
+          ptab[k].woff = wtab.empty() ? 0 : 8 * wtab[pkeys[k] >> 8];
+          ptab[k].doff = (int32_t)dtab64[pkeys[k] >> 8];
+        }
+        m->pair8 = upload(p8.data(), P, m->bytes);
+        m->ptab = upload(ptab.data(), ptab.size(), m->bytes);
+        if (!wtab.empty()) m->wtab = upload(wtab.data(), wtab.size(), m->bytes);
+      }
+    }
     m->val8 = upload(v8.data(), P, m->bytes);
     m->vtab = upload(vtab.data(), vtab.size(), m->bytes);
     m->n_dval = (int)vtab_bits.size();

@@ -70,6 +70,17 @@ struct pg_matrix {
   uint8_t* val8;       // [padded] dictionary index of the value bits, or null
   double* vtab;        // [256]    value dictionary
   int n_dcol, n_dval;  // dictionary sizes (0 = stream not compressed)
+  // x-window plan of the windowed dictionary kernel (spmv.cu): the column
+  // offsets cluster into n_wgrp groups [wlo, wlo + wlen - kWinRows]; a block of
+  // kWinRows natural-order rows reads x only inside the group windows, which
+  // it stages in shared memory (group g at wstart[g]).  wtab[i] = smem
+  // position of dictionary offset i for the block's first row.
+  int32_t* wtab;       // [256] or null (no window plan)
+  uint8_t* pair8;      // packed 1-byte index of the (column offset, value) pair
+  void* ptab;          // [256] PairEnt {value, window byte offset, column offset}
+  int n_wgrp, win_elems;
+  int win_b8;          // largest per-block byte span of each packed stream
+  int32_t wlo[32], wstart[32], wlen[32];
   int32_t* unit_slice; // [n_units+1] first slice of each TMA streaming unit
   int64_t n_units;
   bool use_tma;        // every slice fits a ring stage (kUnitEntries)
@@ -78,8 +89,28 @@ struct pg_matrix {
 };
 
 namespace pg {
+// One entry of the pair dictionary: the value and the byte offset of its
+// column inside the block's x window (relative to the row's own slot).
+struct __align__(16) PairEnt {
+  double v;
+  int32_t woff;  // byte offset in the block's x window (0 without a window plan)
+  int32_t doff;  // column offset col - row (global-gather kernel)
+};
 // Entries per TMA streaming unit of the SpMV ring (12 B each: int32 + f64).
 constexpr int kUnitEntries = 3072;
+// Rows per block of the windowed dictionary SpMV and its window budget
+// (elements per buffer; two buffers per block).
+#ifndef PG_WIN_ROWS
+#define PG_WIN_ROWS 256
+#endif
+constexpr int kWinRows = PG_WIN_ROWS;
+constexpr int kWinMaxGroups = 32;
+constexpr int kWinMaxElems = 6144;
+#ifndef PG_WIN_STAGES
+#define PG_WIN_STAGES 2
+#endif
+constexpr int kWinStages = PG_WIN_STAGES;
+constexpr int kWinMaxStageBytes = (220 * 1024) / kWinStages / 128 * 128;
 // Number of per-block partial slots a reduction may use.
 constexpr int kMaxBlocks = 1024;
 // Per-block partial slots: the Gram stores (hi, lo) for each of the

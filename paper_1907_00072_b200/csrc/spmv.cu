@@ -215,7 +215,9 @@ __device__ __forceinline__ double row_sum(ColPtr cp, Dec dec, ValPtr vp, int w, 
 // entries of each packed 1-byte stream (CM: column offsets, VM: values);
 // uncompressed streams keep their regular SELL positions.  Same sequential
 // order and separately rounded products as row_sum.
-template <int CM, int VM>
+// WIN = 1: x is the block's shared-memory window, `row` the row's index in
+// the block and s_dtab the window-position table (pg_matrix::wtab).
+template <int CM, int VM, int WIN = 0>
 __device__ __forceinline__ double row_sum_dict(const SellArgs& a, int64_t base, int64_t base8,
                                                int row, int w, int len,
                                                const double* __restrict__ x,
@@ -256,7 +258,8 @@ __device__ __forceinline__ double row_sum_dict(const SellArgs& a, int64_t base, 
       if (VM) v[u] = s_vtab[(vbits >> (8 * u)) & 255u];
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) xv[u] = (j + u < len) ? __ldg(x + c[u]) : 0.0;
+    for (int u = 0; u < 4; ++u)
+      xv[u] = (j + u < len) ? (WIN ? x[c[u]] : __ldg(x + c[u])) : 0.0;
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (j + u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
@@ -319,6 +322,259 @@ __global__ void __launch_bounds__(kSellThreads,
     }
     const double r = epilogue<MODE>(e, pre, row, ax);
     if (MODE == kResid) local = __fma_rn(r, r, local);
+  }
+  finish_resid<MODE>(local, partials, counter, nsq);
+}
+
+// ------------------------------------------------------ pair dictionary --
+// One byte per entry (pair8) indexing {value, column offset} in a shared
+// table; x gathered from global memory (L1/L2).  Index words are
+// software-pipelined two 4-entry chunks ahead; full chunks run without
+// predicates, only the row's last partial chunk is predicated.
+__device__ __forceinline__ double row_sum_pairs_global(const uint32_t* __restrict__ pw, int len,
+                                                       int64_t row,
+                                                       const double* __restrict__ x,
+                                                       const PairEnt* s_ptab) {
+  double acc = 0.0;
+  const int nq = (len + 3) >> 2;
+  uint32_t n0 = 0, n1 = 0;
+  if (nq > 0) n0 = __ldcs(pw);
+  if (nq > 1) n1 = __ldcs(pw + PG_SLICE);
+  const double* xr = x + row;
+  for (int q = 0; q < nq; ++q) {
+    const uint32_t pb = n0;
+    n0 = n1;
+    if (q + 2 < nq) n1 = __ldcs(pw + (q + 2) * PG_SLICE);
+    const int left = len - 4 * q;
+    PairEnt pe[4];
+    double xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) pe[u] = s_ptab[(pb >> (8 * u)) & 255u];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xv[u] = (u < left) ? __ldg(xr + pe[u].doff) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (u < left) acc = __dadd_rn(acc, __dmul_rn(pe[u].v, xv[u]));
+  }
+  return acc;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kSellThreads, PG_SELL_DICT_MIN_BLOCKS)
+    sell_pair_kernel(SellArgs a, const uint8_t* __restrict__ pair8,
+                     const PairEnt* __restrict__ ptab, const double* __restrict__ x, Epi e,
+                     double* partials, unsigned int* counter, double* nsq) {
+  pdl_entry();
+  __shared__ PairEnt s_ptab[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_ptab[i] = ptab[i];
+  __syncthreads();
+  double local = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t lane = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lane < a.nlanes;
+       lane += stride) {
+    const int64_t row = lane_row(a, lane);
+    if (row < 0) continue;
+    const int64_t s = lane >> 5;
+    const int len = __ldg(a.row_len + lane);
+    const int64_t base8 = __ldg(a.slice_ptr8 + s) + 4 * (lane & 31);
+    const Pre pre = epi_load<MODE>(e, x, row);
+    const double ax = row_sum_pairs_global(reinterpret_cast<const uint32_t*>(pair8 + base8), len,
+                                           row, x, s_ptab);
+    const double r = epilogue<MODE>(e, pre, row, ax);
+    if (MODE == kResid) local = __fma_rn(r, r, local);
+  }
+  finish_resid<MODE>(local, partials, counter, nsq);
+}
+
+// ---------------------------------------------------- windowed dictionary --
+// Dictionary-compressed matrices in natural row order (stencils): a block
+// owns kWinRows consecutive rows (8 slices).  Their x reads all fall inside
+// the few group windows of the matrix's window plan (abi.cu
+// build_window_plan), and their packed index words are one contiguous byte
+// range per stream.  One thread streams all of it for the block's next row
+// blocks into a kWinStages-deep shared-memory ring with cp.async.bulk (TMA)
+// completing on an mbarrier, so a stage carries ~15-35 KB of loads in flight
+// per copy batch; the 256 row threads then sum their rows from shared memory
+// only.  Window elements outside [0, ncols) are never referenced by a stored
+// entry and are simply not copied.  Same sequential mul-then-add order per
+// row: bitwise equal to the other kernels.
+struct WinArgs {
+  int ng, total, b8;
+  // byte offsets inside a ring stage: [window | pair stream | epilogue
+  // operand A | operand B | row lengths | slice widths]
+  int off_p8, off_ea, off_eb, off_rl, off_sw, stage_bytes;
+  int64_t ncols, nblk, n_slices;
+  int32_t lo[kWinMaxGroups], start[kWinMaxGroups], len[kWinMaxGroups];
+};
+
+// The epilogue operands a row reads (epi_load), as whole vectors so that the
+// producer can stage the block's slice of them: A -> Pre::a, B -> Pre::b.
+template <int MODE>
+__device__ __forceinline__ void epi_vectors(const Epi& e, const double* x, const double*& A,
+                                            const double*& B) {
+  A = B = nullptr;
+  if (MODE == kPoly) {
+    A = (e.flags & PG_PASS_FIRST) ? x : e.acc_in;
+    B = e.base;
+  } else if (MODE == kResid) {
+    A = e.b;
+  } else if (MODE == kRoot) {
+    A = ((e.flags & 3) == PG_ROOT_PAIR_B) ? e.base : x;
+    B = e.acc_in;
+  }
+}
+
+// Row sum over the pair stream: per entry one byte -> one 16-byte table
+// entry {value, window byte offset} -> one window load, mul, add.  Full
+// 4-entry chunks run without predicates; only the row's last partial chunk
+// is predicated.  Same sequential order as every other kernel.
+__device__ __forceinline__ double row_sum_pairs(const uint32_t* pw, int len,
+                                                const unsigned char* winrow,
+                                                const PairEnt* s_ptab) {
+  double acc = 0.0;
+  const int full = len & ~3;
+  int j = 0;
+#pragma unroll 2
+  for (; j < full; j += 4) {
+    const uint32_t pb = pw[(j >> 2) * PG_SLICE];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const PairEnt pe = s_ptab[(pb >> (8 * u)) & 255u];
+      acc = __dadd_rn(acc, __dmul_rn(pe.v, *reinterpret_cast<const double*>(winrow + pe.woff)));
+    }
+  }
+  if (j < len) {
+    const uint32_t pb = pw[(j >> 2) * PG_SLICE];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      if (j + u < len) {
+        const PairEnt pe = s_ptab[(pb >> (8 * u)) & 255u];
+        acc = __dadd_rn(acc,
+                        __dmul_rn(pe.v, *reinterpret_cast<const double*>(winrow + pe.woff)));
+      }
+    }
+  }
+  return acc;
+}
+
+// Copy n doubles src -> dst (both 16-byte aligned) on `bar`: the even part in
+// one bulk copy, an odd tail by a plain copy (made visible to the consumers
+// by the release of the arrive).  Returns the bulk bytes (0 = nothing).
+__device__ __forceinline__ uint32_t stage_f64_tail(double* dst, const double* src, int64_t n) {
+  if (n & 1) dst[n - 1] = __ldg(src + n - 1);
+  return 8u * (uint32_t)(n & ~(int64_t)1);
+}
+
+// Producer side (one thread): queue row block rb into ring stage `buf`.
+template <int MODE>
+__device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, const Epi& e,
+                                          const uint8_t* __restrict__ pair8,
+                                          const double* __restrict__ x, int64_t rb,
+                                          unsigned char* buf, uint64_t* bar) {
+  double* win = reinterpret_cast<double*>(buf);
+  const int64_t s0 = rb * (kWinRows / PG_SLICE);
+  const int64_t s1 = min(s0 + kWinRows / PG_SLICE, wa.n_slices);
+  const int64_t p0 = __ldg(a.slice_ptr8 + s0), p1 = __ldg(a.slice_ptr8 + s1);
+  const int64_t r0 = rb * kWinRows;
+  const int64_t nr = min((int64_t)kWinRows, a.nrows - r0);
+  const double *A, *B;
+  epi_vectors<MODE>(e, x, A, B);
+  // pass 1: byte count (+ odd tails), so that expect_tx precedes the copies
+  uint32_t bytes = (uint32_t)(p1 - p0) + 4u * (uint32_t)((s1 - s0) * PG_SLICE) +
+                   ((s1 - s0) * 4 % 16 == 0 ? 4u * (uint32_t)(s1 - s0) : 0u);
+  for (int g = 0; g < wa.ng; ++g) {
+    const int64_t ga = r0 + wa.lo[g];
+    const int64_t va = max(ga, (int64_t)0), vb = min(ga + wa.len[g], wa.ncols);
+    if (vb > va) bytes += stage_f64_tail(win + wa.start[g] + (va - ga), x + va, vb - va);
+  }
+  if (A) bytes += stage_f64_tail(reinterpret_cast<double*>(buf + wa.off_ea), A + r0, nr);
+  if (B) bytes += stage_f64_tail(reinterpret_cast<double*>(buf + wa.off_eb), B + r0, nr);
+  int32_t* sw = reinterpret_cast<int32_t*>(buf + wa.off_sw);
+  if ((s1 - s0) * 4 % 16 != 0)  // partial last block: slice widths copied plainly
+    for (int64_t q = s0; q < s1; ++q) sw[q - s0] = __ldg(a.slice_w + q);
+  mbar_expect_tx(bar, bytes);
+  for (int g = 0; g < wa.ng; ++g) {
+    const int64_t ga = r0 + wa.lo[g];
+    const int64_t va = max(ga, (int64_t)0), vb = min(ga + wa.len[g], wa.ncols);
+    const int64_t n2 = (vb - va) & ~(int64_t)1;
+    if (vb > va && n2 > 0)
+      bulk_g2s(win + wa.start[g] + (va - ga), x + va, 8u * (uint32_t)n2, bar);
+  }
+  if (p1 > p0) bulk_g2s(buf + wa.off_p8, pair8 + p0, (uint32_t)(p1 - p0), bar);
+  if (A && nr > 1) bulk_g2s(buf + wa.off_ea, A + r0, 8u * (uint32_t)(nr & ~(int64_t)1), bar);
+  if (B && nr > 1) bulk_g2s(buf + wa.off_eb, B + r0, 8u * (uint32_t)(nr & ~(int64_t)1), bar);
+  bulk_g2s(buf + wa.off_rl, a.row_len + r0, 4u * (uint32_t)((s1 - s0) * PG_SLICE), bar);
+  if ((s1 - s0) * 4 % 16 == 0) bulk_g2s(sw, a.slice_w + s0, 4u * (uint32_t)(s1 - s0), bar);
+}
+
+// Warp-specialised: warp 8 is the producer (one lane issues the copies of
+// the block's row blocks as soon as a ring stage is released), warps 0-7 sum
+// one row per thread from shared memory only -- matrix stream, x window,
+// epilogue operands, row lengths all arrive by TMA -- and release the stage
+// through the `empty` mbarrier.  Global memory is only written (outputs).
+constexpr int kWinThreads = kWinRows + 32;
+
+template <int MODE>
+__global__ void __launch_bounds__(kWinThreads, 1)
+    sell_win_kernel(SellArgs a, WinArgs wa, const uint8_t* __restrict__ pair8,
+                    const PairEnt* __restrict__ ptab, const double* __restrict__ x, Epi e,
+                    double* partials, unsigned int* counter, double* nsq) {
+  pdl_entry();
+  extern __shared__ __align__(128) unsigned char smem_win[];
+  __shared__ PairEnt s_ptab[256];
+  __shared__ __align__(8) uint64_t full[kWinStages];
+  __shared__ __align__(8) uint64_t empty[kWinStages];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_ptab[i] = ptab[i];
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kWinStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kWinRows / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  double local = 0.0;
+  const int warp = threadIdx.x >> 5;
+  if (warp == kWinRows / 32) {
+    if ((threadIdx.x & 31) == 0) {
+      int it = 0;
+      for (int64_t rb = blockIdx.x; rb < wa.nblk; rb += gridDim.x, ++it) {
+        const int st = it % kWinStages;
+        if (it >= kWinStages) mbar_wait(&empty[st], (uint32_t)((it / kWinStages - 1) & 1));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        win_issue<MODE>(a, wa, e, pair8, x, rb, smem_win + (size_t)st * wa.stage_bytes,
+                        &full[st]);
+      }
+    }
+  } else {
+    const double *A, *B;
+    epi_vectors<MODE>(e, x, A, B);
+    const int t = threadIdx.x;
+    const int sl = t >> 5;  // slice of this thread's row inside the block
+    int it = 0;
+    for (int64_t rb = blockIdx.x; rb < wa.nblk; rb += gridDim.x, ++it) {
+      const int st = it % kWinStages;
+      const unsigned char* buf = smem_win + (size_t)st * wa.stage_bytes;
+      const int64_t row = rb * kWinRows + t;
+      mbar_wait(&full[st], (uint32_t)((it / kWinStages) & 1));
+      if (row < a.nrows) {
+        const int32_t* sw = reinterpret_cast<const int32_t*>(buf + wa.off_sw);
+        int off8 = 0;  // packed-stream offset of this slice inside the block
+        for (int q = 0; q < sl; ++q) off8 += ((sw[q] + 3) >> 2) * 4 * PG_SLICE;
+        const int w = sw[sl];
+        const int len = reinterpret_cast<const int32_t*>(buf + wa.off_rl)[t];
+        Pre pre{0.0, 0.0};
+        if (A) pre.a = reinterpret_cast<const double*>(buf + wa.off_ea)[t];
+        if (B) pre.b = reinterpret_cast<const double*>(buf + wa.off_eb)[t];
+        const uint32_t* pw = reinterpret_cast<const uint32_t*>(buf + wa.off_p8 + off8) + (t & 31);
+        (void)w;
+        const double ax = row_sum_pairs(pw, len, buf + 8 * t, s_ptab);
+        const double r = epilogue<MODE>(e, pre, row, ax);
+        if (MODE == kResid) local = __fma_rn(r, r, local);
+      }
+      __syncwarp();
+      if ((t & 31) == 0) mbar_arrive(&empty[st]);
+    }
   }
   finish_resid<MODE>(local, partials, counter, nsq);
 }
@@ -436,7 +692,70 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
   unsigned* cnt = ws ? ws->counter : nullptr;
   static int sms[64] = {};
   if (!sms[dev]) PG_CUDA(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
-  if (m->use_tma && !m->col8 && !m->val8) {  // the ring streams the uncompressed arrays
+  // the window kernel's bulk copies need 16-byte aligned vectors
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+  const bool aligned = al16(x) && al16(e.acc_in) && al16(e.base) && al16(e.b);
+  // windowed kernel: long rows (27-point: 1.6x the pair kernel); short rows
+  // (7-point) keep the global-gather pair kernel, which is faster there
+  const bool win_ok = m->pair8 && m->wtab && aligned;
+  if (win_ok) {
+    WinArgs wa;
+    wa.ng = m->n_wgrp;
+    wa.total = m->win_elems;
+    wa.b8 = m->win_b8;
+    wa.off_p8 = ((8 * wa.total + 127) / 128) * 128;
+    wa.off_ea = wa.off_p8 + wa.b8;
+    wa.off_eb = wa.off_ea + 8 * kWinRows;
+    wa.off_rl = wa.off_eb + 8 * kWinRows;
+    wa.off_sw = wa.off_rl + 4 * kWinRows;
+    wa.stage_bytes = wa.off_sw + 128;
+    wa.ncols = m->ncols;
+    wa.nblk = (m->nrows + kWinRows - 1) / kWinRows;
+    wa.n_slices = m->n_slices;
+    for (int g = 0; g < kWinMaxGroups; ++g) {
+      wa.lo[g] = m->wlo[g];
+      wa.start[g] = m->wstart[g];
+      wa.len[g] = m->wlen[g];
+    }
+    const size_t smem = (size_t)kWinStages * wa.stage_bytes;
+    auto kern = sell_win_kernel<MODE>;
+    static bool attr[4][64] = {};
+    if (!attr[MODE][dev]) {
+      PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(kWinStages * kWinMaxStageBytes)));
+      attr[MODE][dev] = true;
+    }
+    // resident grid: blocks per SM from the occupancy calculator at this
+    // stage size (cached per kernel / device / size) x PG_SPMV_WIN_WAVES
+    static int occ_b[4][64] = {}, occ_n[4][64] = {};
+    if (occ_b[MODE][dev] != wa.stage_bytes) {
+      int nb = 0;
+      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kWinThreads, smem));
+      occ_n[MODE][dev] = nb > 0 ? nb : 1;
+      occ_b[MODE][dev] = wa.stage_bytes;
+    }
+    static int waves = -1;
+    if (waves < 0) {
+      const char* s = std::getenv("PG_SPMV_WIN_WAVES");
+      waves = s ? std::atoi(s) : 1;
+    }
+    int64_t g = waves > 0 ? (int64_t)sms[dev] * occ_n[MODE][dev] * waves : wa.nblk;
+    if (g > wa.nblk) g = wa.nblk;
+    if (MODE == kResid && g > kMaxBlocks) g = kMaxBlocks;
+    launch_k(kern, (int)g, kWinThreads, smem, st, a, wa, (const uint8_t*)m->pair8,
+             (const PairEnt*)m->ptab, x, e, part, cnt, nsq);
+  } else if (m->pair8) {
+    static int per_sm = -1;
+    if (per_sm < 0) {
+      const char* s = std::getenv("PG_SPMV_DICT_BLOCKS_PER_SM");
+      per_sm = s ? std::atoi(s) : 4;
+    }
+    int64_t blocks = (a.nlanes + kSellThreads - 1) / kSellThreads;
+    const int64_t cap = (MODE == kResid) ? kMaxBlocks : (int64_t)sms[dev] * per_sm;
+    if (blocks > cap) blocks = cap;
+    launch_k(sell_pair_kernel<MODE>, (int)blocks, kSellThreads, 0, st, a,
+             (const uint8_t*)m->pair8, (const PairEnt*)m->ptab, x, e, part, cnt, nsq);
+  } else if (m->use_tma && !m->col8 && !m->val8) {  // the ring streams the uncompressed arrays
     static bool attr[4][64] = {};
     if (!attr[MODE][dev]) {
       PG_CUDA(cudaFuncSetAttribute(sell_tma_kernel<MODE>,

@@ -39,32 +39,46 @@ def time_pass(e, reps):
     return dt, nb / dt / 1e9
 
 
+VARIANTS = {
+    "window": {"PG_SPMV_WIN_MIN_ROW": "0"},        # windowed pair kernel (TMA ring)
+    "pair": {"PG_SPMV_WIN": "0"},                  # pair dictionary, global gathers
+    "dict": {"PG_SPMV_WIN": "0", "PG_SPMV_PAIR": "0"},  # two 1-byte streams
+    "plain": {"PG_SPMV_WIN": "0", "PG_SPMV_PAIR": "0", "PG_SPMV_DICT": "0"},  # int32 + f64
+    "default": {},
+}
+ENV_KEYS = ("PG_SPMV_WIN", "PG_SPMV_PAIR", "PG_SPMV_DICT", "PG_SPMV_WIN_MIN_ROW")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--variants", default="window,pair,dict,plain")
+    ap.add_argument("--cases", default="cfg2,cfg4,cfg5,cfg3")
     args = ap.parse_args()
-    cases = [("cfg2 7pt 100^3", wl.CONFIGS[2], dict()),
-             ("cfg4 27pt 160^3", wl.CONFIGS[4], dict(grid=160)),
-             ("cfg5 9pt 2048^2", wl.CONFIGS[5], dict()),
-             ("cfg3 random 2e6", wl.CONFIGS[3], dict())]
+    cases = {"cfg2": ("cfg2 7pt 100^3", wl.CONFIGS[2], dict()),
+             "cfg4": ("cfg4 27pt 160^3", wl.CONFIGS[4], dict(grid=160)),
+             "cfg5": ("cfg5 9pt 2048^2", wl.CONFIGS[5], dict()),
+             "cfg3": ("cfg3 random 2e6", wl.CONFIGS[3], dict())}
     out = []
-    for name, conf, kw in cases:
+    for key in args.cases.split(","):
+        name, conf, kw = cases[key]
         A = wl.make_matrix(conf, **kw)
-        for plain in (False, True):
-            if plain:
-                os.environ.pop("PG_SPMV_TMA", None)
-            else:
-                os.environ["PG_SPMV_TMA"] = "1"
+        for var in args.variants.split(","):
+            for k in ENV_KEYS:
+                os.environ.pop(k, None)
+            os.environ.update(VARIANTS[var])
             e = Engine.build(A)
+            st = e.shards[0].stats
             dt, gbs = time_pass(e, args.reps)
-            rec = dict(case=name, kernel="plain" if plain else "tma", us=dt * 1e6, gbs=gbs,
-                       nnz=A.nnz, n=A.nrows, padded=e.shards[0].stats["padded_nnz"])
+            eb = st["col_bytes"] + st["val_bytes"]
+            rec = dict(case=name, kernel=var, us=dt * 1e6, gbs_uncompressed_equiv=gbs,
+                       gbs_stored=(eb * A.nnz + 36 * A.nrows) / dt / 1e9,
+                       nnz=A.nnz, n=A.nrows, padded=st["padded_nnz"], entry_bytes=eb)
             print(json.dumps(rec), flush=True)
             out.append(rec)
             e.close()
             del e
         del A
-    os.environ.pop("PG_SPMV_PLAIN", None)
 
 
 if __name__ == "__main__":
