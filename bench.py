@@ -341,7 +341,7 @@ def run_ours(args):
                 "generation_s": round(gen_s, 2),
             },
             "roofline": {
-                "kernel": "sell_kernel<kPoly> (fused SpMV + polynomial epilogue)",
+                "kernel": KERNEL_NAMES[st["kernel"]] + " (fused SpMV + polynomial epilogue)",
                 "bound": "hbm",
                 "achieved": achieved,
                 "peak": peak,
@@ -353,9 +353,8 @@ def run_ours(args):
                 "kernel_s_per_step": kt / args.steps,
                 "share_of_step": kt / total if total else None,
                 "algorithmic_bytes_per_launch": kb / max(nk, 1),
-                "matrix_format": ("dictionary SELL (1 B offset + 1 B value index)"
-                                  if st.get("val_bytes") == 1 else
-                                  "SELL-C-sigma (int32 column + f64 value)"),
+                "matrix_format": MATRIX_FORMATS[st["kernel"]],
+                "stream_bytes_per_entry": st["stream_bytes"],
                 "uncompressed_equivalent_gbs": (kb12 / kt / 1e9) if kt > 0 else None,
             },
             "cpu_baseline": cpu,
@@ -369,6 +368,17 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# pg_matrix_stats()[11]: the SELL kernel pg_spmv / pg_poly_pass run (spmv.cu)
+KERNEL_NAMES = {0: "sell_kernel<kPoly,0,0>", 1: "sell_kernel<kPoly,1,1>",
+                2: "sell_pair_kernel<kPoly>", 3: "sell_win_kernel<kPoly>"}
+MATRIX_FORMATS = {
+    0: "SELL-C-sigma (int32 column + f64 value, 12 B/entry)",
+    1: "dictionary SELL (1 B offset + 1 B value index)",
+    2: "pair-dictionary SELL (1 B (offset, value) index), global x gathers",
+    3: "pair-dictionary SELL (1 B/entry), x windows staged by a TMA ring",
+}
 
 
 # ---------------------------------------------------------------------------

@@ -82,9 +82,13 @@ PG_API int pg_matrix_create(int device, int64_t nrows, int64_t ncols,
                             const int64_t* row_ptr, const int64_t* col_idx,
                             const double* values, int sigma, pg_matrix** out);
 PG_API int pg_matrix_destroy(pg_matrix* mat);
-/* stats[10] = {nrows, ncols, nnz, padded_nnz, n_slices, device_bytes,
+/* stats[12] = {nrows, ncols, nnz, padded_nnz, n_slices, device_bytes,
  *              max_width, sigma, bytes per column entry (1 = dictionary-
- *              compressed offsets, 4 = int32), bytes per value (1 or 8)} */
+ *              compressed offsets, 4 = int32), bytes per value (1 or 8),
+ *              matrix-stream bytes per entry of the kernel pg_spmv runs
+ *              (1 = pair dictionary, 2 = two dictionary streams, 12 = plain),
+ *              that kernel (0 plain SELL, 1 two-stream dictionary, 2 pair
+ *              dictionary with global gathers, 3 windowed pair TMA ring)} */
 PG_API int pg_matrix_stats(const pg_matrix* mat, int64_t* stats);
 
 /* ---- reduction workspace (one per stream) --------------------------------

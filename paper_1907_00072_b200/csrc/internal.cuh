@@ -106,11 +106,16 @@ constexpr int kUnitEntries = 3072;
 constexpr int kWinRows = PG_WIN_ROWS;
 constexpr int kWinMaxGroups = 32;
 constexpr int kWinMaxElems = 6144;
-#ifndef PG_WIN_STAGES
-#define PG_WIN_STAGES 2
+// Ring depth of the windowed kernel is chosen per matrix at launch: as many
+// stages (2..kWinMaxStages) as fit kWinTargetBlocks blocks per SM.
+constexpr int kWinMaxStages = 8;
+#ifndef PG_WIN_TARGET_BLOCKS
+#define PG_WIN_TARGET_BLOCKS 4
 #endif
-constexpr int kWinStages = PG_WIN_STAGES;
-constexpr int kWinMaxStageBytes = (220 * 1024) / kWinStages / 128 * 128;
+constexpr int kWinTargetBlocks = PG_WIN_TARGET_BLOCKS;
+constexpr int kWinSmemBudget = 220 * 1024;
+// a single stage must leave room for a second one in the budget
+constexpr int kWinMaxStageBytes = kWinSmemBudget / 2 / 128 * 128;
 // Number of per-block partial slots a reduction may use.
 constexpr int kMaxBlocks = 1024;
 // Per-block partial slots: the Gram stores (hi, lo) for each of the

@@ -392,14 +392,21 @@ __global__ void __launch_bounds__(kSellThreads, PG_SELL_DICT_MIN_BLOCKS)
 // the few group windows of the matrix's window plan (abi.cu
 // build_window_plan), and their packed index words are one contiguous byte
 // range per stream.  One thread streams all of it for the block's next row
-// blocks into a kWinStages-deep shared-memory ring with cp.async.bulk (TMA)
+// blocks into a shared-memory ring (WinArgs::stages deep) with cp.async.bulk (TMA)
 // completing on an mbarrier, so a stage carries ~15-35 KB of loads in flight
 // per copy batch; the 256 row threads then sum their rows from shared memory
 // only.  Window elements outside [0, ncols) are never referenced by a stored
 // entry and are simply not copied.  Same sequential mul-then-add order per
 // row: bitwise equal to the other kernels.
+// 1: epilogue operands, row lengths and slice widths ride in the ring stage
+// (bulk copies); 0: the row threads load them from global before waiting
+#ifndef PG_WIN_STAGE_EPI
+#define PG_WIN_STAGE_EPI 1
+#endif
+constexpr bool kWinStageEpi = PG_WIN_STAGE_EPI;
+
 struct WinArgs {
-  int ng, total, b8;
+  int ng, total, b8, stages;
   // byte offsets inside a ring stage: [window | pair stream | epilogue
   // operand A | operand B | row lengths | slice widths]
   int off_p8, off_ea, off_eb, off_rl, off_sw, stage_bytes;
@@ -431,6 +438,12 @@ __device__ __forceinline__ void epi_vectors(const Epi& e, const double* x, const
 __device__ __forceinline__ double row_sum_pairs(const uint32_t* pw, int len,
                                                 const unsigned char* winrow,
                                                 const PairEnt* s_ptab) {
+  // one 16-byte shared load per table entry (value + window offset)
+  auto ent = [&](uint32_t idx, double& v, int& woff) {
+    const int4 raw = reinterpret_cast<const int4*>(s_ptab)[idx];
+    v = __hiloint2double(raw.y, raw.x);
+    woff = raw.z;
+  };
   double acc = 0.0;
   const int full = len & ~3;
   int j = 0;
@@ -439,8 +452,10 @@ __device__ __forceinline__ double row_sum_pairs(const uint32_t* pw, int len,
     const uint32_t pb = pw[(j >> 2) * PG_SLICE];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const PairEnt pe = s_ptab[(pb >> (8 * u)) & 255u];
-      acc = __dadd_rn(acc, __dmul_rn(pe.v, *reinterpret_cast<const double*>(winrow + pe.woff)));
+      double v;
+      int woff;
+      ent((pb >> (8 * u)) & 255u, v, woff);
+      acc = __dadd_rn(acc, __dmul_rn(v, *reinterpret_cast<const double*>(winrow + woff)));
     }
   }
   if (j < len) {
@@ -448,9 +463,10 @@ __device__ __forceinline__ double row_sum_pairs(const uint32_t* pw, int len,
 #pragma unroll
     for (int u = 0; u < 3; ++u) {
       if (j + u < len) {
-        const PairEnt pe = s_ptab[(pb >> (8 * u)) & 255u];
-        acc = __dadd_rn(acc,
-                        __dmul_rn(pe.v, *reinterpret_cast<const double*>(winrow + pe.woff)));
+        double v;
+        int woff;
+        ent((pb >> (8 * u)) & 255u, v, woff);
+        acc = __dadd_rn(acc, __dmul_rn(v, *reinterpret_cast<const double*>(winrow + woff)));
       }
     }
   }
@@ -470,28 +486,32 @@ template <int MODE>
 __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, const Epi& e,
                                           const uint8_t* __restrict__ pair8,
                                           const double* __restrict__ x, int64_t rb,
-                                          unsigned char* buf, uint64_t* bar) {
+                                          int64_t p0, int64_t p1, unsigned char* buf,
+                                          uint64_t* bar) {
   double* win = reinterpret_cast<double*>(buf);
   const int64_t s0 = rb * (kWinRows / PG_SLICE);
   const int64_t s1 = min(s0 + kWinRows / PG_SLICE, wa.n_slices);
-  const int64_t p0 = __ldg(a.slice_ptr8 + s0), p1 = __ldg(a.slice_ptr8 + s1);
   const int64_t r0 = rb * kWinRows;
   const int64_t nr = min((int64_t)kWinRows, a.nrows - r0);
   const double *A, *B;
   epi_vectors<MODE>(e, x, A, B);
   // pass 1: byte count (+ odd tails), so that expect_tx precedes the copies
-  uint32_t bytes = (uint32_t)(p1 - p0) + 4u * (uint32_t)((s1 - s0) * PG_SLICE) +
-                   ((s1 - s0) * 4 % 16 == 0 ? 4u * (uint32_t)(s1 - s0) : 0u);
+  uint32_t bytes = (uint32_t)(p1 - p0);
+  if (kWinStageEpi)  // row lengths + slice widths (bulk unless a partial block)
+    bytes += 4u * (uint32_t)((s1 - s0) * PG_SLICE) +
+             ((s1 - s0) * 4 % 16 == 0 ? 4u * (uint32_t)(s1 - s0) : 0u);
   for (int g = 0; g < wa.ng; ++g) {
     const int64_t ga = r0 + wa.lo[g];
     const int64_t va = max(ga, (int64_t)0), vb = min(ga + wa.len[g], wa.ncols);
     if (vb > va) bytes += stage_f64_tail(win + wa.start[g] + (va - ga), x + va, vb - va);
   }
-  if (A) bytes += stage_f64_tail(reinterpret_cast<double*>(buf + wa.off_ea), A + r0, nr);
-  if (B) bytes += stage_f64_tail(reinterpret_cast<double*>(buf + wa.off_eb), B + r0, nr);
   int32_t* sw = reinterpret_cast<int32_t*>(buf + wa.off_sw);
-  if ((s1 - s0) * 4 % 16 != 0)  // partial last block: slice widths copied plainly
-    for (int64_t q = s0; q < s1; ++q) sw[q - s0] = __ldg(a.slice_w + q);
+  if (kWinStageEpi) {
+    if (A) bytes += stage_f64_tail(reinterpret_cast<double*>(buf + wa.off_ea), A + r0, nr);
+    if (B) bytes += stage_f64_tail(reinterpret_cast<double*>(buf + wa.off_eb), B + r0, nr);
+    if ((s1 - s0) * 4 % 16 != 0)  // partial last block: slice widths copied plainly
+      for (int64_t q = s0; q < s1; ++q) sw[q - s0] = __ldg(a.slice_w + q);
+  }
   mbar_expect_tx(bar, bytes);
   for (int g = 0; g < wa.ng; ++g) {
     const int64_t ga = r0 + wa.lo[g];
@@ -501,10 +521,12 @@ __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, 
       bulk_g2s(win + wa.start[g] + (va - ga), x + va, 8u * (uint32_t)n2, bar);
   }
   if (p1 > p0) bulk_g2s(buf + wa.off_p8, pair8 + p0, (uint32_t)(p1 - p0), bar);
-  if (A && nr > 1) bulk_g2s(buf + wa.off_ea, A + r0, 8u * (uint32_t)(nr & ~(int64_t)1), bar);
-  if (B && nr > 1) bulk_g2s(buf + wa.off_eb, B + r0, 8u * (uint32_t)(nr & ~(int64_t)1), bar);
-  bulk_g2s(buf + wa.off_rl, a.row_len + r0, 4u * (uint32_t)((s1 - s0) * PG_SLICE), bar);
-  if ((s1 - s0) * 4 % 16 == 0) bulk_g2s(sw, a.slice_w + s0, 4u * (uint32_t)(s1 - s0), bar);
+  if (kWinStageEpi) {
+    if (A && nr > 1) bulk_g2s(buf + wa.off_ea, A + r0, 8u * (uint32_t)(nr & ~(int64_t)1), bar);
+    if (B && nr > 1) bulk_g2s(buf + wa.off_eb, B + r0, 8u * (uint32_t)(nr & ~(int64_t)1), bar);
+    bulk_g2s(buf + wa.off_rl, a.row_len + r0, 4u * (uint32_t)((s1 - s0) * PG_SLICE), bar);
+    if ((s1 - s0) * 4 % 16 == 0) bulk_g2s(sw, a.slice_w + s0, 4u * (uint32_t)(s1 - s0), bar);
+  }
 }
 
 // Warp-specialised: warp 8 is the producer (one lane issues the copies of
@@ -515,18 +537,22 @@ __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, 
 constexpr int kWinThreads = kWinRows + 32;
 
 template <int MODE>
-__global__ void __launch_bounds__(kWinThreads, 1)
+#ifndef PG_WIN_MIN_BLOCKS
+#define PG_WIN_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
     sell_win_kernel(SellArgs a, WinArgs wa, const uint8_t* __restrict__ pair8,
                     const PairEnt* __restrict__ ptab, const double* __restrict__ x, Epi e,
                     double* partials, unsigned int* counter, double* nsq) {
   pdl_entry();
   extern __shared__ __align__(128) unsigned char smem_win[];
   __shared__ PairEnt s_ptab[256];
-  __shared__ __align__(8) uint64_t full[kWinStages];
-  __shared__ __align__(8) uint64_t empty[kWinStages];
+  __shared__ __align__(8) uint64_t full[kWinMaxStages];
+  __shared__ __align__(8) uint64_t empty[kWinMaxStages];
+  const int S = wa.stages;
   for (int i = threadIdx.x; i < 256; i += blockDim.x) s_ptab[i] = ptab[i];
   if (threadIdx.x == 0) {
-    for (int st = 0; st < kWinStages; ++st) {
+    for (int st = 0; st < S; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], kWinRows / 32);
     }
@@ -537,13 +563,26 @@ __global__ void __launch_bounds__(kWinThreads, 1)
   const int warp = threadIdx.x >> 5;
   if (warp == kWinRows / 32) {
     if ((threadIdx.x & 31) == 0) {
+      // the packed-stream bounds of the next row block are loaded one
+      // iteration ahead, off the issue path
+      auto bounds = [&](int64_t rb, int64_t& p0, int64_t& p1) {
+        if (rb >= wa.nblk) return;
+        const int64_t s0 = rb * (kWinRows / PG_SLICE);
+        p0 = __ldg(a.slice_ptr8 + s0);
+        p1 = __ldg(a.slice_ptr8 + min(s0 + kWinRows / PG_SLICE, wa.n_slices));
+      };
+      int64_t p0 = 0, p1 = 0, q0 = 0, q1 = 0;
+      bounds(blockIdx.x, p0, p1);
       int it = 0;
       for (int64_t rb = blockIdx.x; rb < wa.nblk; rb += gridDim.x, ++it) {
-        const int st = it % kWinStages;
-        if (it >= kWinStages) mbar_wait(&empty[st], (uint32_t)((it / kWinStages - 1) & 1));
+        bounds(rb + gridDim.x, q0, q1);
+        const int st = it % S;
+        if (it >= S) mbar_wait(&empty[st], (uint32_t)((it / S - 1) & 1));
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        win_issue<MODE>(a, wa, e, pair8, x, rb, smem_win + (size_t)st * wa.stage_bytes,
+        win_issue<MODE>(a, wa, e, pair8, x, rb, p0, p1, smem_win + (size_t)st * wa.stage_bytes,
                         &full[st]);
+        p0 = q0;
+        p1 = q1;
       }
     }
   } else {
@@ -553,21 +592,37 @@ __global__ void __launch_bounds__(kWinThreads, 1)
     const int sl = t >> 5;  // slice of this thread's row inside the block
     int it = 0;
     for (int64_t rb = blockIdx.x; rb < wa.nblk; rb += gridDim.x, ++it) {
-      const int st = it % kWinStages;
+      const int st = it % S;
       const unsigned char* buf = smem_win + (size_t)st * wa.stage_bytes;
       const int64_t row = rb * kWinRows + t;
-      mbar_wait(&full[st], (uint32_t)((it / kWinStages) & 1));
-      if (row < a.nrows) {
-        const int32_t* sw = reinterpret_cast<const int32_t*>(buf + wa.off_sw);
-        int off8 = 0;  // packed-stream offset of this slice inside the block
-        for (int q = 0; q < sl; ++q) off8 += ((sw[q] + 3) >> 2) * 4 * PG_SLICE;
-        const int w = sw[sl];
-        const int len = reinterpret_cast<const int32_t*>(buf + wa.off_rl)[t];
-        Pre pre{0.0, 0.0};
-        if (A) pre.a = reinterpret_cast<const double*>(buf + wa.off_ea)[t];
-        if (B) pre.b = reinterpret_cast<const double*>(buf + wa.off_eb)[t];
+      const bool live = row < a.nrows;
+      const int lane = t & 31;
+      int swl = 0, len = 0;
+      Pre pre{0.0, 0.0};
+      if (!kWinStageEpi) {  // per-row operands from global, overlapping the wait
+        const int64_t s0 = rb * (kWinRows / PG_SLICE);
+        if (lane < sl && s0 + lane < wa.n_slices) swl = __ldg(a.slice_w + s0 + lane);
+        if (live) {
+          len = __ldg(a.row_len + row);
+          pre = epi_load<MODE>(e, x, row);
+        }
+      }
+      mbar_wait(&full[st], (uint32_t)((it / S) & 1));
+      if (kWinStageEpi) {
+        if (lane < sl) swl = reinterpret_cast<const int32_t*>(buf + wa.off_sw)[lane];
+        if (live) {
+          len = reinterpret_cast<const int32_t*>(buf + wa.off_rl)[t];
+          if (A) pre.a = reinterpret_cast<const double*>(buf + wa.off_ea)[t];
+          if (B) pre.b = reinterpret_cast<const double*>(buf + wa.off_eb)[t];
+        }
+      }
+      // packed-stream offset of this warp's slice inside the block: a warp
+      // reduction over the widths of the slices before it (whole warp, before
+      // the row guard)
+      const int wq = lane < sl ? ((swl + 3) >> 2) * 4 * PG_SLICE : 0;
+      const int off8 = (int)__reduce_add_sync(0xffffffffu, (unsigned)wq);
+      if (live) {
         const uint32_t* pw = reinterpret_cast<const uint32_t*>(buf + wa.off_p8 + off8) + (t & 31);
-        (void)w;
         const double ax = row_sum_pairs(pw, len, buf + 8 * t, s_ptab);
         const double r = epilogue<MODE>(e, pre, row, ax);
         if (MODE == kResid) local = __fma_rn(r, r, local);
@@ -717,12 +772,15 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
       wa.start[g] = m->wstart[g];
       wa.len[g] = m->wlen[g];
     }
-    const size_t smem = (size_t)kWinStages * wa.stage_bytes;
+    wa.stages = kWinSmemBudget / kWinTargetBlocks / wa.stage_bytes;
+    if (wa.stages < 2) wa.stages = 2;
+    if (wa.stages > kWinMaxStages) wa.stages = kWinMaxStages;
+    const size_t smem = (size_t)wa.stages * wa.stage_bytes;
     auto kern = sell_win_kernel<MODE>;
     static bool attr[4][64] = {};
     if (!attr[MODE][dev]) {
       PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(kWinStages * kWinMaxStageBytes)));
+                                   kWinSmemBudget));
       attr[MODE][dev] = true;
     }
     // resident grid: blocks per SM from the occupancy calculator at this

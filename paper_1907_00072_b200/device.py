@@ -143,13 +143,13 @@ class Shard:
         _lib.call("pg_workspace_create", self.dev_ord, _lib.C.byref(w))
         self.ws = w
         self.nnz = int(row_ptr[-1])
-        st = (_lib.C.c_int64 * 10)()
+        st = (_lib.C.c_int64 * 12)()
         _lib.call("pg_matrix_stats", self.mat, st)
         self.stats = dict(zip(("nrows", "ncols", "nnz", "padded_nnz", "n_slices",
                                "device_bytes", "max_width", "sigma", "col_bytes",
-                               "val_bytes"), list(st)))
+                               "val_bytes", "stream_bytes", "kernel"), list(st)))
         # bytes streamed per stored matrix entry (dictionary compression: 1+1)
-        self.entry_bytes = int(st[8]) + int(st[9])
+        self.entry_bytes = int(st[10])
         # small per-shard device scratch: [c1 | c2 | nsq | spare]
         self.scal = torch.zeros(2 * KMAX + 8, dtype=F64, device=device)
         self.coef = torch.zeros(KMAX, dtype=F64, device=device)

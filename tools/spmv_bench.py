@@ -70,10 +70,11 @@ def main():
             e = Engine.build(A)
             st = e.shards[0].stats
             dt, gbs = time_pass(e, args.reps)
-            eb = st["col_bytes"] + st["val_bytes"]
+            eb = st["stream_bytes"]
             rec = dict(case=name, kernel=var, us=dt * 1e6, gbs_uncompressed_equiv=gbs,
                        gbs_stored=(eb * A.nnz + 36 * A.nrows) / dt / 1e9,
-                       nnz=A.nnz, n=A.nrows, padded=st["padded_nnz"], entry_bytes=eb)
+                       nnz=A.nnz, n=A.nrows, padded=st["padded_nnz"], entry_bytes=eb,
+                       kernel_kind=st["kernel"])
             print(json.dumps(rec), flush=True)
             out.append(rec)
             e.close()

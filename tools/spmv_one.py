@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--grid", type=int, default=160)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--mode", default="poly", choices=["poly", "spmv"])
     args = ap.parse_args()
     A = wl.make_matrix(wl.CONFIGS[args.config], grid=args.grid)
     e = Engine.build(A)
