@@ -142,6 +142,26 @@ PG_API int pg_root_pass(const pg_matrix* mat, const double* d_x, const double* d
                         const double* d_y_in, double* d_y_out, double* d_v_out, double c1,
                         double c2, double c3, int mode, void* stream);
 
+/* ---- ILU(0) left preconditioning ---------------------------
+ * pg_ilu0_factor: host (no GPU).  Replaces ilu0_factor (ilu.py:38-95): IKJ
+ * elimination restricted to the pattern of (row_ptr, col_idx, values) after
+ * adding diag_shift to the diagonal, in the reference's operation order (the
+ * factors are bit-identical).  out_values[nnz] = combined L\U, out_diag_ptr[n]
+ * = position of each diagonal.  On a missing structural diagonal
+ * (*fail_kind = 1) or a pivot |u_kk| <= eps*max|diag| (*fail_kind = 2) the
+ * failing 0-based row is in *fail_row (PivotError(row)); status stays PG_OK.
+ * pg_ilu_create: device copy of the factors (split L / U / diagonal).
+ * pg_ilu_apply: z = U^{-1} L^{-1} v (ilu0_apply, ilu.py:98-114) as two
+ * sync-free triangular sweeps; d_y is an n-vector scratch (must not alias). */
+typedef struct pg_ilu pg_ilu;
+PG_API int pg_ilu0_factor(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                          const double* values, double diag_shift, double* out_values,
+                          int64_t* out_diag_ptr, int64_t* fail_row, int* fail_kind);
+PG_API int pg_ilu_create(int device, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                         const double* values, const int64_t* diag_ptr, pg_ilu** out);
+PG_API int pg_ilu_destroy(pg_ilu* ilu);
+PG_API int pg_ilu_apply(pg_ilu* ilu, const double* d_v, double* d_y, double* d_z, void* stream);
+
 /* r = b - A x and the partial sum of r^2 into d_nsq[0] (gmres.py:334-335). */
 PG_API int pg_residual(const pg_matrix* mat, const double* d_x, const double* d_b,
                        double* d_r, double* d_nsq, pg_workspace* ws, void* stream);

@@ -161,6 +161,88 @@ def wrapped_apply(y, op, v, tally):
 
 
 # ---------------------------------------------------------------------------
+# ILU(0) left preconditioning  (ilu.py:38-114, gmres.py:63-95)
+# ---------------------------------------------------------------------------
+class IluPivotOracle(Exception):
+    def __init__(self, row, structural=False):
+        super().__init__(f"pivot failure at row {row}")
+        self.row = row
+        self.structural = structural
+
+
+def ilu0_factor(op, diag_shift=0.0):
+    """IKJ elimination restricted to the pattern of ``op`` (ilu.py:38-95),
+    same operation order: ``l_ik = a_ik / u_kk`` then ``a_ij -= l_ik * u_kj``
+    for j in row k's upper part that is also in row i's pattern.  Returns
+    (values, diag_ptr); raises IluPivotOracle(row)."""
+    n = op.nrows
+    rp, ci = op.row_ptr, op.col_idx
+    vals = op.values.copy()
+    diag = np.full(n, -1, dtype=np.int64)
+    hit = op.entry_row == ci
+    diag[ci[hit]] = np.nonzero(hit)[0]
+    if np.any(diag < 0):
+        raise IluPivotOracle(int(np.nonzero(diag < 0)[0][0]), structural=True)
+    if diag_shift != 0.0:
+        vals[diag] += diag_shift
+    floor = np.finfo(np.float64).eps * float(np.max(np.abs(vals[diag])))
+    for i in range(n):
+        where = {int(ci[p]): p for p in range(rp[i], rp[i + 1])}
+        for p in range(rp[i], rp[i + 1]):
+            k = int(ci[p])
+            if k >= i:
+                break
+            ukk = vals[diag[k]]
+            if abs(ukk) <= floor:
+                raise IluPivotOracle(k)
+            vals[p] = vals[p] / ukk
+            for q in range(diag[k] + 1, rp[k + 1]):
+                t = where.get(int(ci[q]))
+                if t is not None:
+                    vals[t] -= vals[p] * vals[q]
+        if abs(vals[diag[i]]) <= floor:
+            raise IluPivotOracle(i)
+    return vals, diag
+
+
+def ilu0_apply(op, vals, diag, v):
+    """``M^{-1} v`` (ilu.py:98-114): forward sweep with unit L, backward with
+    U; each row's off-diagonal sum is a numpy dot as in the reference."""
+    n = op.nrows
+    rp, ci = op.row_ptr, op.col_idx
+    y = np.empty(n)
+    for i in range(n):
+        y[i] = v[i] - vals[rp[i]:diag[i]] @ y[ci[rp[i]:diag[i]]]
+    z = np.empty(n)
+    for i in range(n - 1, -1, -1):
+        d, hi = diag[i], rp[i + 1]
+        z[i] = (y[i] - vals[d + 1:hi] @ z[ci[d + 1:hi]]) / vals[d]
+    return z
+
+
+class OracleIluOperator:
+    """``v -> M^{-1} (A v)`` with its counters (gmres.py:63-95)."""
+
+    def __init__(self, A, vals, diag):
+        self.A, self.vals, self.diag = A, vals, diag
+        self.tally = A.tally
+        self.dimension = A.nrows
+        self.nrows = A.nrows
+
+    def apply(self, x):
+        self.tally.spmvs += 1
+        self.tally.prec_applies += 1
+        return ilu0_apply(self.A, self.vals, self.diag, self.A.matvec(x))
+
+    def matvec(self, x):
+        return ilu0_apply(self.A, self.vals, self.diag, self.A.matvec(x))
+
+    def precondition(self, v):
+        self.tally.prec_applies += 1
+        return ilu0_apply(self.A, self.vals, self.diag, v)
+
+
+# ---------------------------------------------------------------------------
 # two-pass classical Gram-Schmidt  (ortho.py:14, 33-70)
 # ---------------------------------------------------------------------------
 BREAKDOWN_RTOL = 1e-14

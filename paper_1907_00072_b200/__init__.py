@@ -16,10 +16,13 @@ Every vector operation runs in hand-written sm_100a kernels of libpgmres.so
 from .counters import CostCounters
 from .errors import (
     CholeskyFailure,
+    ConfigError,
     DeviceError,
     DimensionMismatchError,
+    MatrixFormatError,
     NumericalBreakdownError,
     ParameterError,
+    PivotError,
     SingularHessenbergError,
 )
 from .workloads import CsrHost
@@ -47,6 +50,10 @@ _LAZY = {
     "leja_order": "polyprec",
     "residual_poly_roots": "polyprec",
     "icgs": "ortho",
+    "DeviceIluOperator": "operators",
+    "Ilu0Factors": "ilu",
+    "ilu0_factor": "ilu",
+    "ilu0_apply": "ilu",
     "OrthoResult": "ortho",
 }
 
@@ -64,5 +71,6 @@ def __getattr__(name):
 
 __all__ = sorted(list(_LAZY) + [
     "CostCounters", "CsrHost", "CholeskyFailure", "DeviceError", "DimensionMismatchError",
-    "NumericalBreakdownError", "ParameterError", "SingularHessenbergError",
+    "NumericalBreakdownError", "ParameterError", "SingularHessenbergError", "PivotError",
+    "ConfigError", "MatrixFormatError",
 ])

@@ -15,11 +15,11 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libpgmres.so")
 BUILD = os.path.join(ROOT, "build", "pgmres")
 
-SOURCES = ["abi.cu", "spmv.cu", "ortho.cu", "host.cu"]
+SOURCES = ["abi.cu", "spmv.cu", "ortho.cu", "host.cu", "ilu.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-fvisibility=hidden",
+    "-Xcompiler", "-fPIC,-fvisibility=hidden,-ffp-contract=off",
     "-Xptxas", "-v",
     "-I", INCLUDE,
 ]

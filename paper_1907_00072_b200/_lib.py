@@ -64,6 +64,10 @@ _SIGNATURES = {
     "pg_host_cholesky_solve": ([_i32, _p, _i32, _p, _p, C.POINTER(C.c_int)], C.c_int),
     "pg_host_degree_select": ([_i32, _p, _i32, _p, _p, C.POINTER(C.c_int)], C.c_int),
     "pg_host_backsolve": ([_i32, _p, _i32, _p, _p, C.POINTER(C.c_int)], C.c_int),
+    "pg_ilu0_factor": ([_i64, _p, _p, _p, _d, _p, _p, _pi64, C.POINTER(C.c_int)], C.c_int),
+    "pg_ilu_create": ([_i32, _i64, _p, _p, _p, _p, C.POINTER(_p)], C.c_int),
+    "pg_ilu_destroy": ([_p], C.c_int),
+    "pg_ilu_apply": ([_p, _p, _p, _p, _p], C.c_int),
 }
 
 _lib = None
@@ -116,7 +120,7 @@ def check(code: int, what: str = ""):
 LAUNCHING = frozenset({
     "pg_spmv", "pg_poly_pass", "pg_root_pass", "pg_residual", "pg_cgs2_phase1", "pg_cgs2_phase2",
     "pg_cgs2_phase3", "pg_normalize", "pg_gram", "pg_gemv", "pg_dot", "pg_scale_add",
-    "pg_gather",
+    "pg_gather", "pg_ilu_apply",
 })
 #: per-entry-point launch tally (bench.py reports it as gpu_launches)
 LAUNCH_COUNT: dict = {}

@@ -332,6 +332,9 @@ class Engine:
         # optional list collecting (start_event, end_event, algorithmic_bytes)
         # per fused polynomial pass (bench.py's live roofline measurement)
         self.timer = None
+        # ILU(0) left preconditioner (attach_ilu): when set, one operator
+        # application is M^{-1} A v (IluPreconditionedOperator, gmres.py:63-95)
+        self.ilu = None
 
     # ---- construction -------------------------------------------------------
     @classmethod
@@ -375,8 +378,52 @@ class Engine:
         return cls([s], comm, int(offs[-1]))
 
     def close(self):
+        if self.ilu is not None:
+            _lib.call("pg_ilu_destroy", self.ilu)
+            self.ilu = None
         for s in self.shards:
             s.close()
+
+    # ---- ILU(0) left preconditioning ---------------------------
+    def attach_ilu(self, factors):
+        """Device copy of ILU(0) factors (ilu.Ilu0Factors); from now on every
+        operator application of this engine is M^{-1} (A v).  Serial like the
+        reference (ilu.py:1-7): a single shard only."""
+        if self.P != 1 or self.comm.distributed:
+            raise ParameterError("ILU(0) preconditioning needs a single shard")
+        s = self.shards[0]
+        if int(factors.n) != s.n:
+            raise DimensionMismatchError("factors do not match the matrix")
+        rp = np.ascontiguousarray(factors.row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(factors.col_idx, dtype=np.int64)
+        va = np.ascontiguousarray(factors.values, dtype=np.float64)
+        dp = np.ascontiguousarray(factors.diag_ptr, dtype=np.int64)
+        h = _lib.C.c_void_p()
+        _lib.call("pg_ilu_create", s.dev_ord, s.n, rp.ctypes.data, ci.ctypes.data, va.ctypes.data,
+                  dp.ctypes.data, _lib.C.byref(h))
+        if self.ilu is not None:
+            _lib.call("pg_ilu_destroy", self.ilu)
+        self.ilu = h
+
+    def precondition(self, vs, outs):
+        """outs = M^{-1} v (two sync-free triangular sweeps)."""
+        s = self.shards[0]
+        tmp = self.cached_vecs("ilu_y")
+        _lib.call("pg_ilu_apply", self.ilu, ptr(vs[0]), ptr(tmp[0]), ptr(outs[0]), s.stream)
+
+    def _op_generic(self, xs, ys):
+        """ys = M^{-1} (A x) (ILU engines)."""
+        t = self.cached_vecs("ilu_t")
+        self.halo(xs)
+        s = self.shards[0]
+        _lib.call("pg_spmv", s.mat, ptr(xs[0]), ptr(t[0]), s.stream)
+        self.precondition(t, ys)
+
+    def count_ops(self, counters, k: int):
+        """Tally k operator applications (spmvs; prec_applies on ILU engines)."""
+        counters.spmvs += k
+        if self.ilu is not None:
+            counters.prec_applies += k
 
     def bind_stream(self):
         """Re-read each device's current torch stream (call at every public
@@ -482,6 +529,9 @@ class Engine:
         self.comm.halo(xs)
 
     def spmv(self, xs, ys):
+        """One operator application: A x, or M^{-1} A x on an ILU engine."""
+        if self.ilu is not None:
+            return self._op_generic(xs, ys)
         self.halo(xs)
         for s, x, y in zip(self._each(), xs, ys):
             _lib.call("pg_spmv", s.mat, ptr(x), ptr(y), s.stream)
@@ -491,6 +541,8 @@ class Engine:
         d = len(y)-1 fused SpMV passes.  acc, w0, w1: scratch shard vectors."""
         y = [float(c) for c in y]
         d = len(y) - 1
+        if self.ilu is not None and d > 0:
+            return self._poly_generic(y, vs, out, acc, w0, w1, base)
         if d == 0:
             for s, v, o, b in zip(self._each(), vs, out, base or [None] * self.P):
                 _lib.call("pg_scale_add", ptr(b) if b is not None else None, y[0], ptr(v), s.n,
@@ -531,11 +583,32 @@ class Engine:
             ev1.record(torch.cuda.current_stream(s0.device))
             self.timer.append((ev0, ev1, nbytes, d, nbytes12))
 
+    def _poly_generic(self, y, vs, out, acc, w0, w1, base):
+        """Running-power recurrence with a non-SpMV operator (ILU engines):
+        acc = y0 v; w = op(w); acc = acc + yk w (polyprec.py:205-211), then
+        out = base + acc.  Same rounding sequence as the reference."""
+        s = self.shards[0]
+        d = len(y) - 1
+        _lib.call("pg_scale_add", None, y[0], ptr(vs[0]), s.n, ptr(acc[0]), s.stream)
+        cur = vs
+        ws = (w0, w1)
+        for k in range(1, d + 1):
+            nxt = ws[k & 1]
+            self._op_generic(cur, nxt)
+            last = k == d
+            dst = out if (last and base is None) else acc
+            _lib.call("pg_scale_add", ptr(acc[0]), y[k], ptr(nxt[0]), s.n, ptr(dst[0]), s.stream)
+            cur = nxt
+        if base is not None:
+            _lib.call("pg_scale_add", ptr(base[0]), 1.0, ptr(acc[0]), s.n, ptr(out[0]), s.stream)
+
     def poly_roots(self, plan, vs, out, t, p0, p1, base=None):
         """out = (base +) p(A) v in root-product form (polyprec.RootPlan): one
         fused ``pg_root_pass`` per step, the running sum y in ``out`` (seeded
         with ``base``), the product in p0/p1 (ping-pong: every pass gathers
         it), the pair temporary in t.  vs is never written."""
+        if self.ilu is not None:
+            raise ParameterError("the root-product form needs the plain SpMV operator")
         if plan.degree == 0:
             for s, v, o, b in zip(self._each(), vs, out, base or [None] * self.P):
                 _lib.call("pg_scale_add", ptr(b) if b is not None else None, plan.y0, ptr(v), s.n,
@@ -589,6 +662,8 @@ class Engine:
         """z = A p(A) v = v - pi(A) v (RootPlan.resid_steps): d+1 fused passes
         that carry only the product -- no running sum is read or written, so
         each pass moves 16 B/row of vectors instead of the monomial's 32."""
+        if self.ilu is not None:
+            raise ParameterError("the root-product form needs the plain SpMV operator")
         if not plan.resid_steps:  # p == 0
             for s, v, o in zip(self._each(), vs, z):
                 _lib.call("pg_scale_add", None, 0.0, ptr(v), s.n, ptr(o), s.stream)
@@ -633,7 +708,13 @@ class Engine:
 
     def residual(self, xs, bs, rs, slot=4) -> float:
         """r = b - A x; returns the global sum of r^2 (host float), also left
-        in device scalar slot ``slot``."""
+        in device scalar slot ``slot``.  ILU engines: r = b - M^{-1} A x."""
+        if self.ilu is not None:
+            z = self.cached_vecs("ilu_z")
+            self._op_generic(xs, z)
+            s = self.shards[0]
+            _lib.call("pg_scale_add", ptr(bs[0]), -1.0, ptr(z[0]), s.n, ptr(rs[0]), s.stream)
+            return self.dot(rs, rs, slot=slot)
         self.halo(xs)
         nsq = self.slot(slot)
         for s, x, b, r, q in zip(self._each(), xs, bs, rs, nsq):

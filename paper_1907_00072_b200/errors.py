@@ -35,3 +35,20 @@ class SingularHessenbergError(RuntimeError):
 class DeviceError(RuntimeError):
     """A CUDA / library failure reported by libpgmres (no reference analogue:
     the reference has no device).  Never silently replaced by a CPU path."""
+
+
+class PivotError(ValueError):
+    """An ILU pivot is zero, below the floor, or structurally missing; ``row``
+    is the 0-based row at which factorisation stopped (errors.py:44-52)."""
+
+    def __init__(self, row, message=None):
+        super().__init__(message or f"zero or near-zero pivot in row {row}")
+        self.row = row
+
+
+class ConfigError(ValueError):
+    """Experiment configuration is malformed or inconsistent (errors.py:69)."""
+
+
+class MatrixFormatError(ValueError):
+    """A matrix file cannot be used (errors.py:12)."""

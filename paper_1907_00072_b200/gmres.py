@@ -206,7 +206,7 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
     else:
         xs = e.ingest(x0)
         if any(bool(torch.any(x[:s.n] != 0.0)) for s, x in zip(e.shards, xs)):
-            counters.spmvs += 1
+            e.count_ops(counters, 1)
             beta = math.sqrt(e.residual(xs, bs, W.r, slot=4))
         else:
             e.copy(bs, W.r)
@@ -248,10 +248,10 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
             c1, c2, nsq = e.cgs2_fetch(handle)
             handle = ahead
             if poly is not None:
-                counters.spmvs += d + 1
+                e.count_ops(counters, d + 1)
                 counters.vector_updates += d + 1
             else:
-                counters.spmvs += 1
+                e.count_ops(counters, 1)
             coeffs = c1 + c2
             new_norm = math.sqrt(nsq) if nsq >= 0.0 else float("nan")
             counters.dots += 3
@@ -298,7 +298,7 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
         e.gemv(W.V, j, y, W.t)
         counters.vector_updates += j
         if poly is not None:
-            counters.spmvs += d
+            e.count_ops(counters, d)
             counters.vector_updates += d + 1
             if plan is not None:
                 e.poly_roots(plan, W.t, xs, W.acc, W.w0, W.w1, base=xs)
@@ -309,7 +309,7 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
         counters.vector_updates += 1
         cycles += 1
 
-        counters.spmvs += 1
+        e.count_ops(counters, 1)
         beta = math.sqrt(e.residual(xs, bs, W.r, slot=4))
         counters.scalar_dots += 1
         true_relres = beta / norm_b

@@ -106,7 +106,7 @@ def _device_power_gram(op, v0, top: int, counters: CostCounters):
     # column 0 = v0 / |v0| (exact division, as numpy's v0 / seed_norm)
     e.normalize_dev(vs, e.slot(6), [blk[0] for blk in P])
     for k in range(top):
-        op.counters.spmvs += 1
+        e.count_ops(op.counters, 1)
         e.spmv([blk[k] for blk in P], [blk[k + 1] for blk in P])
     G = e.gram(P, top + 1)
     return G, seed_norm
@@ -341,7 +341,7 @@ def apply_poly(p: PolyCoefficients, op, v, counters: CostCounters, form: str = "
         raise DimensionMismatchError("vector length does not match operator")
     vs = e.ingest(v)
     out, acc, w0, w1 = e.vecs(), e.vecs(), e.vecs(), e.vecs()
-    op.counters.spmvs += p.degree
+    e.count_ops(op.counters, p.degree)
     counters.vector_updates += p.degree + 1
     if form == "roots":
         e.poly_roots(root_plan(p), vs, out, acc, w0, w1)

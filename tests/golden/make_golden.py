@@ -17,6 +17,8 @@ Cases:
   icgs     random basis n=300 j=20                                (ortho.py:33-70)
   auto     auto_degree bidiag2 cap 20; lap64 cap 16               (polyprec.py:150-190)
   solve    cfg1 full solve; degree sweep; convdiff2d multi-cycle; x0 != 0
+  ilu      ILU(0) factors / applications of lap64 and convdiff48 (+ diag shift),
+           an ILU-left-preconditioned polynomial solve, pivot failures
   small    reduced-size versions of configs 2-5 (this repo's generators) solved
            by the reference with the SURVEY §7(i) degree policy
 """
@@ -183,6 +185,41 @@ def main():
     solve_record("convdiff48_x0_solve", C, bc, pg.random_seed_vector(C.nrows, 4), 4, 15, 1e-8,
                  x0=x0)
     solve_record("convdiff48_noprec", C, bc, None, None, 30, 1e-8, max_iters=400)
+
+    # --- ILU(0) left preconditioning (ilu.py:38-114, gmres.py:63-95) --------
+    F = pg.ilu0_factor(A)  # lap64
+    arrays["ilu_lap64_values"] = F.values
+    arrays["ilu_lap64_diag_ptr"] = F.diag_ptr
+    arrays["ilu_lap64_apply"] = pg.ilu0_apply(F, b)
+    Fc = pg.ilu0_factor(C)  # convdiff48 (non-symmetric)
+    arrays["ilu_convdiff48_values"] = Fc.values
+    arrays["ilu_convdiff48_apply"] = pg.ilu0_apply(Fc, bc)
+    Fs = pg.ilu0_factor(C, diag_shift=0.3)
+    arrays["ilu_convdiff48_shift_values"] = Fs.values
+    # left-preconditioned polynomial solve, the CLI's --ilu flow (cli.py:252-277)
+    counters = pg.CostCounters()
+    opi = pg.IluPreconditionedOperator(C, Fc, counters)
+    b_eff = opi.precondition(bc)
+    arrays["ilu_convdiff48_beff"] = b_eff
+    polyi = pg.build_poly(opi, pg.random_seed_vector(C.nrows, 4), 5, counters)
+    arrays["ilu_convdiff48_y"] = polyi.y
+    before = counters.as_dict()
+    resi = pg.solve(opi, b_eff, right_prec=polyi, config=pg.GmresConfig(20, 1e-10))
+    arrays["ilu_convdiff48_x"] = resi.x
+    meta["ilu_convdiff48_solve"] = dict(
+        iterations=resi.iterations, cycles=resi.cycles, converged=resi.converged,
+        final_relres=resi.final_relres, counters=counters.as_dict(), build_counters=before)
+    for name, dense in (("zero_pivot", [[0.0, 1.0], [1.0, 1.0]]),
+                        ("missing_diag", [[0.0, 1.0], [1.0, 0.0]])):
+        rows, cols = np.nonzero(np.asarray(dense) != 0.0) if name == "missing_diag" else (
+            np.array([0, 0, 1, 1]), np.array([0, 1, 0, 1]))
+        vals = np.asarray(dense)[rows, cols]
+        M = pg.CsrMatrix.from_coo(2, 2, rows, cols, vals)
+        try:
+            pg.ilu0_factor(M)
+            meta[f"ilu_{name}"] = dict(row=None)
+        except pg.PivotError as exc:
+            meta[f"ilu_{name}"] = dict(row=exc.row, message=str(exc))
 
     # --- reduced-size configs 2-5 (this repo's generators, reference solver) --
     small = {
