@@ -19,6 +19,8 @@ Cases:
   solve    cfg1 full solve; degree sweep; convdiff2d multi-cycle; x0 != 0
   ilu      ILU(0) factors / applications of lap64 and convdiff48 (+ diag shift),
            an ILU-left-preconditioned polynomial solve, pivot failures
+  cli      the reference command line on five experiments (incl. --ilu, --degree
+           auto, a Matrix Market file lap10.mtx, a non-converged run)
   small    reduced-size versions of configs 2-5 (this repo's generators) solved
            by the reference with the SURVEY §7(i) degree policy
 """
@@ -239,6 +241,41 @@ def main():
         max_iters = 300 if c == 3 else 200000
         solve_record(f"small{c}", Am, bb, vv, cfg["degree"], cfg["m"], cfg["tol"],
                      max_iters=max_iters)
+
+    # --- the reference command line (cli.py:242-312), run in-process -------
+    import tempfile
+
+    from polygmres import cli as pg_cli
+    mtx = os.path.join(HERE, "lap10.mtx")
+    pg.write_matrix_market(pg.gen_laplacian2d(10), mtx)
+    cli_cases = {
+        "cli_cfg1": ["--generator", "laplacian2d", "--grid-n", "64", "--rhs", "axrandom",
+                     "--seed", "0", "--degree", "10", "-m", "40", "--tol", "1e-8"],
+        "cli_ilu": ["--generator", "convdiff2d", "--grid-n", "48", "--epsilon", "0.05",
+                    "--rhs", "generator", "--ilu", "--degree", "5", "-m", "20", "--tol",
+                    "1e-9", "--format", "jsonl"],
+        "cli_auto": ["--generator", "bidiag2", "--rhs", "random", "--seed", "3", "--degree",
+                     "auto", "--degree-cap", "20", "-m", "30", "--tol", "1e-10"],
+        "cli_mtx": ["--matrix-file", "@MTX@", "--rhs", "random", "--seed", "5", "--degree", "3",
+                    "--v0", "rhs", "-m", "10", "--tol", "1e-9"],
+        "cli_noprec": ["--generator", "laplacian2d", "--grid-n", "32", "--rhs", "random", "-m",
+                       "30", "--max-iters", "50"],
+    }
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, argv in cli_cases.items():
+            out = os.path.join(tmp, name)
+            argv = [a.replace("@MTX@", mtx) for a in argv] + ["-o", out]
+            code = pg_cli.main(argv)
+            fmt = "jsonl" if "jsonl" in argv else "csv"
+            with open(out + ".summary.json") as fh:
+                summary = json.load(fh)
+            with open(f"{out}.history.{fmt}") as fh:
+                history = fh.read()
+            summary["config"]["output"] = "<OUT>"
+            if summary["config"]["matrix_file"]:
+                summary["config"]["matrix_file"] = "<MTX>"
+            meta[name] = dict(argv=[a if a != mtx else "<MTX>" for a in argv[:-2]], exit=code,
+                              summary=summary, history=history)
 
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
