@@ -162,6 +162,33 @@ PG_API int pg_ilu_create(int device, int64_t n, const int64_t* row_ptr, const in
 PG_API int pg_ilu_destroy(pg_ilu* ilu);
 PG_API int pg_ilu_apply(pg_ilu* ilu, const double* d_v, double* d_y, double* d_z, void* stream);
 
+/* ---- whole steps as single calls (host-overhead reduction) ------------------
+ * pg_event_*: a CUDA event owned by the library (record / wait / elapsed ms).
+ * pg_poly_chain: out = (base +) p(A) x with the d fused passes of
+ *   pg_poly_pass (apply_poly, polyprec.py:193-212; x + p(A)u, gmres.py:330);
+ *   d = 0: out = base + y0 x.  Optional ev_start / ev_end bracket the chain.
+ * pg_arnoldi_step: one Arnoldi step of solve (gmres.py:282-316) on a
+ *   single-shard operator: z = A p(A) v_j (d fused passes + the wrapper SpMV;
+ *   d = -1: z = A v_j), CGS2 of z against V[:,0..j] (ortho.py:53-70) with
+ *   w2/|w2| into V[:,j+1], the scalars [c1 (PG_KMAX) | c2 (PG_KMAX) | |w2|^2]
+ *   into d_ring and copied to the pinned h_ring, then ev_done recorded.  V is
+ *   column-major with leading dimension ld.  Bit-identical to issuing the
+ *   same entry points one by one. */
+typedef struct pg_event pg_event;
+PG_API int pg_event_create(int device, pg_event** out);
+PG_API int pg_event_destroy(pg_event* ev);
+PG_API int pg_event_record(pg_event* ev, void* stream);
+PG_API int pg_event_wait(pg_event* ev);
+PG_API int pg_event_elapsed(pg_event* start, pg_event* end, float* ms);
+PG_API int pg_poly_chain(const pg_matrix* mat, const double* y, int d, const double* d_x,
+                         const double* d_base, double* d_out, double* d_acc, double* d_w0,
+                         double* d_w1, pg_event* ev_start, pg_event* ev_end, void* stream);
+PG_API int pg_arnoldi_step(const pg_matrix* mat, const double* y, int d, double* d_V, int64_t ld,
+                           int j, double* d_z, double* d_t, double* d_acc, double* d_w0,
+                           double* d_w1, double* d_ring, double* h_ring, pg_workspace* ws,
+                           pg_event* ev_done, pg_event* ev_chain0, pg_event* ev_chain1,
+                           void* stream);
+
 /* r = b - A x and the partial sum of r^2 into d_nsq[0] (gmres.py:334-335). */
 PG_API int pg_residual(const pg_matrix* mat, const double* d_x, const double* d_b,
                        double* d_r, double* d_nsq, pg_workspace* ws, void* stream);

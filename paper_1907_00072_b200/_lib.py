@@ -64,6 +64,14 @@ _SIGNATURES = {
     "pg_host_cholesky_solve": ([_i32, _p, _i32, _p, _p, C.POINTER(C.c_int)], C.c_int),
     "pg_host_degree_select": ([_i32, _p, _i32, _p, _p, C.POINTER(C.c_int)], C.c_int),
     "pg_host_backsolve": ([_i32, _p, _i32, _p, _p, C.POINTER(C.c_int)], C.c_int),
+    "pg_event_create": ([_i32, C.POINTER(_p)], C.c_int),
+    "pg_event_destroy": ([_p], C.c_int),
+    "pg_event_record": ([_p, _p], C.c_int),
+    "pg_event_wait": ([_p], C.c_int),
+    "pg_event_elapsed": ([_p, _p, C.POINTER(C.c_float)], C.c_int),
+    "pg_poly_chain": ([_p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p], C.c_int),
+    "pg_arnoldi_step": ([_p, _p, _i32, _p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,
+                         _p, _p], C.c_int),
     "pg_ilu0_factor": ([_i64, _p, _p, _p, _d, _p, _p, _pi64, C.POINTER(C.c_int)], C.c_int),
     "pg_ilu_create": ([_i32, _i64, _p, _p, _p, _p, C.POINTER(_p)], C.c_int),
     "pg_ilu_destroy": ([_p], C.c_int),
@@ -128,6 +136,12 @@ LAUNCH_COUNT: dict = {}
 
 def launches() -> int:
     return sum(LAUNCH_COUNT.values())
+
+
+def add_launches(name: str, n: int):
+    """Tally kernels launched inside one multi-kernel entry point
+    (pg_arnoldi_step, pg_poly_chain)."""
+    LAUNCH_COUNT[name] = LAUNCH_COUNT.get(name, 0) + int(n)
 
 
 _FN: dict = {}

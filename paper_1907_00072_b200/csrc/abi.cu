@@ -332,7 +332,15 @@ static void build_dictionaries(const SellHost& h, const int32_t* col, const doub
     m->n_dval = (int)vtab_bits.size();
     any = true;
   }
-  if (any) m->slice_ptr8 = upload(sp8.data(), sp8.size(), m->bytes);
+  if (any) {
+    m->slice_ptr8 = upload(sp8.data(), sp8.size(), m->bytes);
+    // uniform slice widths (stencils): packed-stream offsets are computable
+    const int64_t st = h.n_slices > 0 ? sp8[1] - sp8[0] : 0;
+    bool uniform = st > 0;
+    for (int64_t s = 1; uniform && s + 1 < h.n_slices; ++s) uniform = sp8[s + 1] - sp8[s] == st;
+    const char* env = std::getenv("PG_SPMV_STRIDE");
+    m->stride8 = (uniform && !(env && std::atoi(env) == 0)) ? st : 0;
+  }
 }
 
 struct DeviceScope {

@@ -65,6 +65,8 @@ struct pg_matrix {
   int32_t* col;        // [padded]  SELL column indices (int32)
   double* val;         // [padded]  SELL values
   int64_t* slice_ptr8; // [n_slices+1] slice offsets of the packed 1-byte streams
+  int64_t stride8;     // > 0: every slice but the last spans stride8 bytes, so
+                       // slice_ptr8[s] = s * stride8 (no dependent load)
   uint8_t* col8;       // packed dictionary index of (col - row), or null
   int32_t* dtab;       // [256]    column-offset dictionary
   uint8_t* val8;       // [padded] dictionary index of the value bits, or null

@@ -66,6 +66,7 @@ struct SellArgs {
   const int32_t* __restrict__ dtab;
   const uint8_t* __restrict__ val8;
   const double* __restrict__ vtab;
+  int64_t stride8;  // pg_matrix::stride8
 };
 
 // Matrix-stream loads.  With l2_keep the index/value lines carry an L2
@@ -331,15 +332,17 @@ __global__ void __launch_bounds__(kSellThreads,
 // table; x gathered from global memory (L1/L2).  Index words are
 // software-pipelined two 4-entry chunks ahead; full chunks run without
 // predicates, only the row's last partial chunk is predicated.
+// avail: index words present in this lane's slice (>= the row's own count);
+// the first two are requested before the row length arrives.
 __device__ __forceinline__ double row_sum_pairs_global(const uint32_t* __restrict__ pw, int len,
-                                                       int64_t row,
+                                                       int avail, int64_t row,
                                                        const double* __restrict__ x,
                                                        const PairEnt* s_ptab) {
   double acc = 0.0;
-  const int nq = (len + 3) >> 2;
   uint32_t n0 = 0, n1 = 0;
-  if (nq > 0) n0 = __ldcs(pw);
-  if (nq > 1) n1 = __ldcs(pw + PG_SLICE);
+  if (avail > 0) n0 = __ldcs(pw);
+  if (avail > 1) n1 = __ldcs(pw + PG_SLICE);
+  const int nq = (len + 3) >> 2;
   const double* xr = x + row;
   for (int q = 0; q < nq; ++q) {
     const uint32_t pb = n0;
@@ -356,6 +359,31 @@ __device__ __forceinline__ double row_sum_pairs_global(const uint32_t* __restric
     for (int u = 0; u < 4; ++u)
       if (u < left) acc = __dadd_rn(acc, __dmul_rn(pe[u].v, xv[u]));
   }
+  return acc;
+}
+
+// Rows of at most 8 stored entries (7-point stencils): both index words, all
+// table entries and all gathers are issued before the first add, so the row
+// costs one gather round trip instead of one per 4-entry chunk.
+__device__ __forceinline__ double row_sum_pairs_short(const uint32_t* __restrict__ pw, int len,
+                                                      int64_t row,
+                                                      const double* __restrict__ x,
+                                                      const PairEnt* s_ptab) {
+  const uint32_t w0 = __ldcs(pw);
+  const uint32_t w1 = len > 4 ? __ldcs(pw + PG_SLICE) : 0u;
+  const double* xr = x + row;
+  double v[8], xv[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const uint32_t idx = ((u < 4 ? w0 : w1) >> (8 * (u & 3))) & 255u;
+    const int4 raw = reinterpret_cast<const int4*>(s_ptab)[idx];
+    v[u] = __hiloint2double(raw.y, raw.x);
+    xv[u] = (u < len) ? __ldg(xr + raw.w) : 0.0;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
   return acc;
 }
 
@@ -376,10 +404,16 @@ __global__ void __launch_bounds__(kSellThreads, PG_SELL_DICT_MIN_BLOCKS)
     if (row < 0) continue;
     const int64_t s = lane >> 5;
     const int len = __ldg(a.row_len + lane);
-    const int64_t base8 = __ldg(a.slice_ptr8 + s) + 4 * (lane & 31);
+    // uniform slices: the stream offset needs no load, so the pair words are
+    // requested together with the row length (one round trip less per row)
+    const int64_t base8 =
+        (a.stride8 > 0 ? s * a.stride8 : __ldg(a.slice_ptr8 + s)) + 4 * (lane & 31);
     const Pre pre = epi_load<MODE>(e, x, row);
-    const double ax = row_sum_pairs_global(reinterpret_cast<const uint32_t*>(pair8 + base8), len,
-                                           row, x, s_ptab);
+    const int avail = a.stride8 > 0 ? (int)(a.stride8 >> 7) : (len + 3) >> 2;
+    const uint32_t* pw = reinterpret_cast<const uint32_t*>(pair8 + base8);
+    const double ax = (avail <= 2 && len > 0)
+                          ? row_sum_pairs_short(pw, len, row, x, s_ptab)
+                          : row_sum_pairs_global(pw, len, avail, row, x, s_ptab);
     const double r = epilogue<MODE>(e, pre, row, ax);
     if (MODE == kResid) local = __fma_rn(r, r, local);
   }
@@ -726,6 +760,7 @@ static SellArgs args_of(const pg_matrix* m) {
   a.dtab = m->dtab;
   a.val8 = m->val8;
   a.vtab = m->vtab;
+  a.stride8 = m->stride8;
   return a;
 }
 

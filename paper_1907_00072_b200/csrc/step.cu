@@ -1,0 +1,155 @@
+// libpgmres: whole Arnoldi steps and polynomial chains as single host calls.
+//
+// The Python solver used to issue every kernel of an Arnoldi step (d fused
+// passes, the wrapper SpMV, three CGS2 phases, the normalisation, the copy of
+// the step's scalars to pinned memory) through ctypes: ~20 calls and ~0.2 ms
+// of interpreter time per step, about half the GPU time of a cfg2 step, so the
+// one-step look-ahead had little slack.  pg_arnoldi_step / pg_poly_chain do
+// the same launches in C++ (same kernels, same order, same arguments as the
+// per-kernel entry points: results are bit-identical), one call per step.
+
+#include "internal.cuh"
+
+struct pg_event {
+  cudaEvent_t ev;
+  int device;
+};
+
+namespace {
+
+// a nested entry point failed: keep its status and its message
+void ok(int code) {
+  if (code != PG_OK) {
+    char msg[512];
+    pg_last_error(msg, sizeof msg);
+    throw pg::Error(code, msg);
+  }
+}
+
+// d fused monomial passes, out = (base +) p(A) x  (Engine.poly)
+void poly_chain(const pg_matrix* m, const double* y, int d, const double* x, const double* base,
+                double* out, double* acc, double* w0, double* w1, void* st) {
+  if (d == 0) {
+    ok(pg_scale_add(base, y[0], x, m->nrows, out, st));
+    return;
+  }
+  const double* cur = x;
+  double* ws[2] = {w0, w1};
+  for (int k = 1; k <= d; ++k) {
+    const bool last = k == d;
+    const int flags = (k == 1 ? PG_PASS_FIRST : 0) | (last ? 0 : PG_PASS_WRITE_W);
+    double* nxt = ws[k & 1];
+    ok(pg_poly_pass(m, cur, k > 1 ? acc : nullptr, last ? base : nullptr, last ? out : acc,
+                    last ? nullptr : nxt, y[0], y[k], flags, st));
+    cur = nxt;
+  }
+}
+
+void record(pg_event* e, void* st) {
+  if (e) PG_CUDA(cudaEventRecord(e->ev, pg::as_stream(st)));
+}
+
+}  // namespace
+
+using namespace pg;
+
+extern "C" {
+
+PG_API int pg_event_create(int device, pg_event** out) {
+  return guard([&] {
+    PG_REQUIRE(out, PG_ERR_PARAMETER, "out is null");
+    int prev = 0;
+    PG_CUDA(cudaGetDevice(&prev));
+    PG_CUDA(cudaSetDevice(device));
+    pg_event* e = new pg_event();
+    e->device = device;
+    const cudaError_t rc = cudaEventCreate(&e->ev);
+    cudaSetDevice(prev);
+    if (rc != cudaSuccess) {
+      delete e;
+      throw Error(PG_ERR_CUDA, std::string("cudaEventCreate: ") + cudaGetErrorString(rc));
+    }
+    *out = e;
+  });
+}
+
+PG_API int pg_event_destroy(pg_event* e) {
+  return guard([&] {
+    if (!e) return;
+    cudaEventDestroy(e->ev);
+    delete e;
+  });
+}
+
+PG_API int pg_event_record(pg_event* e, void* stream) {
+  return guard([&] {
+    PG_REQUIRE(e, PG_ERR_PARAMETER, "event is null");
+    record(e, stream);
+  });
+}
+
+PG_API int pg_event_wait(pg_event* e) {
+  return guard([&] {
+    PG_REQUIRE(e, PG_ERR_PARAMETER, "event is null");
+    PG_CUDA(cudaEventSynchronize(e->ev));
+  });
+}
+
+PG_API int pg_event_elapsed(pg_event* start, pg_event* end, float* ms) {
+  return guard([&] {
+    PG_REQUIRE(start && end && ms, PG_ERR_PARAMETER, "null argument");
+    PG_CUDA(cudaEventElapsedTime(ms, start->ev, end->ev));
+  });
+}
+
+PG_API int pg_poly_chain(const pg_matrix* mat, const double* y, int d, const double* d_x,
+                         const double* d_base, double* d_out, double* d_acc, double* d_w0,
+                         double* d_w1, pg_event* ev_start, pg_event* ev_end, void* stream) {
+  return guard([&] {
+    PG_REQUIRE(mat && y && d_x && d_out && d >= 0, PG_ERR_PARAMETER, "null argument");
+    PG_REQUIRE(d == 0 || (d_acc && d_w0 && d_w1), PG_ERR_PARAMETER, "scratch vectors required");
+    record(ev_start, stream);
+    poly_chain(mat, y, d, d_x, d_base, d_out, d_acc, d_w0, d_w1, stream);
+    record(ev_end, stream);
+  });
+}
+
+PG_API int pg_arnoldi_step(const pg_matrix* mat, const double* y, int d, double* d_V, int64_t ld,
+                           int j, double* d_z, double* d_t, double* d_acc, double* d_w0,
+                           double* d_w1, double* d_ring, double* h_ring, pg_workspace* ws,
+                           pg_event* ev_done, pg_event* ev_chain0, pg_event* ev_chain1,
+                           void* stream) {
+  return guard([&] {
+    PG_REQUIRE(mat && d_V && d_z && d_ring && h_ring && ws && ev_done, PG_ERR_PARAMETER,
+               "null argument");
+    const int k = j + 1;
+    PG_REQUIRE(j >= 0 && k < PG_KMAX && ld >= mat->nrows, PG_ERR_PARAMETER,
+               "step index out of range");
+    const int64_t n = mat->nrows;
+    const double* vj = d_V + (int64_t)j * ld;
+    // z = A p(A) v_j  (gmres.py:112-113, 283), or z = A v_j without a polynomial
+    if (d >= 0) {
+      PG_REQUIRE(y && d_t, PG_ERR_PARAMETER, "polynomial step needs y and t");
+      record(ev_chain0, stream);
+      poly_chain(mat, y, d, vj, nullptr, d_t, d_acc, d_w0, d_w1, stream);
+      record(ev_chain1, stream);
+      ok(pg_spmv(mat, d_t, d_z, stream));
+    } else {
+      ok(pg_spmv(mat, vj, d_z, stream));
+    }
+    // CGS2 against v_0..v_{k-1}; w2/|w2| into column k (ortho.py:53-70)
+    double* c1 = d_ring;
+    double* c2 = d_ring + PG_KMAX;
+    double* nsq = d_ring + 2 * PG_KMAX;
+    double* col = d_V + (int64_t)k * ld;
+    ok(pg_cgs2_phase1(d_V, ld, k, d_z, n, c1, ws, stream));
+    ok(pg_cgs2_phase2(d_V, ld, k, d_z, n, c1, c2, ws, stream));
+    ok(pg_cgs2_phase3(d_V, ld, k, d_z, n, c1, c2, col, nsq, ws, stream));
+    ok(pg_normalize(col, nsq, n, col, stream));
+    PG_CUDA(cudaMemcpyAsync(h_ring, d_ring, sizeof(double) * (2 * PG_KMAX + 1),
+                            cudaMemcpyDeviceToHost, as_stream(stream)));
+    record(ev_done, stream);
+  });
+}
+
+}  // extern "C"

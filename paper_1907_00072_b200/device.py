@@ -323,6 +323,38 @@ def exchange_send_lists(shards, comm):
 # ---------------------------------------------------------------------------
 # the engine: every vector op of the solver, over the shard list
 # ---------------------------------------------------------------------------
+class PgEvent:
+    """A libpgmres-owned CUDA event (pg_event_*), with the two methods the
+    solver and bench.py use on torch events."""
+
+    def __init__(self, device_ordinal: int):
+        h = _lib.C.c_void_p()
+        _lib.call("pg_event_create", int(device_ordinal), _lib.C.byref(h))
+        self.h = h
+
+    def record(self, stream):
+        _lib.call("pg_event_record", self.h, stream)
+
+    def synchronize(self):
+        _lib.call("pg_event_wait", self.h)
+
+    def elapsed_time(self, end) -> float:
+        ms = _lib.C.c_float(0.0)
+        _lib.call("pg_event_elapsed", self.h, end.h, _lib.C.byref(ms))
+        return float(ms.value)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.pg_event_destroy(h)
+            self.h = None
+
+
+def _fast_steps_enabled() -> bool:
+    import os
+    return os.environ.get("PG_FAST_STEP", "1") != "0"
+
+
 class Engine:
     def __init__(self, shards, comm, n_global: int):
         self.shards = shards
@@ -335,6 +367,8 @@ class Engine:
         # ILU(0) left preconditioner (attach_ilu): when set, one operator
         # application is M^{-1} A v (IluPreconditionedOperator, gmres.py:63-95)
         self.ilu = None
+        self._fast = _fast_steps_enabled()
+        self._done_events = None
 
     # ---- construction -------------------------------------------------------
     @classmethod
@@ -418,6 +452,56 @@ class Engine:
         s = self.shards[0]
         _lib.call("pg_spmv", s.mat, ptr(xs[0]), ptr(t[0]), s.stream)
         self.precondition(t, ys)
+
+    @property
+    def fast_steps(self) -> bool:
+        """Whole Arnoldi steps / polynomial chains as one native call
+        (pg_arnoldi_step / pg_poly_chain): single shard, plain SpMV operator."""
+        return self._fast and self.P == 1 and not self.comm.distributed and self.ilu is None
+
+    def _chain_events(self):
+        if self.timer is None:
+            return None, None
+        s0 = self.shards[0]
+        return PgEvent(s0.dev_ord), PgEvent(s0.dev_ord)
+
+    def _time_chain(self, ev0, ev1, s, d, pass_vec_bytes):
+        """Record one chain of d fused passes in the bench timer (same byte
+        accounting as Engine.poly)."""
+        nbytes = nbytes12 = 0
+        for k, vec in enumerate(pass_vec_bytes):
+            nbytes += s.entry_bytes * s.nnz + (12 + vec) * s.n
+            nbytes12 += 12 * s.nnz + (12 + vec) * s.n
+        self.timer.append((ev0, ev1, nbytes, d, nbytes12))
+
+    @staticmethod
+    def _chain_vec_bytes(d, base):
+        return [8 * (int(k > 1) + 1 + int(k < d) + int(base and k == d)) for k in range(1, d + 1)]
+
+    def arnoldi_step(self, Vs, j: int, y, W, slot: int):
+        """One native call for Arnoldi step j (fast path of gmres._launch_step):
+        z = A p(A) v_j, CGS2 into column j+1, scalars copied to the pinned ring
+        slot behind a library event.  Returns a cgs2_fetch handle."""
+        s = self.shards[0]
+        if self._done_events is None:
+            self._done_events = [PgEvent(s.dev_ord), PgEvent(s.dev_ord)]
+        ev = self._done_events[slot]
+        if y is None:
+            d, yp = -1, None
+        else:
+            yarr = np.ascontiguousarray(y, dtype=np.float64)
+            d, yp = len(yarr) - 1, yarr.ctypes.data
+        c0, c1 = self._chain_events() if d > 0 else (None, None)
+        host = s.pinned[slot]
+        _lib.call("pg_arnoldi_step", s.mat, yp, d, ptr(Vs[0]), s.ld, j, ptr(W.z[0]),
+                  ptr(W.t[0]), ptr(W.acc[0]), ptr(W.w0[0]), ptr(W.w1[0]), ptr(s.ring[slot]),
+                  host.data_ptr(), s.ws, ev.h, c0.h if c0 else None, c1.h if c1 else None,
+                  s.stream)
+        # d passes (a scale for d = 0), wrapper SpMV, 3 CGS2 phases, normalisation
+        _lib.add_launches("pg_arnoldi_step", (max(d, 1) if d >= 0 else 0) + 5)
+        if c0 is not None:
+            self._time_chain(c0, c1, s, d, self._chain_vec_bytes(d, False))
+        return ev, host, j + 1
 
     def count_ops(self, counters, k: int):
         """Tally k operator applications (spmvs; prec_applies on ILU engines)."""
@@ -543,6 +627,18 @@ class Engine:
         d = len(y) - 1
         if self.ilu is not None and d > 0:
             return self._poly_generic(y, vs, out, acc, w0, w1, base)
+        if self.fast_steps:
+            s = self.shards[0]
+            yarr = np.asarray(y, dtype=np.float64)
+            c0, c1 = self._chain_events() if d > 0 else (None, None)
+            b = base[0] if base is not None else None
+            _lib.call("pg_poly_chain", s.mat, yarr.ctypes.data, d, ptr(vs[0]),
+                      ptr(b) if b is not None else None, ptr(out[0]), ptr(acc[0]), ptr(w0[0]),
+                      ptr(w1[0]), c0.h if c0 else None, c1.h if c1 else None, s.stream)
+            _lib.add_launches("pg_poly_chain", max(d, 1))
+            if c0 is not None:
+                self._time_chain(c0, c1, s, d, self._chain_vec_bytes(d, base is not None))
+            return
         if d == 0:
             for s, v, o, b in zip(self._each(), vs, out, base or [None] * self.P):
                 _lib.call("pg_scale_add", ptr(b) if b is not None else None, y[0], ptr(v), s.n,
