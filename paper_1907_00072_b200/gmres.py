@@ -220,6 +220,7 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
     cycles = 0
     true_relres = beta / norm_b
     converged = true_relres < tol
+    rho = None  # per-step residual contraction, for the look-ahead guess
     Hrot = np.empty((m + 1, m))
     cs = np.empty(m)
     sn = np.empty(m)
@@ -236,14 +237,23 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
         j = 0
         breakdown = False
         pending_row = None
+        cur_res = true_relres  # residual the next step starts from
         while j < m and total_iters < config.max_iters:
             # one step of look-ahead: step j+1's device work (it only needs
             # v_{j+1}, already normalized on the device) is queued before the
             # host waits for step j's scalars, so the GPU never idles during
             # the host Givens update.  If step j ends the cycle, the queued
             # step is abandoned unused (no counter, no history row).
+            # ... unless step j is predicted to converge: the residual
+            # history's last contraction factor, applied once more, lands
+            # under 2 tol -- then the look-ahead would most likely be wasted
+            # (a whole step of device work), while a wrong guess only costs
+            # one un-overlapped host round trip.
+            if handle is None:  # the previous step skipped its look-ahead
+                handle = _launch_step(e, W, poly, j, plan)
             ahead = None
-            if j + 1 < m and total_iters + 1 < config.max_iters:
+            likely_done = rho is not None and cur_res * rho < 2.0 * tol
+            if j + 1 < m and total_iters + 1 < config.max_iters and not likely_done:
                 ahead = _launch_step(e, W, poly, j + 1, plan)
             c1, c2, nsq = e.cgs2_fetch(handle)
             handle = ahead
@@ -280,6 +290,9 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
             total_iters += 1
             j += 1
             implicit = abs(g[j]) / norm_b
+            if cur_res > 0.0:
+                rho = implicit / cur_res  # last per-step contraction (kept across cycles)
+            cur_res = implicit
             pending_row = (total_iters, implicit)
             if step_breakdown:
                 breakdown = True

@@ -463,3 +463,22 @@ def test_spmv_kernel_variants_bitwise(env, monkeypatch):
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy(), O.matvec(x))
         op.close()
+
+
+def test_native_step_path_is_bitwise_the_kernel_by_kernel_path(golden, monkeypatch):
+    """pg_arnoldi_step / pg_poly_chain (one native call per Arnoldi step or
+    polynomial chain) issue the same kernels as the per-kernel entry points:
+    the whole solve, x and history, is bit-identical."""
+    a, _ = golden
+    out = []
+    for fast in ("1", "0"):
+        monkeypatch.setenv("PG_FAST_STEP", fast)
+        c = pg.CostCounters()
+        op = pg.DeviceMatrixOperator(_lap64(golden), c)
+        assert op.engine.fast_steps == (fast == "1")
+        p = pg.PolyCoefficients(10, a["cfg1_y10"], 1.0)
+        res = pg.solve(op, a["cfg1_b"], right_prec=p, config=pg.GmresConfig(15, 1e-10))
+        out.append((res.x, res.history, c.as_dict(), res.cycles))
+        op.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1] and out[0][2] == out[1][2] and out[0][3] == out[1][3] > 1
