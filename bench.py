@@ -372,12 +372,14 @@ def run_ours(args):
 
 # pg_matrix_stats()[11]: the SELL kernel pg_spmv / pg_poly_pass run (spmv.cu)
 KERNEL_NAMES = {0: "sell_kernel<kPoly,0,0>", 1: "sell_kernel<kPoly,1,1>",
-                2: "sell_pair_kernel<kPoly>", 3: "sell_win_kernel<kPoly>"}
+                2: "sell_pair_kernel<kPoly>", 3: "sell_win_kernel<kPoly>",
+                4: "sell_pair_short_kernel<kPoly>"}
 MATRIX_FORMATS = {
     0: "SELL-C-sigma (int32 column + f64 value, 12 B/entry)",
     1: "dictionary SELL (1 B offset + 1 B value index)",
     2: "pair-dictionary SELL (1 B (offset, value) index), global x gathers",
     3: "pair-dictionary SELL (1 B/entry), x windows staged by a TMA ring",
+    4: "pair-dictionary SELL (1 B/entry), rows <= 8 entries, one gather round trip",
 }
 
 

@@ -88,7 +88,8 @@ PG_API int pg_matrix_destroy(pg_matrix* mat);
  *              matrix-stream bytes per entry of the kernel pg_spmv runs
  *              (1 = pair dictionary, 2 = two dictionary streams, 12 = plain),
  *              that kernel (0 plain SELL, 1 two-stream dictionary, 2 pair
- *              dictionary with global gathers, 3 windowed pair TMA ring)} */
+ *              dictionary with global gathers, 3 windowed pair TMA ring,
+ *              4 pair dictionary, short uniform rows)} */
 PG_API int pg_matrix_stats(const pg_matrix* mat, int64_t* stats);
 
 /* ---- reduction workspace (one per stream) --------------------------------

@@ -482,7 +482,8 @@ PG_API int pg_matrix_stats(const pg_matrix* m, int64_t* s) {
     s[8] = m->col8 ? 1 : 4;  // bytes per stored column entry
     s[9] = m->val8 ? 1 : 8;  // bytes per stored value entry
     // the kernel launch_sell picks for 16-byte aligned vectors (spmv.cu)
-    s[11] = m->pair8 ? (m->wtab ? 3 : 2) : (m->col8 || m->val8) ? 1 : 0;
+    s[11] = m->pair8 ? (m->wtab ? 3 : (m->stride8 > 0 && m->stride8 <= 256) ? 4 : 2)
+                     : (m->col8 || m->val8) ? 1 : 0;
     s[10] = m->pair8 ? 1 : (s[8] + s[9]);
   });
 }

@@ -387,6 +387,38 @@ __device__ __forceinline__ double row_sum_pairs_short(const uint32_t* __restrict
   return acc;
 }
 
+// Uniform slices of at most 8 entries per row only (7-point stencils): the
+// short-row body alone, so the kernel needs fewer registers than the general
+// pair kernel and more warps fit on an SM.
+#ifndef PG_PAIR_SHORT_MIN_BLOCKS
+#define PG_PAIR_SHORT_MIN_BLOCKS 4
+#endif
+template <int MODE>
+__global__ void __launch_bounds__(kSellThreads, PG_PAIR_SHORT_MIN_BLOCKS)
+    sell_pair_short_kernel(SellArgs a, const uint8_t* __restrict__ pair8,
+                           const PairEnt* __restrict__ ptab, const double* __restrict__ x,
+                           Epi e, double* partials, unsigned int* counter, double* nsq) {
+  pdl_entry();
+  __shared__ PairEnt s_ptab[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_ptab[i] = ptab[i];
+  __syncthreads();
+  double local = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t lane = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lane < a.nlanes;
+       lane += stride) {
+    const int64_t row = lane_row(a, lane);
+    if (row < 0) continue;
+    const int len = __ldg(a.row_len + lane);
+    const Pre pre = epi_load<MODE>(e, x, row);
+    const uint32_t* pw =
+        reinterpret_cast<const uint32_t*>(pair8 + (lane >> 5) * a.stride8 + 4 * (lane & 31));
+    const double ax = len > 0 ? row_sum_pairs_short(pw, len, row, x, s_ptab) : 0.0;
+    const double r = epilogue<MODE>(e, pre, row, ax);
+    if (MODE == kResid) local = __fma_rn(r, r, local);
+  }
+  finish_resid<MODE>(local, partials, counter, nsq);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kSellThreads, PG_SELL_DICT_MIN_BLOCKS)
     sell_pair_kernel(SellArgs a, const uint8_t* __restrict__ pair8,
@@ -846,8 +878,23 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
     int64_t blocks = (a.nlanes + kSellThreads - 1) / kSellThreads;
     const int64_t cap = (MODE == kResid) ? kMaxBlocks : (int64_t)sms[dev] * per_sm;
     if (blocks > cap) blocks = cap;
-    launch_k(sell_pair_kernel<MODE>, (int)blocks, kSellThreads, 0, st, a,
-             (const uint8_t*)m->pair8, (const PairEnt*)m->ptab, x, e, part, cnt, nsq);
+    static int short_ok = -1, short_bps = -1;
+    if (short_ok < 0) {
+      const char* s = std::getenv("PG_SPMV_PAIR_SHORT");
+      short_ok = s ? std::atoi(s) : 1;
+      const char* b = std::getenv("PG_SPMV_SHORT_BLOCKS_PER_SM");
+      short_bps = b ? std::atoi(b) : PG_PAIR_SHORT_MIN_BLOCKS;
+    }
+    if (short_ok && m->stride8 > 0 && m->stride8 <= 2 * 4 * PG_SLICE) {
+      int64_t sb = (a.nlanes + kSellThreads - 1) / kSellThreads;
+      const int64_t scap = (MODE == kResid) ? kMaxBlocks : (int64_t)sms[dev] * short_bps;
+      if (sb > scap) sb = scap;
+      launch_k(sell_pair_short_kernel<MODE>, (int)sb, kSellThreads, 0, st, a,
+               (const uint8_t*)m->pair8, (const PairEnt*)m->ptab, x, e, part, cnt, nsq);
+    } else {
+      launch_k(sell_pair_kernel<MODE>, (int)blocks, kSellThreads, 0, st, a,
+               (const uint8_t*)m->pair8, (const PairEnt*)m->ptab, x, e, part, cnt, nsq);
+    }
   } else if (m->use_tma && !m->col8 && !m->val8) {  // the ring streams the uncompressed arrays
     static bool attr[4][64] = {};
     if (!attr[MODE][dev]) {
