@@ -177,6 +177,10 @@ def build_poly_or_auto(op, v0, deg: int, counters: CostCounters,
     (oracle.degree_policy_shared)."""
     if deg < 1:
         return build_poly(op, v0, deg, counters, seed_mode), None
+    # the tall-skinny kernels take PG_KMAX columns: a request past that is
+    # decided on the leading KMAX-2 degrees (a failing leading Gram block
+    # fails every larger one; in practice the exact decision stops near 20)
+    deg = min(deg, KMAX - 2)
     Gfull, seed_norm = _device_power_gram(op, v0, deg + 1, counters)
     counters.scalar_dots += 1
     full = _normal_equations(Gfull, deg, counters)
