@@ -151,7 +151,6 @@ static void free_matrix(pg_matrix* m) {
   cudaFree(m->perm);
   cudaFree(m->col);
   cudaFree(m->val);
-  cudaFree(m->unit_slice);
   cudaFree(m->col8);
   cudaFree(m->slice_ptr8);
   cudaFree(m->dtab);
@@ -429,33 +428,7 @@ PG_API int pg_matrix_create(int device, int64_t nrows, int64_t ncols, const int6
       if (sigma > 1) m->perm = upload(h.perm.data(), h.perm.size(), m->bytes);
       m->col = upload(col.data(), (size_t)h.padded, m->bytes);
       m->val = upload(val.data(), (size_t)h.padded, m->bytes);
-      // TMA streaming units: greedy runs of whole slices <= kUnitEntries entries
-      std::vector<int32_t> units(1, 0);
-      // the TMA ring is opt-in: on the measured configs the plain
-      // one-row-per-thread kernel (all index/value loads issued before the
-      // gathers) reaches a higher fraction of HBM
-      m->use_tma = std::getenv("PG_SPMV_TMA") != nullptr;
-      // L2 evict_last policy on the matrix stream (opt-in, PG_SPMV_L2KEEP=1):
-      // measured slower on config 2 (the pinned lines crowd out the x gathers
-      // and vectors), so streaming evict_first loads are the default
-      {
-        const char* kv = std::getenv("PG_SPMV_L2KEEP");
-        m->l2_keep = kv ? std::atoi(kv) : 0;
-      }
       build_dictionaries(h, col.data(), val.data(), m);
-      int64_t acc = 0;
-      for (int64_t s = 0; s < h.n_slices; ++s) {
-        const int64_t ne = h.slice_ptr[s + 1] - h.slice_ptr[s];
-        if (ne > kUnitEntries) m->use_tma = false;
-        if (acc + ne > kUnitEntries && acc > 0) {
-          units.push_back((int32_t)s);
-          acc = 0;
-        }
-        acc += ne;
-      }
-      units.push_back((int32_t)h.n_slices);
-      m->n_units = (int64_t)units.size() - 1;
-      m->unit_slice = upload(units.data(), units.size(), m->bytes);
     } catch (...) {
       free_matrix(m);
       throw;

@@ -83,10 +83,6 @@ struct pg_matrix {
   int n_wgrp, win_elems;
   int win_b8;          // largest per-block byte span of each packed stream
   int32_t wlo[32], wstart[32], wlen[32];
-  int32_t* unit_slice; // [n_units+1] first slice of each TMA streaming unit
-  int64_t n_units;
-  bool use_tma;        // every slice fits a ring stage (kUnitEntries)
-  int l2_keep;         // matrix loads carry an L2 evict_last policy
   size_t bytes;
 };
 
@@ -98,8 +94,6 @@ struct __align__(16) PairEnt {
   int32_t woff;  // byte offset in the block's x window (0 without a window plan)
   int32_t doff;  // column offset col - row (global-gather kernel)
 };
-// Entries per TMA streaming unit of the SpMV ring (12 B each: int32 + f64).
-constexpr int kUnitEntries = 3072;
 // Rows per block of the windowed dictionary SpMV and its window budget
 // (elements per buffer; two buffers per block).
 #ifndef PG_WIN_ROWS

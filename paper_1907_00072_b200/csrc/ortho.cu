@@ -246,124 +246,6 @@ __global__ void __launch_bounds__(kTileThreads)
   }
 }
 
-// ---------------------------------------------------------------------------
-// TMA ring for CGS2 phases 1-2 (default for k > 12).  One persistent CTA per
-// SM: a producer warp streams 128-row tiles of the k basis columns and z into
-// a `stages`-deep shared-memory ring with cp.async.bulk (one 1 KB bulk copy
-// per column segment, completion counted on an mbarrier), while 8 consumer
-// warps reduce the previous tiles out of shared memory.  >150 KB per SM stays
-// in flight with one issuing thread, which the 16-byte cp.async tiles
-// (tile_kernel) could not sustain at n = 1e6.
-// ---------------------------------------------------------------------------
-constexpr int kRingRows = 128;
-constexpr int kRingConsumerWarps = 8;
-constexpr int kRingThreads = (kRingConsumerWarps + 1) * 32;
-constexpr int kRingMaxStages = 8;
-constexpr size_t kRingSmemMax = 220 * 1024;
-
-__device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kRingConsumerWarps * 32) : "memory");
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(kRingThreads, 1)
-    ring_kernel(const double* __restrict__ V, int64_t ld, int k, const double* __restrict__ z,
-                int64_t n, const double* __restrict__ c1, int stages, double* partials,
-                unsigned int* counter, double* out) {
-  pdl_entry();
-  extern __shared__ __align__(128) unsigned char ring_raw[];
-  double* sbuf = reinterpret_cast<double*>(ring_raw);
-  __shared__ __align__(8) uint64_t full[kRingMaxStages];
-  __shared__ __align__(8) uint64_t empty[kRingMaxStages];
-  __shared__ double c1s[PG_KMAX];
-  __shared__ double w1s[kRingRows];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ncol = k + 1;
-  const size_t stage_elems = (size_t)ncol * kRingRows;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kRingConsumerWarps);
-    }
-    mbar_fence_init();
-  }
-  if (MODE == kUpdDots)
-    for (int i = threadIdx.x; i < k; i += blockDim.x) c1s[i] = c1[i];
-  __syncthreads();
-  const int64_t ntiles = (n + kRingRows - 1) / kRingRows;
-
-  double acc[kColsPerWarp];
-#pragma unroll
-  for (int m = 0; m < kColsPerWarp; ++m) acc[m] = 0.0;
-
-  if (warp == kRingConsumerWarps) {
-    if (lane == 0) {
-      int it = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int s = it % stages;
-        mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-        const int64_t r0 = tile * kRingRows;
-        const int64_t rows = min((int64_t)kRingRows, n - r0);
-        const uint32_t bytes = (uint32_t)(((rows + 1) & ~int64_t(1)) * 8);  // 16-B multiple
-        double* dst = sbuf + (size_t)s * stage_elems;
-        mbar_expect_tx(&full[s], bytes * (uint32_t)ncol);
-        for (int c = 0; c < k; ++c)
-          bulk_g2s(dst + (size_t)c * kRingRows, V + (int64_t)c * ld + r0, bytes, &full[s]);
-        bulk_g2s(dst + (size_t)k * kRingRows, z + r0, bytes, &full[s]);
-      }
-    }
-  } else {
-    int it = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const int s = it % stages;
-      const int rows = (int)min((int64_t)kRingRows, n - tile * kRingRows);
-      mbar_wait(&full[s], (it / stages) & 1);
-      const double* S = sbuf + (size_t)s * stage_elems;
-      const double* vec = S + (size_t)k * kRingRows;
-      if (MODE == kUpdDots) {
-        if (threadIdx.x < kRingRows) {
-          const int r = threadIdx.x;
-          double w1 = 0.0;
-          if (r < rows) {
-            const double t = row_proj(k, c1s, [&](int i) { return S[i * kRingRows + r]; });
-            w1 = __dsub_rn(vec[r], t);
-          }
-          w1s[r] = w1;
-        }
-        consumer_sync();
-        vec = w1s;
-      }
-#pragma unroll
-      for (int m = 0; m < kColsPerWarp; ++m) {
-        const int i = warp + m * kRingConsumerWarps;
-        if (i < k) {
-          const double* col = S + (size_t)i * kRingRows;
-#pragma unroll
-          for (int q = 0; q < kRingRows / 32; ++q) {
-            const int r = lane + 32 * q;
-            if (r < rows) acc[m] = __fma_rn(col[r], vec[r], acc[m]);
-          }
-        }
-      }
-      if (MODE == kUpdDots) consumer_sync();  // w1s is rewritten by the next tile
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
-#pragma unroll
-    for (int m = 0; m < kColsPerWarp; ++m) {
-      double v = acc[m];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      const int i = warp + m * kRingConsumerWarps;
-      if (lane == 0 && i < k) partials[(size_t)blockIdx.x * k + i] = v;
-    }
-  }
-  last_block_reduce(partials, counter, k, out);
-}
-
-// Phase 3 / GEMV: one thread per row, streaming the k columns from HBM.
-//   PHASE3: w2 = (z - V c1) - V c2 -> out, sum w2^2 -> nsq
-//   GEMV:   out = V y
 constexpr int kRowThreads = 256;
 
 template <bool PHASE3>
@@ -720,46 +602,6 @@ static bool use_tile_cgs2(int k) {
   return force_tile == 1 || k > chunk_kmax;
 }
 
-// Phases 1-2 for wide bases: the multi-stage cp.async tile kernel; the
-// TMA-bulk ring is opt-in (PG_CGS2_RING=1) -- one producer thread issuing a
-// 1 KB bulk copy per column segment measured issue-bound (3.1-4.2 TB/s).
-static bool use_ring_cgs2() {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = std::getenv("PG_CGS2_RING");
-    v = s ? std::atoi(s) != 0 : 0;
-  }
-  return v == 1;
-}
-
-template <int MODE>
-static void launch_ring(const double* V, int64_t ld, int k, const double* z, int64_t n,
-                        const double* c1, double* out, pg_workspace* ws, cudaStream_t st) {
-  check_ws(ws);
-  PG_REQUIRE(ld % 2 == 0, PG_ERR_PARAMETER, "leading dimension must be even");
-  PG_REQUIRE(((uintptr_t)V & 15) == 0 && ((uintptr_t)z & 15) == 0, PG_ERR_PARAMETER,
-             "ring operands must be 16-byte aligned");
-  const int64_t ntiles = (n + kRingRows - 1) / kRingRows;
-  if (ntiles == 0) {
-    PG_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * k, st));
-    return;
-  }
-  const size_t stage_bytes = sizeof(double) * (size_t)(k + 1) * kRingRows;
-  int stages = (int)(kRingSmemMax / stage_bytes);
-  if (stages > kRingMaxStages) stages = kRingMaxStages;
-  const int dev = ws->device;
-  static bool attr[4][64] = {};
-  if (!attr[MODE][dev]) {
-    PG_CUDA(cudaFuncSetAttribute(ring_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kRingSmemMax));
-    attr[MODE][dev] = true;
-  }
-  int g = ws->num_sms;
-  if (ntiles < g) g = (int)ntiles;
-  launch_k(ring_kernel<MODE>, g, kRingThreads, stage_bytes * stages, st, V, ld, k, z, n, c1, stages, ws->partials, ws->counter, out);
-  check_launch();
-}
-
 template <int MODE>
 static void launch_chunk_dots(const double* V, int64_t ld, int k, const double* z, int64_t n,
                               const double* c1, double* out, pg_workspace* ws, cudaStream_t st) {
@@ -844,8 +686,6 @@ PG_API int pg_cgs2_phase1(const double* d_V, int64_t ld, int k, const double* d_
     PG_REQUIRE(d_z && d_c1, PG_ERR_PARAMETER, "null argument");
     if (!use_tile_cgs2(k))
       launch_chunk_dots<1>(d_V, ld, k, d_z, n, nullptr, d_c1, ws, as_stream(stream));
-    else if (use_ring_cgs2())
-      launch_ring<kDots>(d_V, ld, k, d_z, n, nullptr, d_c1, ws, as_stream(stream));
     else
       launch_tile<kDots>(d_V, ld, k, d_z, n, nullptr, d_c1, ws, as_stream(stream));
   });
@@ -858,8 +698,6 @@ PG_API int pg_cgs2_phase2(const double* d_V, int64_t ld, int k, const double* d_
     PG_REQUIRE(d_z && d_c1 && d_c2, PG_ERR_PARAMETER, "null argument");
     if (!use_tile_cgs2(k))
       launch_chunk_dots<2>(d_V, ld, k, d_z, n, d_c1, d_c2, ws, as_stream(stream));
-    else if (use_ring_cgs2())
-      launch_ring<kUpdDots>(d_V, ld, k, d_z, n, d_c1, d_c2, ws, as_stream(stream));
     else
       launch_tile<kUpdDots>(d_V, ld, k, d_z, n, d_c1, d_c2, ws, as_stream(stream));
   });

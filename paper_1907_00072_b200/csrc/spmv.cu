@@ -19,10 +19,11 @@
 //    dictionary -- constant-coefficient stencils): 1-byte column-offset and
 //    value indices packed 4 per 32-bit lane word (abi.cu), decoded through
 //    shared-memory tables; ~2 B of matrix stream per entry instead of 12.
-//  * sell_tma_kernel (opt-in, PG_SPMV_TMA=1): one persistent CTA per SM, a
-//    producer warp streams runs of slices into a shared-memory ring with
-//    cp.async.bulk + mbarrier; measured slower than sell_kernel (the gathers,
-//    not the matrix stream, bound it), kept for reference.
+//  * sell_pair_kernel / sell_pair_short_kernel: one 1-byte (offset, value)
+//    pair index per entry; rows of <= 8 entries issue all gathers at once.
+//  * sell_win_kernel: natural-order stencil rows, x windows + pair stream
+//    staged by a warp-specialised TMA ring (see its comment).
+//  * sell_kernel<kRoot>: the root-product form of the polynomial (pg_root_pass).
 
 #include <cstdlib>
 
@@ -46,10 +47,6 @@ constexpr int kSellMinBlocks = PG_SELL_MIN_BLOCKS;
 #define PG_SELL_UNROLL 4
 #endif
 constexpr int kUnroll = PG_SELL_UNROLL;
-constexpr int kConsumerWarps = 16;
-constexpr int kTmaThreads = (kConsumerWarps + 1) * 32;
-constexpr int kStages = 6;
-constexpr size_t kTmaSmem = (size_t)kStages * kUnitEntries * (sizeof(int32_t) + sizeof(double));
 
 struct SellArgs {
   const int64_t* __restrict__ slice_ptr;
@@ -60,7 +57,6 @@ struct SellArgs {
   const double* __restrict__ val;
   int64_t nrows;
   int64_t nlanes;
-  int l2_keep;  // matrix stream marked L2 evict_last (resident across a pass chain)
   const int64_t* __restrict__ slice_ptr8;  // packed 1-byte stream offsets
   const uint8_t* __restrict__ col8;  // dictionary-compressed streams (abi.cu)
   const int32_t* __restrict__ dtab;
@@ -68,33 +64,6 @@ struct SellArgs {
   const double* __restrict__ vtab;
   int64_t stride8;  // pg_matrix::stride8
 };
-
-// Matrix-stream loads.  With l2_keep the index/value lines carry an L2
-// evict_last policy: a degree-d polynomial streams the same A d+1 times in a
-// row, and when A fits in the 126 MB L2 (config 2: 83 MB) passes 2..d+1 read
-// it from L2 instead of HBM.  Otherwise they are streaming (evict_first) loads.
-__device__ __forceinline__ uint64_t l2_policy_keep() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-// mode 0: streaming (evict-first), 1: L2 evict_last policy, 2: default caching
-__device__ __forceinline__ int ld_mat(const int32_t* p, int mode, uint64_t pol) {
-  if (mode == 0) return __ldcs(p);
-  if (mode == 2) return __ldg(p);
-  int v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;\n"
-               : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double ld_mat(const double* p, int mode, uint64_t pol) {
-  if (mode == 0) return __ldcs(p);
-  if (mode == 2) return __ldg(p);
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n"
-               : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
 
 struct Epi {
   const double* acc_in;
@@ -308,17 +277,15 @@ __global__ void __launch_bounds__(kSellThreads,
     const int len = __ldg(a.row_len + lane);
     const int64_t base = __ldg(a.slice_ptr + s) + (lane & 31);
     const Pre pre = epi_load<MODE>(e, x, row);
-    const int keep = a.l2_keep;
-    const uint64_t pol = keep == 1 ? l2_policy_keep() : 0;
     double ax;
     if (CM || VM) {
       const int64_t base8 = __ldg(a.slice_ptr8 + s) + 4 * (lane & 31);
       ax = row_sum_dict<CM, VM>(a, base, base8, (int)row, w, len, x, s_dtab, s_vtab);
     } else {
       ax = row_sum(
-          [&](int j) { return ld_mat(a.col + base + (int64_t)j * PG_SLICE, keep, pol); },
+          [&](int j) { return __ldcs(a.col + base + (int64_t)j * PG_SLICE); },
           [](int raw) { return raw; },
-          [&](int j) { return ld_mat(a.val + base + (int64_t)j * PG_SLICE, keep, pol); }, w,
+          [&](int j) { return __ldcs(a.val + base + (int64_t)j * PG_SLICE); }, w,
           len, x);
     }
     const double r = epilogue<MODE>(e, pre, row, ax);
@@ -700,82 +667,6 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
   finish_resid<MODE>(local, partials, counter, nsq);
 }
 
-// -------------------------------------------------------- TMA ring kernel --
-template <int MODE>
-__global__ void __launch_bounds__(kTmaThreads, 1)
-    sell_tma_kernel(SellArgs a, const int32_t* __restrict__ unit_slice, int64_t n_units,
-                    const double* __restrict__ x, Epi e, double* partials,
-                    unsigned int* counter, double* nsq) {
-  pdl_entry();
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  int32_t* scol = reinterpret_cast<int32_t*>(smem_raw);
-  double* sval = reinterpret_cast<double*>(smem_raw + (size_t)kStages * kUnitEntries * 4);
-  __shared__ __align__(8) uint64_t full[kStages];
-  __shared__ __align__(8) uint64_t empty[kStages];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  double local = 0.0;
-  if (warp == kConsumerWarps) {
-    // producer: one elected lane streams this CTA's units into the ring
-    if (lane == 0) {
-      int it = 0;
-      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-        const int s = it % kStages;
-        mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-        const int64_t e0 = __ldg(a.slice_ptr + __ldg(unit_slice + u));
-        const int64_t e1 = __ldg(a.slice_ptr + __ldg(unit_slice + u + 1));
-        const uint32_t ne = (uint32_t)(e1 - e0);
-        mbar_expect_tx(&full[s], ne * 12u);  // tx 0 (empty unit) completes at once
-        if (ne) {
-          bulk_g2s(scol + (size_t)s * kUnitEntries, a.col + e0, ne * 4u, &full[s]);
-          bulk_g2s(sval + (size_t)s * kUnitEntries, a.val + e0, ne * 8u, &full[s]);
-        }
-      }
-    }
-  } else {
-    // consumers: slices of this CTA's stream go round-robin to the 8 warps
-    int it = 0;
-    int64_t seen = 0;  // slices of earlier units in this CTA's stream
-    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-      const int s = it % kStages;
-      const int64_t s0 = __ldg(unit_slice + u), s1 = __ldg(unit_slice + u + 1);
-      const int64_t e0 = __ldg(a.slice_ptr + s0);
-      const int32_t* C = scol + (size_t)s * kUnitEntries;
-      const double* Vv = sval + (size_t)s * kUnitEntries;
-      int64_t first = s0 + ((warp - seen) % kConsumerWarps + kConsumerWarps) % kConsumerWarps;
-      if (first < s1) mbar_wait(&full[s], (it / kStages) & 1);
-      for (int64_t sl = first; sl < s1; sl += kConsumerWarps) {
-        const int64_t ln = sl * PG_SLICE + lane;
-        const int64_t row = lane_row(a, ln);
-        const int w = __ldg(a.slice_w + sl);
-        const int len = __ldg(a.row_len + ln);
-        const int off = (int)(__ldg(a.slice_ptr + sl) - e0) + lane;
-        const Pre pre = epi_load<MODE>(e, x, row);
-        const double ax = row_sum([&](int j) { return C[off + j * PG_SLICE]; },
-                                  [](int raw) { return raw; },
-                                  [&](int j) { return Vv[off + j * PG_SLICE]; }, w, len, x);
-        if (row >= 0) {
-          const double r = epilogue<MODE>(e, pre, row, ax);
-          if (MODE == kResid) local = __fma_rn(r, r, local);
-        }
-      }
-      seen += s1 - s0;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
-  }
-  finish_resid<MODE>(local, partials, counter, nsq);
-}
-
 static SellArgs args_of(const pg_matrix* m) {
   SellArgs a;
   a.slice_ptr = m->slice_ptr;
@@ -786,7 +677,6 @@ static SellArgs args_of(const pg_matrix* m) {
   a.val = m->val;
   a.nrows = m->nrows;
   a.nlanes = m->n_slices * PG_SLICE;
-  a.l2_keep = m->l2_keep;
   a.slice_ptr8 = m->slice_ptr8;
   a.col8 = m->col8;
   a.dtab = m->dtab;
@@ -895,17 +785,6 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
       launch_k(sell_pair_kernel<MODE>, (int)blocks, kSellThreads, 0, st, a,
                (const uint8_t*)m->pair8, (const PairEnt*)m->ptab, x, e, part, cnt, nsq);
     }
-  } else if (m->use_tma && !m->col8 && !m->val8) {  // the ring streams the uncompressed arrays
-    static bool attr[4][64] = {};
-    if (!attr[MODE][dev]) {
-      PG_CUDA(cudaFuncSetAttribute(sell_tma_kernel<MODE>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
-      attr[MODE][dev] = true;
-    }
-    int g = sms[dev];
-    if (m->n_units < g) g = (int)m->n_units;
-    launch_k(sell_tma_kernel<MODE>, g, kTmaThreads, kTmaSmem, st, a, m->unit_slice, m->n_units, x, e,
-                                                           part, cnt, nsq);
   } else {
     // one row per thread; reductions keep the grid within the partial slots
     int64_t blocks = (a.nlanes + kSellThreads - 1) / kSellThreads;
