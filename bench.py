@@ -222,10 +222,17 @@ def run_ours(args):
     max_iters = args.max_iters if args.max_iters else BENCH_MAX_ITERS.get(args.config, 200000)
     cfg = pg.GmresConfig(conf["m"], conf["tol"], max_iters, poly_form=args.poly_form)
 
+    def build(op, v0, c):
+        # "policy": the reference's construction (build, else auto-degree);
+        # "arnoldi": the harmonic-Ritz construction at the requested degree
+        if args.construction == "arnoldi":
+            return pg.build_poly_arnoldi(op, v0, conf["degree"], c), None
+        return pg.build_poly_or_auto(op, v0, conf["degree"], c)
+
     def step(b, v0):
         c = pg.CostCounters()
         op.counters = c
-        poly, pivot = pg.build_poly_or_auto(op, v0, conf["degree"], c)
+        poly, pivot = build(op, v0, c)
         res = pg.solve(op, b, right_prec=poly, config=cfg)
         return poly, pivot, res, c
 
@@ -290,7 +297,7 @@ def run_ours(args):
         t0 = time.perf_counter()
         cc = pg.CostCounters()
         op.counters = cc
-        p2, _ = pg.build_poly_or_auto(op, v0_pin, conf["degree"], cc)
+        p2, _ = build(op, v0_pin, cc)
         r2 = pg.solve(op, b_pin, right_prec=p2, config=cfg)
         x_host = r2.x  # CPU tensor (D2H inside the timed region)
         torch.cuda.synchronize()
@@ -333,6 +340,7 @@ def run_ours(args):
                 "restart_m": conf["m"], "tol": conf["tol"], "max_iters": max_iters,
                 "degree_requested": conf["degree"], "degree_effective": poly.degree,
                 "build_poly_failed_pivot": pivot, "poly_form": args.poly_form,
+                "construction": args.construction,
                 "iterations": res.iterations, "cycles": res.cycles,
                 "converged": bool(res.converged), "final_relres": res.final_relres,
                 "spmvs": c.spmvs, "dots": c.dots,
@@ -481,6 +489,9 @@ def main():
     # "monomial" = the reference's bit-identical evaluation (default, the
     # headline); "roots" = the Leja root-product form
     ap.add_argument("--poly-form", default="monomial", choices=["monomial", "roots"])
+    # "arnoldi" builds the requested degree from harmonic Ritz values (SURVEY
+    # f1) -- not the reference's construction, so not the headline
+    ap.add_argument("--construction", default="policy", choices=["policy", "arnoldi"])
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

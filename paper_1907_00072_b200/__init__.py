@@ -43,6 +43,7 @@ _LAZY = {
     "build_poly": "polyprec",
     "auto_degree": "polyprec",
     "build_poly_or_auto": "polyprec",
+    "build_poly_arnoldi": "polyprec",
     "dense_cholesky": "polyprec",
     "lambda_p_lambda": "polyprec",
     "RootPlan": "polyprec",

@@ -35,6 +35,10 @@ class PolyCoefficients:
     y: np.ndarray
     seed_norm: float
     seed_mode: str = "unspecified"
+    # roots of the residual polynomial 1 - z p(z), when the polynomial was
+    # built from them (build_poly_arnoldi); the root-product form uses them
+    # directly instead of re-deriving them from y.  Not a reference field.
+    roots: np.ndarray | None = None
 
     def __post_init__(self):
         object.__setattr__(self, "y", np.asarray(self.y, dtype=np.float64))
@@ -42,6 +46,11 @@ class PolyCoefficients:
             raise ParameterError("coefficient vector must have length degree + 1")
         if not np.all(np.isfinite(self.y)):
             raise ParameterError("polynomial coefficients must be finite")
+        if self.roots is not None:
+            r = np.asarray(self.roots, dtype=np.complex128)
+            if r.shape != (self.degree + 1,) or not np.all(np.isfinite(r)) or np.any(r == 0):
+                raise ParameterError("roots must be degree + 1 finite nonzero values")
+            object.__setattr__(self, "roots", r)
 
 
 @dataclass(frozen=True)
@@ -190,6 +199,77 @@ def build_poly_or_auto(op, v0, deg: int, counters: CostCounters,
     return _select_degree(full, deg, seed_norm, seed_mode), pivot
 
 
+def build_poly_arnoldi(op, v0, deg: int, counters: CostCounters | None = None,
+                       seed_mode: str = "unspecified") -> PolyCoefficients:
+    """Degree-``deg`` GMRES polynomial from harmonic Ritz values (SURVEY row
+    f1, "a stable construction"; PAPER.md:195-202 names the power basis's
+    ill-conditioning as the degree limit).  deg+1 Arnoldi steps on the operator
+    from the unit seed (device SpMV + CGS2), then on the host the harmonic
+    Ritz values of the (deg+1)-step Hessenberg -- the roots of the GMRES
+    residual polynomial 1 - z p(z), the same minimiser build_poly finds from
+    the normal equations (polyprec.py:125-147), without forming them.  Degrees
+    far past the power basis's ~13 stay well conditioned; evaluate them with
+    ``form="roots"``.  Costs deg+1 SpMVs, like build_poly.  No reference
+    counterpart, so it is checked against build_poly's polynomial at low
+    degree and by its residual minimisation at high degree."""
+    if counters is None:
+        counters = CostCounters()
+    if deg < 0:
+        raise ParameterError("polynomial degree must be non-negative")
+    e = _engine(op)
+    m = deg + 1
+    if m + 1 > KMAX:
+        raise ParameterError(f"degree {deg} exceeds the kernel limit {KMAX - 2}")
+    if isinstance(v0, torch.Tensor):
+        if v0.shape != (op.dimension,) and not (e.comm.distributed and v0.shape == (e.local_n,)):
+            raise DimensionMismatchError("seed vector length does not match operator")
+    else:
+        v0 = np.asarray(v0, dtype=np.float64)
+        if v0.shape != (op.dimension,) and not (e.comm.distributed and v0.shape == (e.local_n,)):
+            raise DimensionMismatchError("seed vector length does not match operator")
+    vs = e.ingest(v0)
+    seed_norm = float(np.sqrt(e.dot(vs, vs, slot=6)))
+    counters.scalar_dots += 1
+    if seed_norm == 0.0:
+        raise ParameterError("seed vector v0 must be nonzero")
+    V = e.cached_blocks("harmonic", m + 1)
+    z = e.cached_vecs("harmonic_z")
+    e.normalize_dev(vs, e.slot(6), [blk[0] for blk in V])
+    H = np.zeros((m + 1, m))
+    for j in range(m):
+        e.count_ops(counters, 1)
+        e.spmv([blk[j] for blk in V], z)
+        c1, c2, nsq = e.cgs2(V, j + 1, z)
+        counters.dots += 3
+        counters.scalar_dots += 2 * (j + 1) + 1
+        counters.vector_updates += 2 * (j + 1) + 1
+        H[:j + 1, j] = c1 + c2
+        H[j + 1, j] = np.sqrt(max(nsq, 0.0))
+        if not np.all(np.isfinite(H[:j + 2, j])):
+            raise ParameterError("non-finite Arnoldi data while building the polynomial")
+        if H[j + 1, j] <= 1e-14 * np.linalg.norm(H[:j + 2, j]):  # invariant subspace
+            m = j + 1
+            H = H[:m + 1, :m]
+            break
+    Hm = H[:m, :m]
+    em = np.zeros(m)
+    em[-1] = 1.0
+    T = Hm.copy()
+    if H[m, m - 1] != 0.0:
+        f = np.linalg.solve(Hm.T, em)
+        T[:, m - 1] += H[m, m - 1] ** 2 * f
+    theta = np.linalg.eigvals(T).astype(np.complex128)
+    if np.any(theta == 0) or not np.all(np.isfinite(theta)):
+        raise ParameterError("singular harmonic Ritz problem (operator singular on the seed space)")
+    # conjugate pairs exact: eigenvalues of a real matrix come in exact pairs;
+    # the monomial coefficients follow from the product (reporting / monomial form)
+    pi = np.array([1.0 + 0j])
+    for th in theta:
+        pi = np.convolve(pi, np.array([1.0, -1.0 / th]))
+    y = -pi.real[1:]
+    return PolyCoefficients(m - 1, y, seed_norm, seed_mode, roots=theta)
+
+
 POLY_FORMS = ("monomial", "roots")
 
 
@@ -288,7 +368,7 @@ def root_plan(p: PolyCoefficients) -> RootPlan:
         rs = ((_lib.PG_ROOT_REAL | _lib.PG_ROOT_RESID, float(p.y[0]), 0.0, 0.0, True),) \
             if th is not None else ()
         return RootPlan(0, np.zeros(0, np.complex128), (), float(p.y[0]), rs)
-    order = leja_order(residual_poly_roots(p.y))
+    order = leja_order(p.roots if p.roots is not None else residual_poly_roots(p.y))
     units = []
     i = 0
     while i < len(order):

@@ -185,3 +185,68 @@ def test_small_configs_roots(cfg, kw):
     if ref.converged:
         assert res.final_relres < conf["tol"]
     assert abs(res.iterations - ref.iterations) <= 2
+
+
+def _res_norm(A, y, v):
+    """|| v - A p(A) v || / ||v|| in extended precision (oracle yardstick)."""
+    pv = orc.poly_eval_extended(y, A, v)
+    return float(np.linalg.norm(v - A.matvec(pv)) / np.linalg.norm(v))
+
+
+@pytest.mark.parametrize("deg", [4, 8, 10])
+def test_arnoldi_construction_matches_power_basis(golden, deg):
+    """build_poly_arnoldi (harmonic Ritz values of deg+1 Arnoldi steps) finds
+    the same minimum-residual polynomial as the power-basis normal equations
+    (build_poly, polyprec.py:125-147) wherever those are well conditioned:
+    same residual norm, same roots, same coefficients to the conditioning."""
+    h = _lap64(golden)
+    v0 = orc.sm64_uniform(1, h.nrows)
+    c = pg.CostCounters()
+    op = pg.DeviceMatrixOperator(h, c)
+    pa = pg.build_poly_arnoldi(op, v0, deg, c)
+    assert pa.degree == deg and len(pa.roots) == deg + 1 and c.spmvs == deg + 1
+    pp = pg.build_poly(op, v0, deg, pg.CostCounters())
+    O = orc.OracleMatrix.of(h)
+    v = v0 / np.linalg.norm(v0)
+    ra, rp = _res_norm(O, pa.y, v), _res_norm(O, pp.y, v)
+    # the harmonic-Ritz minimiser is never worse; the power basis loses a
+    # little to its conditioning at the top usable degree (2e-4 at deg 10)
+    assert ra <= rp * (1 + 1e-6) and rp <= ra * (1 + 1e-3)
+    rr = np.sort_complex(pg.residual_poly_roots(pp.y))
+    assert np.allclose(np.sort_complex(pa.roots), rr, rtol=1e-4 if deg < 10 else 1e-2)
+    if deg <= 8:
+        np.testing.assert_allclose(pa.y, pp.y, rtol=1e-5 * 10 ** (deg / 2))
+    op.close()
+
+
+def test_arnoldi_high_degree_solves():
+    """Degrees the power basis cannot build (cfg2 operator: Cholesky fails
+    near 13): the harmonic-Ritz polynomial of degree 25 and 40, evaluated in
+    root-product form, keeps decreasing the residual polynomial's norm and
+    cuts GMRES iterations; the solves converge to tol."""
+    conf = wl.CONFIGS[2]
+    h = wl.make_matrix(conf, grid=24)
+    b = wl.make_rhs(conf, h)
+    v0 = wl.make_v0(h.nrows)
+    O = orc.OracleMatrix.of(h)
+    v = v0 / np.linalg.norm(v0)
+    its, res = [], []
+    for deg in (10, 25, 40):
+        c = pg.CostCounters()
+        op = pg.DeviceMatrixOperator(h, c)
+        p = pg.build_poly_arnoldi(op, v0, deg, c)
+        assert p.degree == deg
+        # || v - A p(A) v || evaluated on the device in root form
+        z = pg.PolynomialWrappedOperator(op, p)
+        out = pg.apply_poly(p, op, v, pg.CostCounters(), form="roots")
+        res.append(float(np.linalg.norm(v - O.matvec(out))))
+        r = pg.solve(op, b, right_prec=p, config=pg.GmresConfig(conf["m"], conf["tol"],
+                                                                   poly_form="roots"))
+        assert r.converged and r.final_relres < conf["tol"]
+        tr = np.linalg.norm(b - O.matvec(r.x)) / np.linalg.norm(b)
+        assert tr == pytest.approx(r.final_relres, rel=1e-3)
+        its.append(r.iterations)
+        op.close()
+        del z
+    assert res[0] > res[1] > res[2]
+    assert its[0] > its[1] >= its[2]
