@@ -26,6 +26,10 @@ def main():
     ap.add_argument("--max-iters", type=int, default=3000)
     ap.add_argument("--degrees", default="1,4,8,16,32,64")
     ap.add_argument("--out", default=None)
+    # policy: the reference construction (power basis, auto-degree fallback);
+    # arnoldi: harmonic Ritz values at the requested degree (capped at 62),
+    # evaluated in root-product form
+    ap.add_argument("--construction", default="policy", choices=["policy", "arnoldi"])
     args = ap.parse_args()
     conf = wl.CONFIGS[5]
     A = wl.make_matrix(conf, grid=args.grid)
@@ -42,12 +46,18 @@ def main():
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            p, piv = pg.build_poly_or_auto(op, v0, d, c)
-            res = pg.solve(op, b, right_prec=p, config=pg.GmresConfig(conf["m"], conf["tol"],
-                                                                     args.max_iters))
+            if args.construction == "arnoldi":
+                p, piv = pg.build_poly_arnoldi(op, v0, min(d, 62), c), None
+                form = "roots"
+            else:
+                p, piv = pg.build_poly_or_auto(op, v0, d, c)
+                form = "monomial"
+            res = pg.solve(op, b, right_prec=p, config=pg.GmresConfig(
+                conf["m"], conf["tol"], args.max_iters, poly_form=form))
             e1.record()
             torch.cuda.synchronize()
-        rec = dict(degree_requested=d, degree_effective=p.degree, failed_pivot=piv,
+        rec = dict(construction=args.construction, degree_requested=d,
+                   degree_effective=p.degree, failed_pivot=piv,
                    iterations=res.iterations, cycles=res.cycles, converged=res.converged,
                    final_relres=res.final_relres, spmvs=c.spmvs, dots=c.dots,
                    global_reductions=c.dots + res.cycles, time_s=e0.elapsed_time(e1) / 1e3)
@@ -55,7 +65,8 @@ def main():
         rows.append(rec)
     if args.out:
         with open(args.out, "w") as fh:
-            json.dump(dict(config=conf["name"], n=A.nrows, nnz=A.nnz, rows=rows), fh, indent=1)
+            json.dump(dict(config=conf["name"], n=A.nrows, nnz=A.nnz, construction=args.construction,
+                           rows=rows), fh, indent=1)
 
 
 if __name__ == "__main__":
