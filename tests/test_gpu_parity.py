@@ -482,3 +482,29 @@ def test_native_step_path_is_bitwise_the_kernel_by_kernel_path(golden, monkeypat
         op.close()
     assert np.array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1] and out[0][2] == out[1][2] and out[0][3] == out[1][3] > 1
+
+
+@pytest.mark.parametrize("grid", [3, 5, 7, 9, 13])
+@pytest.mark.parametrize("env", [{}, {"PG_SPMV_WIN_MIN_ROW": "0"}])
+def test_stencil_kernels_ragged_sizes(grid, env, monkeypatch):
+    """Windowed / short-row pair kernels at sizes that leave partial 32-row
+    slices and partial 256-row blocks (n = g^3 for the 27-point operator, g^3
+    for the 7-point one, forced through the windowed kernel with
+    PG_SPMV_WIN_MIN_ROW=0): SpMV, the fused pass chain and the residual stay
+    bit-identical."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for h in (wl.aniso27(grid), wl.convdiff3d_7pt(max(grid, 2))):
+        O = _oracle(h)
+        x = wl.splitmix_uniform(grid, h.nrows)
+        op = pg.DeviceMatrixOperator(h)
+        assert np.array_equal(op.apply(x), O.matvec(x))
+        y = np.random.default_rng(grid).uniform(-1, 1, 4)
+        got = pg.apply_poly(pg.PolyCoefficients(3, y, 1.0), op, x, pg.CostCounters())
+        assert np.array_equal(got, orc.poly_eval(y, O, x, orc.Tally()))
+        e = op.engine
+        rs = e.vecs()
+        b = wl.splitmix_uniform(grid + 1, h.nrows)
+        e.residual(e.ingest(x), e.ingest(b), rs)
+        assert np.array_equal(e.to_host(rs), b - O.matvec(x))
+        op.close()
