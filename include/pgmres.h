@@ -189,6 +189,18 @@ PG_API int pg_arnoldi_step(const pg_matrix* mat, const double* y, int d, double*
                            double* d_w1, double* d_ring, double* h_ring, pg_workspace* ws,
                            pg_event* ev_done, pg_event* ev_chain0, pg_event* ev_chain1,
                            void* stream);
+/* The same step recorded once as a CUDA graph (launched later with
+ * pg_graph_launch on any stream): for solves repeated with the same operator,
+ * polynomial and buffers.  The coefficients and pointers are baked in; the
+ * recorded launches carry plain edges (no programmatic serialization). */
+typedef struct pg_graph pg_graph;
+PG_API int pg_step_graph_create(const pg_matrix* mat, const double* y, int d, double* d_V,
+                                int64_t ld, int j, double* d_z, double* d_t, double* d_acc,
+                                double* d_w0, double* d_w1, double* d_ring, double* h_ring,
+                                pg_workspace* ws, pg_event* ev_done, pg_event* ev_chain0,
+                                pg_event* ev_chain1, pg_graph** out);
+PG_API int pg_graph_launch(pg_graph* graph, void* stream);
+PG_API int pg_graph_destroy(pg_graph* graph);
 
 /* r = b - A x and the partial sum of r^2 into d_nsq[0] (gmres.py:334-335). */
 PG_API int pg_residual(const pg_matrix* mat, const double* d_x, const double* d_b,

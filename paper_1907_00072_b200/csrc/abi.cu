@@ -21,6 +21,8 @@ static thread_local std::string g_last_error;
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
+thread_local bool g_capturing = false;
+
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) {

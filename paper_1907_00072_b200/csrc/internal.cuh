@@ -194,6 +194,8 @@ __device__ __forceinline__ void pdl_entry() {
 }
 
 bool pdl_enabled();
+// true while this thread records launches into a CUDA graph
+extern thread_local bool g_capturing;
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -207,7 +209,9 @@ inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  // launches recorded into a CUDA graph (pg_step_graph_create) get plain
+  // edges: programmatic edges measured slower inside a graph
+  cfg.numAttrs = (pdl_enabled() && !g_capturing) ? 1 : 0;
   PG_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
 }
 

@@ -46,7 +46,13 @@ void poly_chain(const pg_matrix* m, const double* y, int d, const double* x, con
 }
 
 void record(pg_event* e, void* st) {
-  if (e) PG_CUDA(cudaEventRecord(e->ev, pg::as_stream(st)));
+  if (!e) return;
+  // inside a capture only an "external" record becomes a graph node that
+  // re-records the event at every replay
+  if (pg::g_capturing)
+    PG_CUDA(cudaEventRecordWithFlags(e->ev, pg::as_stream(st), cudaEventRecordExternal));
+  else
+    PG_CUDA(cudaEventRecord(e->ev, pg::as_stream(st)));
 }
 
 }  // namespace
@@ -114,12 +120,15 @@ PG_API int pg_poly_chain(const pg_matrix* mat, const double* y, int d, const dou
   });
 }
 
-PG_API int pg_arnoldi_step(const pg_matrix* mat, const double* y, int d, double* d_V, int64_t ld,
-                           int j, double* d_z, double* d_t, double* d_acc, double* d_w0,
-                           double* d_w1, double* d_ring, double* h_ring, pg_workspace* ws,
-                           pg_event* ev_done, pg_event* ev_chain0, pg_event* ev_chain1,
-                           void* stream) {
-  return guard([&] {
+}  // extern "C"
+
+namespace {
+
+void arnoldi_step_body(const pg_matrix* mat, const double* y, int d, double* d_V, int64_t ld,
+                       int j, double* d_z, double* d_t, double* d_acc, double* d_w0,
+                       double* d_w1, double* d_ring, double* h_ring, pg_workspace* ws,
+                       pg_event* ev_done, pg_event* ev_chain0, pg_event* ev_chain1,
+                       void* stream) {
     PG_REQUIRE(mat && d_V && d_z && d_ring && h_ring && ws && ev_done, PG_ERR_PARAMETER,
                "null argument");
     const int k = j + 1;
@@ -149,6 +158,85 @@ PG_API int pg_arnoldi_step(const pg_matrix* mat, const double* y, int d, double*
     PG_CUDA(cudaMemcpyAsync(h_ring, d_ring, sizeof(double) * (2 * PG_KMAX + 1),
                             cudaMemcpyDeviceToHost, as_stream(stream)));
     record(ev_done, stream);
+}
+
+}  // namespace
+
+struct pg_graph {
+  cudaGraphExec_t exec;
+  int device;
+};
+
+extern "C" {
+
+PG_API int pg_arnoldi_step(const pg_matrix* mat, const double* y, int d, double* d_V, int64_t ld,
+                           int j, double* d_z, double* d_t, double* d_acc, double* d_w0,
+                           double* d_w1, double* d_ring, double* h_ring, pg_workspace* ws,
+                           pg_event* ev_done, pg_event* ev_chain0, pg_event* ev_chain1,
+                           void* stream) {
+  return guard([&] {
+    arnoldi_step_body(mat, y, d, d_V, ld, j, d_z, d_t, d_acc, d_w0, d_w1, d_ring, h_ring, ws,
+                      ev_done, ev_chain0, ev_chain1, stream);
+  });
+}
+
+PG_API int pg_step_graph_create(const pg_matrix* mat, const double* y, int d, double* d_V,
+                                int64_t ld, int j, double* d_z, double* d_t, double* d_acc,
+                                double* d_w0, double* d_w1, double* d_ring, double* h_ring,
+                                pg_workspace* ws, pg_event* ev_done, pg_event* ev_chain0,
+                                pg_event* ev_chain1, pg_graph** out) {
+  return guard([&] {
+    PG_REQUIRE(out && mat, PG_ERR_PARAMETER, "null argument");
+    *out = nullptr;
+    int prev = 0;
+    PG_CUDA(cudaGetDevice(&prev));
+    PG_CUDA(cudaSetDevice(mat->device));
+    cudaStream_t cs = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t rc = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (rc == cudaSuccess) rc = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (rc != cudaSuccess) {
+      if (cs) cudaStreamDestroy(cs);
+      cudaSetDevice(prev);
+      throw Error(PG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(rc));
+    }
+    g_capturing = true;
+    try {
+      arnoldi_step_body(mat, y, d, d_V, ld, j, d_z, d_t, d_acc, d_w0, d_w1, d_ring, h_ring, ws,
+                        ev_done, ev_chain0, ev_chain1, cs);
+    } catch (...) {
+      g_capturing = false;
+      cudaStreamEndCapture(cs, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      cudaStreamDestroy(cs);
+      cudaSetDevice(prev);
+      throw;
+    }
+    g_capturing = false;
+    rc = cudaStreamEndCapture(cs, &graph);
+    if (rc == cudaSuccess) rc = cudaGraphInstantiate(&exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    cudaStreamDestroy(cs);
+    cudaSetDevice(prev);
+    if (rc != cudaSuccess)
+      throw Error(PG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(rc));
+    *out = new pg_graph{exec, mat->device};
+  });
+}
+
+PG_API int pg_graph_launch(pg_graph* g, void* stream) {
+  return guard([&] {
+    PG_REQUIRE(g, PG_ERR_PARAMETER, "graph is null");
+    PG_CUDA(cudaGraphLaunch(g->exec, as_stream(stream)));
+  });
+}
+
+PG_API int pg_graph_destroy(pg_graph* g) {
+  return guard([&] {
+    if (!g) return;
+    cudaGraphExecDestroy(g->exec);
+    delete g;
   });
 }
 

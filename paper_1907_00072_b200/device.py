@@ -21,6 +21,7 @@ kernel.  PyTorch provides device memory, streams and the collectives.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -351,8 +352,36 @@ class PgEvent:
 
 
 def _fast_steps_enabled() -> bool:
-    import os
     return os.environ.get("PG_FAST_STEP", "1") != "0"
+
+
+def _step_graphs_enabled() -> bool:
+    return os.environ.get("PG_STEP_GRAPHS", "1") != "0"
+
+
+class _Elapsed:
+    """A chain time already read back (ms), in the (start, end) slot of the
+    bench timer: ``start.elapsed_time(end)`` returns it."""
+
+    def __init__(self, ms: float):
+        self.ms = ms
+
+    def elapsed_time(self, _end=None) -> float:
+        return self.ms
+
+
+class _StepGraph:
+    """One Arnoldi step recorded as a CUDA graph (pg_step_graph_create) with
+    its own chain-timing events."""
+
+    def __init__(self, h, c0, c1):
+        self.h, self.c0, self.c1 = h, c0, c1
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.pg_graph_destroy(h)
+            self.h = None
 
 
 class Engine:
@@ -369,6 +398,11 @@ class Engine:
         self.ilu = None
         self._fast = _fast_steps_enabled()
         self._done_events = None
+        # recorded Arnoldi steps, keyed by everything baked into the graph;
+        # a step is recorded the second time its key is seen (repeated solves)
+        self._graphs_on = _step_graphs_enabled()
+        self._graphs: dict = {}
+        self._graph_seen: set = set()
 
     # ---- construction -------------------------------------------------------
     @classmethod
@@ -481,27 +515,52 @@ class Engine:
     def arnoldi_step(self, Vs, j: int, y, W, slot: int):
         """One native call for Arnoldi step j (fast path of gmres._launch_step):
         z = A p(A) v_j, CGS2 into column j+1, scalars copied to the pinned ring
-        slot behind a library event.  Returns a cgs2_fetch handle."""
+        slot behind a library event.  A step seen before with the same
+        coefficients and buffers is replayed as a recorded CUDA graph.
+        Returns a cgs2_fetch handle."""
         s = self.shards[0]
         if self._done_events is None:
             self._done_events = [PgEvent(s.dev_ord), PgEvent(s.dev_ord)]
         ev = self._done_events[slot]
         if y is None:
-            d, yp = -1, None
+            d, yarr = -1, None
         else:
             yarr = np.ascontiguousarray(y, dtype=np.float64)
-            d, yp = len(yarr) - 1, yarr.ctypes.data
-        c0, c1 = self._chain_events() if d > 0 else (None, None)
+            d = len(yarr) - 1
         host = s.pinned[slot]
-        _lib.call("pg_arnoldi_step", s.mat, yp, d, ptr(Vs[0]), s.ld, j, ptr(W.z[0]),
-                  ptr(W.t[0]), ptr(W.acc[0]), ptr(W.w0[0]), ptr(W.w1[0]), ptr(s.ring[slot]),
-                  host.data_ptr(), s.ws, ev.h, c0.h if c0 else None, c1.h if c1 else None,
-                  s.stream)
+        args = (s.mat, yarr.ctypes.data if yarr is not None else None, d, ptr(Vs[0]), s.ld, j,
+                ptr(W.z[0]), ptr(W.t[0]), ptr(W.acc[0]), ptr(W.w0[0]), ptr(W.w1[0]),
+                ptr(s.ring[slot]), host.data_ptr(), s.ws, ev.h)
         # d passes (a scale for d = 0), wrapper SpMV, 3 CGS2 phases, normalisation
-        _lib.add_launches("pg_arnoldi_step", (max(d, 1) if d >= 0 else 0) + 5)
-        if c0 is not None:
-            self._time_chain(c0, c1, s, d, self._chain_vec_bytes(d, False))
-        return ev, host, j + 1
+        nlaunch = (max(d, 1) if d >= 0 else 0) + 5
+        graph = None
+        if self._graphs_on:
+            key = (j, d, yarr.tobytes() if yarr is not None else b"", args[3], args[6:12], s.ld,
+                   id(s.mat))
+            graph = self._graphs.get(key)
+            if graph is None and key in self._graph_seen:
+                if len(self._graphs) >= 512:  # bounded: drop the recorded set
+                    self._graphs.clear()
+                c0 = PgEvent(s.dev_ord) if d > 0 else None
+                c1 = PgEvent(s.dev_ord) if d > 0 else None
+                h = _lib.C.c_void_p()
+                _lib.call("pg_step_graph_create", *args, c0.h if c0 else None,
+                          c1.h if c1 else None, _lib.C.byref(h))
+                graph = self._graphs[key] = _StepGraph(h, c0, c1)
+            elif graph is None:
+                self._graph_seen.add(key)
+        if graph is not None:
+            _lib.call("pg_graph_launch", graph.h, s.stream)
+            c0, c1 = graph.c0, graph.c1
+        else:
+            c0, c1 = self._chain_events() if d > 0 else (None, None)
+            _lib.call("pg_arnoldi_step", *args, c0.h if c0 else None, c1.h if c1 else None,
+                      s.stream)
+        _lib.add_launches("pg_arnoldi_step", nlaunch)
+        timing = None
+        if c0 is not None and self.timer is not None:
+            timing = (c0, c1, s, d)
+        return ev, host, j + 1, timing
 
     def count_ops(self, counters, k: int):
         """Tally k operator applications (spmvs; prec_applies on ILU engines)."""
@@ -867,10 +926,15 @@ class Engine:
         ev.record(torch.cuda.current_stream(s0.device))
         return ev, host, k
 
-    @staticmethod
-    def cgs2_fetch(handle):
-        ev, host, k = handle
+    def cgs2_fetch(self, handle):
+        ev, host, k = handle[:3]
         ev.synchronize()
+        if len(handle) > 3 and handle[3] is not None and self.timer is not None:
+            # the step's chain time, read now (a recorded step's events are
+            # re-recorded by its next replay)
+            c0, c1, s, d = handle[3]
+            self._time_chain(_Elapsed(c0.elapsed_time(c1)), None, s, d,
+                             self._chain_vec_bytes(d, False))
         h = host.numpy()
         return h[:k].copy(), h[KMAX:KMAX + k].copy(), float(h[2 * KMAX])
 

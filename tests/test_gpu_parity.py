@@ -508,3 +508,23 @@ def test_stencil_kernels_ragged_sizes(grid, env, monkeypatch):
         e.residual(e.ingest(x), e.ingest(b), rs)
         assert np.array_equal(e.to_host(rs), b - O.matvec(x))
         op.close()
+
+
+def test_recorded_step_graphs_replay_bitwise(golden, monkeypatch):
+    """Repeated solves on one operator: the first issues every step, the
+    second records each step as a CUDA graph, later ones replay the graphs.
+    All runs are bit-identical (x, history, counters), and graphs are used."""
+    a, _ = golden
+    c = pg.CostCounters()
+    op = pg.DeviceMatrixOperator(_lap64(golden), c)
+    p = pg.PolyCoefficients(10, a["cfg1_y10"], 1.0)
+    runs = []
+    for _ in range(4):
+        c.__init__()
+        res = pg.solve(op, a["cfg1_b"], right_prec=p, config=pg.GmresConfig(15, 1e-10))
+        runs.append((res.x, res.history, c.as_dict(), res.cycles, res.iterations))
+    assert len(op.engine._graphs) > 0
+    for r in runs[1:]:
+        assert np.array_equal(r[0], runs[0][0])
+        assert r[1:] == runs[0][1:]
+    op.close()
