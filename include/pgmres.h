@@ -174,7 +174,10 @@ PG_API int pg_ilu_apply(pg_ilu* ilu, const double* d_v, double* d_y, double* d_z
  *   w2/|w2| into V[:,j+1], the scalars [c1 (PG_KMAX) | c2 (PG_KMAX) | |w2|^2]
  *   into d_ring and copied to the pinned h_ring, then ev_done recorded.  V is
  *   column-major with leading dimension ld.  Bit-identical to issuing the
- *   same entry points one by one. */
+ *   same entry points one by one.  nroot > 0: z is computed in root-product
+ *   form instead (y, d unused): nroot pg_root_pass passes with modes rmode[q]
+ *   and constants (c1, c2, c3) = rc[3q .. 3q+2], the last one PG_ROOT_RESID
+ *   (RootPlan.resid_steps), with scratch acc (pair temporary), w0, w1. */
 typedef struct pg_event pg_event;
 PG_API int pg_event_create(int device, pg_event** out);
 PG_API int pg_event_destroy(pg_event* ev);
@@ -188,7 +191,7 @@ PG_API int pg_arnoldi_step(const pg_matrix* mat, const double* y, int d, double*
                            int j, double* d_z, double* d_t, double* d_acc, double* d_w0,
                            double* d_w1, double* d_ring, double* h_ring, pg_workspace* ws,
                            pg_event* ev_done, pg_event* ev_chain0, pg_event* ev_chain1,
-                           void* stream);
+                           int nroot, const int* rmode, const double* rc, void* stream);
 /* The same step recorded once as a CUDA graph (launched later with
  * pg_graph_launch on any stream): for solves repeated with the same operator,
  * polynomial and buffers.  The coefficients and pointers are baked in; the
@@ -198,7 +201,8 @@ PG_API int pg_step_graph_create(const pg_matrix* mat, const double* y, int d, do
                                 int64_t ld, int j, double* d_z, double* d_t, double* d_acc,
                                 double* d_w0, double* d_w1, double* d_ring, double* h_ring,
                                 pg_workspace* ws, pg_event* ev_done, pg_event* ev_chain0,
-                                pg_event* ev_chain1, pg_graph** out);
+                                pg_event* ev_chain1, int nroot, const int* rmode,
+                                const double* rc, pg_graph** out);
 PG_API int pg_graph_launch(pg_graph* graph, void* stream);
 PG_API int pg_graph_destroy(pg_graph* graph);
 

@@ -71,9 +71,9 @@ _SIGNATURES = {
     "pg_event_elapsed": ([_p, _p, C.POINTER(C.c_float)], C.c_int),
     "pg_poly_chain": ([_p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p], C.c_int),
     "pg_arnoldi_step": ([_p, _p, _i32, _p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,
-                         _p, _p], C.c_int),
+                         _p, _i32, _p, _p, _p], C.c_int),
     "pg_step_graph_create": ([_p, _p, _i32, _p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p,
-                              _p, _p, C.POINTER(_p)], C.c_int),
+                              _p, _p, _i32, _p, _p, C.POINTER(_p)], C.c_int),
     "pg_graph_launch": ([_p, _p], C.c_int),
     "pg_graph_destroy": ([_p], C.c_int),
     "pg_ilu0_factor": ([_i64, _p, _p, _p, _d, _p, _p, _pi64, C.POINTER(C.c_int)], C.c_int),

@@ -124,11 +124,35 @@ PG_API int pg_poly_chain(const pg_matrix* mat, const double* y, int d, const dou
 
 namespace {
 
+// z = A p(A) v = v - pi(A) v in root-product form (Engine.wrapped_roots):
+// the plan's passes carry only the product; PAIR_A writes the pair
+// temporary t, REAL / PAIR_B the next product (ping-pong w0 / w1), the
+// PG_ROOT_RESID pass writes z.
+void roots_chain(const pg_matrix* m, int nroot, const int* rmode, const double* rc,
+                 const double* v, double* z, double* t, double* w0, double* w1, void* st) {
+  const double* prod = v;
+  double* bufs[2] = {w0, w1};
+  int nb = 0;
+  for (int q = 0; q < nroot; ++q) {
+    const int mode = rmode[q], kind = mode & 3;
+    const bool resid = (mode & PG_ROOT_RESID) != 0;
+    const double* x = kind == PG_ROOT_PAIR_B ? t : prod;
+    const double* p = kind == PG_ROOT_PAIR_B ? prod : nullptr;
+    double* w = resid ? z : (kind == PG_ROOT_PAIR_A ? t : bufs[nb]);
+    ok(pg_root_pass(m, x, p, resid ? v : nullptr, nullptr, w, rc[3 * q], rc[3 * q + 1],
+                    rc[3 * q + 2], mode, st));
+    if (!resid && kind != PG_ROOT_PAIR_A) {
+      prod = w;
+      nb ^= 1;
+    }
+  }
+}
+
 void arnoldi_step_body(const pg_matrix* mat, const double* y, int d, double* d_V, int64_t ld,
                        int j, double* d_z, double* d_t, double* d_acc, double* d_w0,
                        double* d_w1, double* d_ring, double* h_ring, pg_workspace* ws,
                        pg_event* ev_done, pg_event* ev_chain0, pg_event* ev_chain1,
-                       void* stream) {
+                       int nroot, const int* rmode, const double* rc, void* stream) {
     PG_REQUIRE(mat && d_V && d_z && d_ring && h_ring && ws && ev_done, PG_ERR_PARAMETER,
                "null argument");
     const int k = j + 1;
@@ -137,7 +161,13 @@ void arnoldi_step_body(const pg_matrix* mat, const double* y, int d, double* d_V
     const int64_t n = mat->nrows;
     const double* vj = d_V + (int64_t)j * ld;
     // z = A p(A) v_j  (gmres.py:112-113, 283), or z = A v_j without a polynomial
-    if (d >= 0) {
+    if (nroot > 0) {
+      PG_REQUIRE(rmode && rc && d_acc && d_w0 && d_w1, PG_ERR_PARAMETER,
+                 "root plan needs its scratch vectors");
+      record(ev_chain0, stream);
+      roots_chain(mat, nroot, rmode, rc, vj, d_z, d_acc, d_w0, d_w1, stream);
+      record(ev_chain1, stream);
+    } else if (d >= 0) {
       PG_REQUIRE(y && d_t, PG_ERR_PARAMETER, "polynomial step needs y and t");
       record(ev_chain0, stream);
       poly_chain(mat, y, d, vj, nullptr, d_t, d_acc, d_w0, d_w1, stream);
@@ -173,10 +203,10 @@ PG_API int pg_arnoldi_step(const pg_matrix* mat, const double* y, int d, double*
                            int j, double* d_z, double* d_t, double* d_acc, double* d_w0,
                            double* d_w1, double* d_ring, double* h_ring, pg_workspace* ws,
                            pg_event* ev_done, pg_event* ev_chain0, pg_event* ev_chain1,
-                           void* stream) {
+                           int nroot, const int* rmode, const double* rc, void* stream) {
   return guard([&] {
     arnoldi_step_body(mat, y, d, d_V, ld, j, d_z, d_t, d_acc, d_w0, d_w1, d_ring, h_ring, ws,
-                      ev_done, ev_chain0, ev_chain1, stream);
+                      ev_done, ev_chain0, ev_chain1, nroot, rmode, rc, stream);
   });
 }
 
@@ -184,7 +214,8 @@ PG_API int pg_step_graph_create(const pg_matrix* mat, const double* y, int d, do
                                 int64_t ld, int j, double* d_z, double* d_t, double* d_acc,
                                 double* d_w0, double* d_w1, double* d_ring, double* h_ring,
                                 pg_workspace* ws, pg_event* ev_done, pg_event* ev_chain0,
-                                pg_event* ev_chain1, pg_graph** out) {
+                                pg_event* ev_chain1, int nroot, const int* rmode,
+                                const double* rc, pg_graph** out) {
   return guard([&] {
     PG_REQUIRE(out && mat, PG_ERR_PARAMETER, "null argument");
     *out = nullptr;
@@ -194,17 +225,17 @@ PG_API int pg_step_graph_create(const pg_matrix* mat, const double* y, int d, do
     cudaStream_t cs = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
-    cudaError_t rc = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
-    if (rc == cudaSuccess) rc = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
-    if (rc != cudaSuccess) {
+    cudaError_t err = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (err == cudaSuccess) err = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (err != cudaSuccess) {
       if (cs) cudaStreamDestroy(cs);
       cudaSetDevice(prev);
-      throw Error(PG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(rc));
+      throw Error(PG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(err));
     }
     g_capturing = true;
     try {
       arnoldi_step_body(mat, y, d, d_V, ld, j, d_z, d_t, d_acc, d_w0, d_w1, d_ring, h_ring, ws,
-                        ev_done, ev_chain0, ev_chain1, cs);
+                        ev_done, ev_chain0, ev_chain1, nroot, rmode, rc, cs);
     } catch (...) {
       g_capturing = false;
       cudaStreamEndCapture(cs, &graph);
@@ -214,13 +245,13 @@ PG_API int pg_step_graph_create(const pg_matrix* mat, const double* y, int d, do
       throw;
     }
     g_capturing = false;
-    rc = cudaStreamEndCapture(cs, &graph);
-    if (rc == cudaSuccess) rc = cudaGraphInstantiate(&exec, graph, 0);
+    err = cudaStreamEndCapture(cs, &graph);
+    if (err == cudaSuccess) err = cudaGraphInstantiate(&exec, graph, 0);
     if (graph) cudaGraphDestroy(graph);
     cudaStreamDestroy(cs);
     cudaSetDevice(prev);
-    if (rc != cudaSuccess)
-      throw Error(PG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(rc));
+    if (err != cudaSuccess)
+      throw Error(PG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(err));
     *out = new pg_graph{exec, mat->device};
   });
 }

@@ -512,7 +512,7 @@ class Engine:
     def _chain_vec_bytes(d, base):
         return [8 * (int(k > 1) + 1 + int(k < d) + int(base and k == d)) for k in range(1, d + 1)]
 
-    def arnoldi_step(self, Vs, j: int, y, W, slot: int):
+    def arnoldi_step(self, Vs, j: int, y, W, slot: int, plan=None):
         """One native call for Arnoldi step j (fast path of gmres._launch_step):
         z = A p(A) v_j, CGS2 into column j+1, scalars copied to the pinned ring
         slot behind a library event.  A step seen before with the same
@@ -522,7 +522,14 @@ class Engine:
         if self._done_events is None:
             self._done_events = [PgEvent(s.dev_ord), PgEvent(s.dev_ord)]
         ev = self._done_events[slot]
-        if y is None:
+        nroot, rmode, rc = 0, None, None
+        if plan is not None:  # root-product chain (RootPlan.resid_steps)
+            d, yarr = -1, None
+            nroot = len(plan.resid_steps)
+            rmode = np.ascontiguousarray([st[0] for st in plan.resid_steps], dtype=np.int32)
+            rc = np.ascontiguousarray([v for st in plan.resid_steps for v in st[1:4]],
+                                      dtype=np.float64)
+        elif y is None:
             d, yarr = -1, None
         else:
             yarr = np.ascontiguousarray(y, dtype=np.float64)
@@ -531,21 +538,26 @@ class Engine:
         args = (s.mat, yarr.ctypes.data if yarr is not None else None, d, ptr(Vs[0]), s.ld, j,
                 ptr(W.z[0]), ptr(W.t[0]), ptr(W.acc[0]), ptr(W.w0[0]), ptr(W.w1[0]),
                 ptr(s.ring[slot]), host.data_ptr(), s.ws, ev.h)
-        # d passes (a scale for d = 0), wrapper SpMV, 3 CGS2 phases, normalisation
-        nlaunch = (max(d, 1) if d >= 0 else 0) + 5
+        tail = (nroot, rmode.ctypes.data if rmode is not None else None,
+                rc.ctypes.data if rc is not None else None)
+        # the chain (d passes + wrapper SpMV, or the nroot root passes), 3 CGS2
+        # phases, normalisation
+        nlaunch = (nroot if nroot else (max(d, 1) + 1 if d >= 0 else 1)) + 4
+        chained = nroot > 0 or d > 0
         graph = None
         if self._graphs_on:
-            key = (j, d, yarr.tobytes() if yarr is not None else b"", args[3], args[6:12], s.ld,
+            key = (j, d, yarr.tobytes() if yarr is not None else b"",
+                   (rmode.tobytes() + rc.tobytes()) if nroot else b"", args[3], args[6:12], s.ld,
                    id(s.mat))
             graph = self._graphs.get(key)
             if graph is None and key in self._graph_seen:
                 if len(self._graphs) >= 512:  # bounded: drop the recorded set
                     self._graphs.clear()
-                c0 = PgEvent(s.dev_ord) if d > 0 else None
-                c1 = PgEvent(s.dev_ord) if d > 0 else None
+                c0 = PgEvent(s.dev_ord) if chained else None
+                c1 = PgEvent(s.dev_ord) if chained else None
                 h = _lib.C.c_void_p()
                 _lib.call("pg_step_graph_create", *args, c0.h if c0 else None,
-                          c1.h if c1 else None, _lib.C.byref(h))
+                          c1.h if c1 else None, *tail, _lib.C.byref(h))
                 graph = self._graphs[key] = _StepGraph(h, c0, c1)
             elif graph is None:
                 self._graph_seen.add(key)
@@ -553,13 +565,18 @@ class Engine:
             _lib.call("pg_graph_launch", graph.h, s.stream)
             c0, c1 = graph.c0, graph.c1
         else:
-            c0, c1 = self._chain_events() if d > 0 else (None, None)
+            c0, c1 = self._chain_events() if chained else (None, None)
             _lib.call("pg_arnoldi_step", *args, c0.h if c0 else None, c1.h if c1 else None,
-                      s.stream)
+                      *tail, s.stream)
         _lib.add_launches("pg_arnoldi_step", nlaunch)
         timing = None
         if c0 is not None and self.timer is not None:
-            timing = (c0, c1, s, d)
+            if nroot:  # root passes: w write, [p read], [v read] (as wrapped_roots)
+                vec = [8 * (1 + int((m & 3) == _lib.PG_ROOT_PAIR_B) +
+                            int(bool(m & _lib.PG_ROOT_RESID))) for m in rmode]
+                timing = (c0, c1, s, nroot, vec)
+            else:
+                timing = (c0, c1, s, d, self._chain_vec_bytes(d, False))
         return ev, host, j + 1, timing
 
     def count_ops(self, counters, k: int):
@@ -932,9 +949,8 @@ class Engine:
         if len(handle) > 3 and handle[3] is not None and self.timer is not None:
             # the step's chain time, read now (a recorded step's events are
             # re-recorded by its next replay)
-            c0, c1, s, d = handle[3]
-            self._time_chain(_Elapsed(c0.elapsed_time(c1)), None, s, d,
-                             self._chain_vec_bytes(d, False))
+            c0, c1, s, d, vec = handle[3]
+            self._time_chain(_Elapsed(c0.elapsed_time(c1)), None, s, d, vec)
         h = host.numpy()
         return h[:k].copy(), h[KMAX:KMAX + k].copy(), float(h[2 * KMAX])
 

@@ -340,8 +340,9 @@ def _launch_step(e, W, poly, j, plan=None):
     the wrapper SpMV, gmres.py:112-113, 283 -- or, in root form, d+1 passes
     ending in v - pi(A) v) and its CGS2 against v_0..v_j writing v_{j+1}
     (ortho.py:53-70).  Returns the scalar handle."""
-    if plan is None and e.fast_steps:  # one native call for the whole step
-        return e.arnoldi_step(W.V, j, poly.y if poly is not None else None, W, j & 1)
+    if e.fast_steps and (plan is None or plan.resid_steps):  # one native call per step
+        return e.arnoldi_step(W.V, j, poly.y if (poly is not None and plan is None) else None,
+                              W, j & 1, plan)
     vj = W.col(j)
     if plan is not None:
         e.wrapped_roots(plan, vj, W.z, W.acc, W.w0, W.w1)

@@ -250,3 +250,25 @@ def test_arnoldi_high_degree_solves():
         del z
     assert res[0] > res[1] > res[2]
     assert its[0] > its[1] >= its[2]
+
+
+def test_roots_solve_native_and_graph_paths_bitwise(golden, monkeypatch):
+    """The root-form Arnoldi chain inside pg_arnoldi_step (and its recorded
+    graphs on repeated solves) is bit-identical to the per-pass path."""
+    a, _ = golden
+    p = pg.PolyCoefficients(10, a["cfg1_y10"], 1.0)
+    outs = []
+    for fast in ("0", "1"):
+        monkeypatch.setenv("PG_FAST_STEP", fast)
+        c = pg.CostCounters()
+        op = pg.DeviceMatrixOperator(_lap64(golden), c)
+        for _ in range(3):  # 3rd run replays recorded graphs on the fast path
+            c.__init__()
+            r = pg.solve(op, a["cfg1_b"], right_prec=p,
+                         config=pg.GmresConfig(15, 1e-10, poly_form="roots"))
+            outs.append((r.x, r.history, c.as_dict()))
+        if fast == "1":
+            assert len(op.engine._graphs) > 0
+        op.close()
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0]) and o[1:] == outs[0][1:]

@@ -40,7 +40,7 @@ def main():
         t2 = time.perf_counter()
         return t1 - t0, t2 - t1, r
 
-    for _ in range(3):
+    for _ in range(4):  # the second solve records the step graphs
         one()
     pr = cProfile.Profile()
     pr.enable()
@@ -49,6 +49,7 @@ def main():
     print(f"build {tb*1e3:.2f} ms  solve {ts*1e3:.2f} ms  iters {r.iterations}")
     st = pstats.Stats(pr)
     st.sort_stats("tottime").print_stats(25)
+    st.sort_stats("cumulative").print_stats(40)
 
 
 if __name__ == "__main__":
