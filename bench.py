@@ -291,7 +291,7 @@ def run_ours(args):
     b_pin = torch.from_numpy(b_host).pin_memory()
     v0_pin = torch.from_numpy(v0_host).pin_memory()
     e2e_times = []
-    for i in range(max(1, min(args.steps, 3)) + 1):
+    for i in range(max(1, min(args.steps, 10)) + 1):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -369,6 +369,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": 16 * N,
                     "d2h_bytes_per_step": 8 * N,
+                    "median": float(np.median(e2e_times)),
+                    "all_ms": [round(1e3 * t, 3) for t in e2e_times],
                     "note": "public API (build_poly_or_auto + solve) from pinned host b/v0, x to host"},
             "gpu_launches": launches,
             "clocks": clocks,
@@ -388,13 +390,14 @@ BENCH_MAX_ITERS = {3: 300, 5: 2000}
 # pg_matrix_stats()[11]: the SELL kernel pg_spmv / pg_poly_pass run (spmv.cu)
 KERNEL_NAMES = {0: "sell_kernel<kPoly,0,0>", 1: "sell_kernel<kPoly,1,1>",
                 2: "sell_pair_kernel<kPoly>", 3: "sell_win_kernel<kPoly>",
-                4: "sell_pair_short_kernel<kPoly>"}
+                4: "sell_pair_short_kernel<kPoly>", 5: "sell_pat_kernel<kPoly>"}
 MATRIX_FORMATS = {
     0: "SELL-C-sigma (int32 column + f64 value, 12 B/entry)",
     1: "dictionary SELL (1 B offset + 1 B value index)",
     2: "pair-dictionary SELL (1 B (offset, value) index), global x gathers",
     3: "pair-dictionary SELL (1 B/entry), x windows staged by a TMA ring",
     4: "pair-dictionary SELL (1 B/entry), rows <= 8 entries, one gather round trip",
+    5: "row-pattern dictionary (1 B per row names its (offset, value) sequence; table in smem)",
 }
 
 

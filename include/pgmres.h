@@ -177,8 +177,23 @@ PG_API int pg_ilu_apply(pg_ilu* ilu, const double* d_v, double* d_y, double* d_z
  *   same entry points one by one.  nroot > 0: z is computed in root-product
  *   form instead (y, d unused): nroot pg_root_pass passes with modes rmode[q]
  *   and constants (c1, c2, c3) = rc[3q .. 3q+2], the last one PG_ROOT_RESID
- *   (RootPlan.resid_steps), with scratch acc (pair temporary), w0, w1. */
+ *   (RootPlan.resid_steps), with scratch acc (pair temporary), w0, w1.
+ *   On matrices pg_chain_fused reports, the step's d+1 passes (or nroot root
+ *   passes) run as ONE dependency-driven kernel (temporal blocking across the
+ *   passes): bit-identical results, and ev_chain1 is then
+ *   recorded after the wrapper SpMV instead of before it.
+ * pg_chain_fused: *fused = 1 when pg_arnoldi_step runs its passes as one
+ *   kernel on this matrix (natural-order square short-row pair format,
+ *   narrow dependency pattern, PG_CHAIN != 0). */
 typedef struct pg_event pg_event;
+PG_API int pg_chain_fused(const pg_matrix* mat, int* fused);
+/* pg_wrapped_apply: z = A p(A) x, t = p(A) x (PolynomialWrappedOperator.apply,
+ * gmres.py:98-113) for d >= 1: the d monomial passes + the wrapper SpMV, as
+ * one chain kernel when pg_chain_fused, else pass by pass; acc, w0, w1 are
+ * scratch n-vectors.  Bit-identical either way. */
+PG_API int pg_wrapped_apply(const pg_matrix* mat, const double* y, int d, const double* d_x,
+                            double* d_t, double* d_z, double* d_acc, double* d_w0, double* d_w1,
+                            pg_workspace* ws, void* stream);
 PG_API int pg_event_create(int device, pg_event** out);
 PG_API int pg_event_destroy(pg_event* ev);
 PG_API int pg_event_record(pg_event* ev, void* stream);

@@ -15,7 +15,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libpgmres.so")
 BUILD = os.path.join(ROOT, "build", "pgmres")
 
-SOURCES = ["abi.cu", "spmv.cu", "ortho.cu", "host.cu", "ilu.cu", "step.cu"]
+SOURCES = ["abi.cu", "spmv.cu", "ortho.cu", "host.cu", "ilu.cu", "step.cu", "chain.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -41,7 +41,7 @@ def _stale(target, deps):
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
     headers = [os.path.join(INCLUDE, "pgmres.h"), os.path.join(CSRC, "internal.cuh"),
-               os.path.join(CSRC, "pipeline.cuh")]
+               os.path.join(CSRC, "pipeline.cuh"), os.path.join(CSRC, "sell.cuh")]
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     if not force and not _stale(LIB, srcs + headers + [__file__]):
         return LIB

@@ -11,6 +11,7 @@
 #include <unordered_map>
 #include <cstring>
 #include <numeric>
+#include <string>
 #include <vector>
 
 #include "internal.cuh"
@@ -161,6 +162,9 @@ static void free_matrix(pg_matrix* m) {
   cudaFree(m->wtab);
   cudaFree(m->pair8);
   cudaFree(m->ptab);
+  cudaFree(m->rpat);
+  cudaFree(m->pat_ptr);
+  cudaFree(m->pat_ent);
   cudaSetDevice(cur);
   delete m;
 }
@@ -253,6 +257,60 @@ static std::vector<int32_t> build_window_plan(const std::vector<int64_t>& offs,
   return wtab;
 }
 
+// Row-pattern dictionary.  On a constant-coefficient stencil a row is one of
+// a few dozen sequences of (column offset, value) pairs -- 27 for a 3-D 7- or
+// 27-point operator (low / interior / high boundary in each dimension) -- so
+// one byte per row names the whole row: no per-entry stream and no row
+// length.  The table keeps each pattern's pairs in the row's stored order,
+// so the row sum is still the reference's sequential one.  Built from the
+// pair stream; none when there are more than 256 patterns, a pattern longer
+// than kPatMaxLen or more than kPatMaxEnt table entries.  PG_SPMV_PAT=0
+// disables it.
+static void build_patterns(const SellHost& h, const std::vector<uint8_t>& p8,
+                           const std::vector<int64_t>& sp8, const std::vector<PairEnt>& ptab,
+                           pg_matrix* m) {
+  const char* env = std::getenv("PG_SPMV_PAT");
+  if (env && std::atoi(env) == 0) return;
+  if (h.max_width > kPatMaxLen) return;
+  const int64_t nl = h.n_slices * PG_SLICE;
+  std::vector<uint8_t> rpat(std::max<int64_t>(nl, 1), 0);
+  std::unordered_map<std::string, int> ids;
+  std::vector<std::string> seqs;
+  std::string key;
+  for (int64_t s = 0; s < h.n_slices; ++s) {
+    for (int t = 0; t < PG_SLICE; ++t) {
+      const int64_t lane = s * PG_SLICE + t;
+      key.clear();
+      const int len = h.perm[lane] < 0 ? 0 : h.row_len[lane];
+      for (int j = 0; j < len; ++j)
+        key.push_back((char)p8[(size_t)sp8[s] + (size_t)(j / 4) * 128 + 4 * t + (j & 3)]);
+      auto it = ids.find(key);
+      if (it == ids.end()) {
+        if (ids.size() == 256) return;
+        it = ids.emplace(key, (int)seqs.size()).first;
+        seqs.push_back(key);
+      }
+      rpat[lane] = (uint8_t)it->second;
+    }
+  }
+  std::vector<int32_t> ptr(seqs.size() + 1, 0);
+  std::vector<PairEnt> ent;
+  int maxlen = 0;
+  for (size_t p = 0; p < seqs.size(); ++p) {
+    for (char c : seqs[p]) ent.push_back(ptab[(uint8_t)c]);
+    ptr[p + 1] = (int32_t)ent.size();
+    maxlen = std::max(maxlen, (int)seqs[p].size());
+  }
+  if ((int)ent.size() > kPatMaxEnt) return;
+  if (ent.empty()) ent.push_back(PairEnt{});
+  m->rpat = upload(rpat.data(), rpat.size(), m->bytes);
+  m->pat_ptr = upload(ptr.data(), ptr.size(), m->bytes);
+  m->pat_ent = upload(ent.data(), ent.size(), m->bytes);
+  m->n_pat = (int)seqs.size();
+  m->pat_nent = (int)ptr.back();
+  m->pat_maxlen = maxlen;
+}
+
 static void build_dictionaries(const SellHost& h, const int32_t* col, const double* val,
                                pg_matrix* m) {
   const char* env = std::getenv("PG_SPMV_DICT");
@@ -293,6 +351,8 @@ static void build_dictionaries(const SellHost& h, const int32_t* col, const doub
       dtab[i] = (int32_t)dtab64[i];
     }
     if (fits) {
+      m->n_doff = (int)dtab64.size();
+      for (size_t i = 0; i < dtab64.size(); ++i) m->doff[i] = (int32_t)dtab64[i];
       m->col8 = upload(c8.data(), P, m->bytes);
       m->dtab = upload(dtab.data(), dtab.size(), m->bytes);
       m->n_dcol = (int)dtab64.size();
@@ -325,6 +385,7 @@ static void build_dictionaries(const SellHost& h, const int32_t* col, const doub
         }
         m->pair8 = upload(p8.data(), P, m->bytes);
         m->ptab = upload(ptab.data(), ptab.size(), m->bytes);
+        build_patterns(h, p8, sp8, ptab, m);
         if (!wtab.empty()) m->wtab = upload(wtab.data(), wtab.size(), m->bytes);
       }
     }
@@ -423,6 +484,15 @@ PG_API int pg_matrix_create(int device, int64_t nrows, int64_t ncols, const int6
     m->n_slices = h.n_slices;
     m->sigma = sigma;
     m->max_width = h.max_width;
+    // band of column offsets (the chain kernel's dependency pattern when the
+    // offsets are not dictionary-compressible)
+    m->dband_lo = m->dband_hi = 0;
+    for (int64_t r = 0; r < nrows; ++r)
+      for (int64_t q = row_ptr[r]; q < row_ptr[r + 1]; ++q) {
+        const int64_t o = col_idx[q] - r;
+        m->dband_lo = std::min(m->dband_lo, o);
+        m->dband_hi = std::max(m->dband_hi, o);
+      }
     try {
       m->slice_ptr = upload(h.slice_ptr.data(), h.slice_ptr.size(), m->bytes);
       m->slice_w = upload(h.slice_w.data(), h.slice_w.size(), m->bytes);
@@ -457,8 +527,9 @@ PG_API int pg_matrix_stats(const pg_matrix* m, int64_t* s) {
     s[8] = m->col8 ? 1 : 4;  // bytes per stored column entry
     s[9] = m->val8 ? 1 : 8;  // bytes per stored value entry
     // the kernel launch_sell picks for 16-byte aligned vectors (spmv.cu)
-    s[11] = m->pair8 ? (m->wtab ? 3 : (m->stride8 > 0 && m->stride8 <= 256) ? 4 : 2)
-                     : (m->col8 || m->val8) ? 1 : 0;
+    s[11] = pattern_kernel(m) ? 5
+            : m->pair8 ? (m->wtab ? 3 : (m->stride8 > 0 && m->stride8 <= 256) ? 4 : 2)
+                       : (m->col8 || m->val8) ? 1 : 0;
     s[10] = m->pair8 ? 1 : (s[8] + s[9]);
   });
 }
@@ -478,6 +549,13 @@ PG_API int pg_workspace_create(int device, pg_workspace** out) {
       throw Error(PG_ERR_ALLOC, "workspace allocation failed");
     }
     PG_CUDA(cudaMemset(w->counter, 0, 64));
+    if (cudaMalloc(&w->chain_ctl, 64) != cudaSuccess) {
+      cudaFree(w->partials);
+      cudaFree(w->counter);
+      delete w;
+      throw Error(PG_ERR_ALLOC, "workspace allocation failed");
+    }
+    PG_CUDA(cudaMemset(w->chain_ctl, 0, 64));
     *out = w;
   });
 }
@@ -488,6 +566,9 @@ PG_API int pg_workspace_destroy(pg_workspace* ws) {
     DeviceScope scope(ws->device);
     cudaFree(ws->partials);
     cudaFree(ws->counter);
+    cudaFree(ws->chain_ctl);
+    cudaFree(ws->chain_flags);
+    for (int i = 0; i < ws->n_retired; ++i) cudaFree(ws->chain_retired[i]);
     delete ws;
   });
 }

@@ -83,6 +83,20 @@ struct pg_matrix {
   int n_wgrp, win_elems;
   int win_b8;          // largest per-block byte span of each packed stream
   int32_t wlo[32], wstart[32], wlen[32];
+  // row-pattern dictionary (abi.cu build_patterns): every row is one of
+  // n_pat <= 256 distinct sequences of (column offset, value) pairs; rpat is
+  // the 1-byte pattern id per SELL lane, pattern p's entries are
+  // pat_ent[pat_ptr[p] .. pat_ptr[p+1]) (PairEnt), in the row's stored order
+  uint8_t* rpat;
+  int32_t* pat_ptr;
+  void* pat_ent;
+  int n_pat, pat_nent, pat_maxlen;
+  // row dependency pattern of the dependency-driven chain kernel (chain.cu):
+  // the n_doff distinct column offsets col - row (n_doff <= 256, from the
+  // dictionary), or n_doff = 0 and the band [dband_lo, dband_hi] of offsets
+  int n_doff;
+  int32_t doff[256];
+  int64_t dband_lo, dband_hi;
   size_t bytes;
 };
 
@@ -114,6 +128,10 @@ constexpr int kWinSmemBudget = 220 * 1024;
 constexpr int kWinMaxStageBytes = kWinSmemBudget / 2 / 128 * 128;
 // Number of per-block partial slots a reduction may use.
 constexpr int kMaxBlocks = 1024;
+// Row-pattern dictionary budget: table entries staged in shared memory per
+// block (16 B each) and the longest pattern a kernel unrolls over.
+constexpr int kPatMaxEnt = 2048;
+constexpr int kPatMaxLen = 32;
 // Per-block partial slots: the Gram stores (hi, lo) for each of the
 // ncols*(ncols+1)/2 pairs, ncols <= PG_KMAX.
 constexpr int kMaxOut = PG_KMAX * (PG_KMAX + 1);
@@ -124,6 +142,15 @@ struct pg_workspace {
   int num_sms;
   double* partials;        // [kMaxBlocks * kMaxOut]
   unsigned int* counter;   // completion counter (self-resetting)
+  // chain kernel state (chain.cu): ctl = {ticket, exited, generation (u64)},
+  // flags[chunk] = (generation << 8) | passes completed on that row chunk.
+  // Grown on demand; retired arrays stay allocated until destroy because a
+  // recorded graph may still reference them.
+  unsigned int* chain_ctl;
+  unsigned long long* chain_flags;
+  int64_t chain_cap;
+  void* chain_retired[32];
+  int n_retired;
 };
 
 namespace pg {
@@ -216,5 +243,29 @@ inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
 }
 
 int grid_for(int device, const void* kernel, int block, size_t smem, int64_t work_blocks);
+
+// One SpMV pass of a chain (chain.cu): x is the gathered vector; the other
+// fields are the pass's epilogue (pg_poly_pass / pg_root_pass / pg_spmv
+// arguments: acc_out doubles as the SpMV output).
+enum { PG_CHAIN_SPMV = 0, PG_CHAIN_POLY = 1, PG_CHAIN_ROOT = 3 };
+struct ChainStep {
+  int mode;
+  const double* x;
+  const double* acc_in;
+  const double* base;
+  double* acc_out;
+  double* w_out;
+  double y0, yk;
+  int flags;
+  double c1, c2, c3;
+};
+// pg_spmv & co. run the row-pattern kernel on this matrix (spmv.cu).
+bool pattern_kernel(const pg_matrix* m);
+// Matrix format the chain kernel handles (and PG_CHAIN != 0).
+bool chain_supported(const pg_matrix* m);
+// Issue the np passes as one dependency-driven kernel on st; false (nothing
+// issued) when the matrix, the workspace or the pass count does not qualify.
+bool chain_launch(const pg_matrix* m, const ChainStep* steps, int np, pg_workspace* ws,
+                  cudaStream_t st);
 
 }  // namespace pg

@@ -29,126 +29,10 @@
 
 #include "internal.cuh"
 #include "pipeline.cuh"
+#include "sell.cuh"
 
 namespace pg {
 
-enum SellMode { kSpmv = 0, kPoly = 1, kResid = 2, kRoot = 3 };
-
-constexpr int kSellThreads = 256;
-// Occupancy floor and row-chunk unroll of the plain kernel, chosen by sweep
-// on B200 (tools/spmv_bench.py over build variants): (4 blocks, unroll 4)
-// gives cfg2 5.40, cfg4 6.19, cfg5 5.26, cfg3 2.41 TB/s; forcing 6+ blocks
-// (<= 40 registers) spills and loses 30-40%.
-#ifndef PG_SELL_MIN_BLOCKS
-#define PG_SELL_MIN_BLOCKS 4
-#endif
-constexpr int kSellMinBlocks = PG_SELL_MIN_BLOCKS;
-#ifndef PG_SELL_UNROLL
-#define PG_SELL_UNROLL 4
-#endif
-constexpr int kUnroll = PG_SELL_UNROLL;
-
-struct SellArgs {
-  const int64_t* __restrict__ slice_ptr;
-  const int32_t* __restrict__ slice_w;
-  const int32_t* __restrict__ row_len;
-  const int32_t* __restrict__ perm;
-  const int32_t* __restrict__ col;
-  const double* __restrict__ val;
-  int64_t nrows;
-  int64_t nlanes;
-  const int64_t* __restrict__ slice_ptr8;  // packed 1-byte stream offsets
-  const uint8_t* __restrict__ col8;  // dictionary-compressed streams (abi.cu)
-  const int32_t* __restrict__ dtab;
-  const uint8_t* __restrict__ val8;
-  const double* __restrict__ vtab;
-  int64_t stride8;  // pg_matrix::stride8
-};
-
-struct Epi {
-  const double* acc_in;
-  const double* base;
-  double* acc_out;
-  double* w_out;
-  const double* b;
-  double y0, yk;
-  int flags;
-  // kRoot (root-product form, PG_ROOT_*): acc_in = y_in, acc_out = y_out,
-  // w_out = v_out, base = p_in; c1 = 1/|theta|^2 or 1/theta, c2 = 2 Re(theta),
-  // c3 = folded trailing real root (0 = none)
-  double c1, c2, c3;
-};
-
-__device__ __forceinline__ int64_t lane_row(const SellArgs& a, int64_t lane) {
-  if (a.perm) return __ldg(a.perm + lane);
-  return lane < a.nrows ? lane : -1;
-}
-
-// Epilogue operands of a row, loaded BEFORE the row's gathers so that their
-// HBM latency overlaps the gather latency.
-struct Pre {
-  double a, b;
-};
-
-template <int MODE>
-__device__ __forceinline__ Pre epi_load(const Epi& e, const double* __restrict__ x, int64_t row) {
-  Pre p{0.0, 0.0};
-  if (row < 0) return p;
-  if (MODE == kPoly) {
-    p.a = (e.flags & PG_PASS_FIRST) ? x[row] : e.acc_in[row];
-    if (e.base) p.b = e.base[row];
-  } else if (MODE == kResid) {
-    p.a = e.b[row];
-  } else if (MODE == kRoot) {
-    p.a = ((e.flags & 3) == PG_ROOT_PAIR_B) ? e.base[row] : x[row];
-    if (e.acc_in) p.b = e.acc_in[row];
-  }
-  return p;
-}
-
-// Row epilogue; returns the residual entry (kResid) for the norm.
-template <int MODE>
-__device__ __forceinline__ double epilogue(const Epi& e, const Pre& p, int64_t row, double ax) {
-  if (MODE == kSpmv) {
-    e.acc_out[row] = ax;
-    return 0.0;
-  } else if (MODE == kPoly) {
-    double t = (e.flags & PG_PASS_FIRST) ? __dmul_rn(e.y0, p.a) : p.a;
-    t = __dadd_rn(t, __dmul_rn(e.yk, ax));
-    if (e.flags & PG_PASS_WRITE_W) e.w_out[row] = ax;
-    if (e.base) t = __dadd_rn(p.b, t);
-    e.acc_out[row] = t;
-    return 0.0;
-  } else if (MODE == kResid) {
-    const double r = __dsub_rn(p.a, ax);
-    e.acc_out[row] = r;
-    return r;
-  } else {
-    // root-product step (Loe-Morgan running sum): p.a = operand / prod row,
-    // p.b = running sum y (or v for the PG_ROOT_RESID final pass)
-    const int mode = e.flags & 3;
-    const bool resid = (e.flags & PG_ROOT_RESID) != 0;
-    if (mode == PG_ROOT_PAIR_A) {
-      const double t2 = __fma_rn(e.c2, p.a, -ax);   // 2 Re(theta) prod - A prod
-      if (e.w_out) e.w_out[row] = t2;
-      if (e.acc_out) e.acc_out[row] = __fma_rn(e.c1, t2, p.b);  // y + t2 / |theta|^2
-    } else {
-      // REAL: prod - A prod / theta;  PAIR_B: prod - A t2 / |theta|^2
-      const double pn = __fma_rn(-e.c1, ax, p.a);
-      if (resid) {
-        e.w_out[row] = __dsub_rn(p.b, pn);          // A p(A) v = v - pi(A) v
-      } else {
-        if (e.w_out) e.w_out[row] = pn;
-        if (e.acc_out) {
-          double y = (mode == PG_ROOT_REAL) ? __fma_rn(e.c1, p.a, p.b) : p.b;
-          if (e.c3 != 0.0) y = __fma_rn(e.c3, pn, y);  // folded trailing real root
-          e.acc_out[row] = y;
-        }
-      }
-    }
-    return 0.0;
-  }
-}
 
 // Sequential row sum over the row's entries.  cp(j) loads the raw column
 // entry j (an int32 column, or a 1-byte dictionary index), dec(raw) turns it
@@ -329,30 +213,6 @@ __device__ __forceinline__ double row_sum_pairs_global(const uint32_t* __restric
   return acc;
 }
 
-// Rows of at most 8 stored entries (7-point stencils): both index words, all
-// table entries and all gathers are issued before the first add, so the row
-// costs one gather round trip instead of one per 4-entry chunk.
-__device__ __forceinline__ double row_sum_pairs_short(const uint32_t* __restrict__ pw, int len,
-                                                      int64_t row,
-                                                      const double* __restrict__ x,
-                                                      const PairEnt* s_ptab) {
-  const uint32_t w0 = __ldcs(pw);
-  const uint32_t w1 = len > 4 ? __ldcs(pw + PG_SLICE) : 0u;
-  const double* xr = x + row;
-  double v[8], xv[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const uint32_t idx = ((u < 4 ? w0 : w1) >> (8 * (u & 3))) & 255u;
-    const int4 raw = reinterpret_cast<const int4*>(s_ptab)[idx];
-    v[u] = __hiloint2double(raw.y, raw.x);
-    xv[u] = (u < len) ? __ldg(xr + raw.w) : 0.0;
-  }
-  double acc = 0.0;
-#pragma unroll
-  for (int u = 0; u < 8; ++u)
-    if (u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
-  return acc;
-}
 
 // Uniform slices of at most 8 entries per row only (7-point stencils): the
 // short-row body alone, so the kernel needs fewer registers than the general
@@ -415,6 +275,77 @@ __global__ void __launch_bounds__(kSellThreads, PG_SELL_DICT_MIN_BLOCKS)
                           : row_sum_pairs_global(pw, len, avail, row, x, s_ptab);
     const double r = epilogue<MODE>(e, pre, row, ax);
     if (MODE == kResid) local = __fma_rn(r, r, local);
+  }
+  finish_resid<MODE>(local, partials, counter, nsq);
+}
+
+// ------------------------------------------------------ row patterns --
+// One byte per row names its whole (offset, value) sequence (abi.cu
+// build_patterns): the matrix stream is n bytes, the table lives in shared
+// memory.  The table is staged before griddepcontrol.wait (it is never
+// written after matrix creation), so the copy overlaps the previous kernel.
+#ifndef PG_PAT_MIN_BLOCKS
+#define PG_PAT_MIN_BLOCKS 4
+#endif
+// RB > 1: patterns of <= 8 entries, RB rows per thread batched
+// (rows_pattern_batch); RB = 1: any pattern length
+template <int MODE, int RB>
+__global__ void __launch_bounds__(kSellThreads, PG_PAT_MIN_BLOCKS)
+    sell_pat_kernel(SellArgs a, const uint8_t* __restrict__ rpat,
+                    const int32_t* __restrict__ pptr, const PairEnt* __restrict__ pent, int npat,
+                    int nent, const double* __restrict__ x, Epi e, double* partials,
+                    unsigned int* counter, double* nsq) {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  extern __shared__ __align__(16) unsigned char smem_pat[];
+  const int32_t* s_ptr = stage_patterns(smem_pat, pptr, pent, npat, nent);
+  const PairEnt* s_ent = reinterpret_cast<const PairEnt*>(smem_pat);
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  __syncthreads();
+  double local = 0.0;
+  if (RB == 1) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t lane = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lane < a.nlanes;
+         lane += stride) {
+      const int64_t row = lane_row(a, lane);
+      if (row < 0) continue;
+      const int pid = __ldg(rpat + lane);
+      const Pre pre = epi_load<MODE>(e, x, row);
+      const double ax = row_sum_pattern<false>(s_ptr[pid], s_ptr[pid + 1], row, x, s_ent);
+      const double r = epilogue<MODE>(e, pre, row, ax);
+      if (MODE == kResid) local = __fma_rn(r, r, local);
+    }
+  } else {
+    // a block takes RB * blockDim consecutive lanes per step; thread t owns
+    // lanes base + t + j * blockDim (coalesced for each j)
+    const int64_t step = (int64_t)RB * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * step; base < a.nlanes;
+         base += (int64_t)gridDim.x * step) {
+      int64_t row[RB];
+      int beg[RB], end[RB];
+      Pre pre[RB];
+#pragma unroll
+      for (int j = 0; j < RB; ++j) {
+        const int64_t lane = base + threadIdx.x + (int64_t)j * blockDim.x;
+        row[j] = lane < a.nlanes ? lane_row(a, lane) : -1;
+        beg[j] = end[j] = 0;
+        if (row[j] >= 0) {
+          const int pid = __ldg(rpat + lane);
+          beg[j] = s_ptr[pid];
+          end[j] = s_ptr[pid + 1];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < RB; ++j) pre[j] = epi_load<MODE>(e, x, row[j]);
+      double ax[RB];
+      rows_pattern_batch<RB>(row, beg, end, x, s_ent, ax,
+                             [](const double* p) { return __ldg(p); });
+#pragma unroll
+      for (int j = 0; j < RB; ++j)
+        if (row[j] >= 0) {
+          const double r = epilogue<MODE>(e, pre[j], row[j], ax[j]);
+          if (MODE == kResid) local = __fma_rn(r, r, local);
+        }
+    }
   }
   finish_resid<MODE>(local, partials, counter, nsq);
 }
@@ -686,6 +617,23 @@ static SellArgs args_of(const pg_matrix* m) {
   return a;
 }
 
+static int env_or(const char* name, int dflt) {
+  const char* s = std::getenv(name);
+  return s ? std::atoi(s) : dflt;
+}
+
+// The row-pattern kernel runs when the matrix has a pattern dictionary and,
+// for matrices with a window plan (long stencil rows), only when
+// PG_SPMV_PAT_WIN=1 (measured against the windowed kernel per matrix).
+bool pattern_kernel(const pg_matrix* m) {
+  static int on = -1, win = -1;
+  if (on < 0) {
+    on = env_or("PG_SPMV_PAT_KERNEL", 1);
+    win = env_or("PG_SPMV_PAT_WIN", 0);
+  }
+  return on && m->rpat && (!m->wtab || win);
+}
+
 template <int MODE>
 static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace* ws,
                         double* nsq, cudaStream_t st) {
@@ -710,7 +658,29 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
   // windowed kernel: long rows (27-point: 1.6x the pair kernel); short rows
   // (7-point) keep the global-gather pair kernel, which is faster there
   const bool win_ok = m->pair8 && m->wtab && aligned;
-  if (win_ok) {
+  if (pattern_kernel(m)) {
+    int64_t blocks = (a.nlanes + kSellThreads - 1) / kSellThreads;
+    static int per_sm = -1;
+    if (per_sm < 0) per_sm = env_or("PG_SPMV_PAT_BLOCKS_PER_SM", PG_PAT_MIN_BLOCKS);
+    const int64_t cap = (MODE == kResid) ? kMaxBlocks : (int64_t)sms[dev] * per_sm;
+    if (blocks > cap) blocks = cap;
+    const size_t smem = pattern_smem_bytes(m->n_pat, m->pat_nent);
+    static int rb = -1;
+    if (rb < 0) rb = env_or("PG_SPMV_PAT_RB", 2);
+    const int r = m->pat_maxlen <= 8 ? rb : 1;
+    auto kern = r >= 4 ? sell_pat_kernel<MODE, 4> : r == 2 ? sell_pat_kernel<MODE, 2>
+                                                           : sell_pat_kernel<MODE, 1>;
+    static bool attr[4][3][64] = {};
+    const int ri = r >= 4 ? 2 : r == 2 ? 1 : 0;
+    if (!attr[MODE][ri][dev]) {
+      PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)pattern_smem_bytes(256, kPatMaxEnt)));
+      attr[MODE][ri][dev] = true;
+    }
+    launch_k(kern, (int)blocks, kSellThreads, smem, st, a, (const uint8_t*)m->rpat,
+             (const int32_t*)m->pat_ptr, (const PairEnt*)m->pat_ent, m->n_pat, m->pat_nent, x,
+             e, part, cnt, nsq);
+  } else if (win_ok) {
     WinArgs wa;
     wa.ng = m->n_wgrp;
     wa.total = m->win_elems;

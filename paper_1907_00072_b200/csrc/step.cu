@@ -8,6 +8,8 @@
 // the same launches in C++ (same kernels, same order, same arguments as the
 // per-kernel entry points: results are bit-identical), one call per step.
 
+#include <vector>
+
 #include "internal.cuh"
 
 struct pg_event {
@@ -43,6 +45,24 @@ void poly_chain(const pg_matrix* m, const double* y, int d, const double* x, con
                     last ? nullptr : nxt, y[0], y[k], flags, st));
     cur = nxt;
   }
+}
+
+// The passes poly_chain issues, as chain steps (same buffers and flags).
+std::vector<pg::ChainStep> poly_steps(const double* y, int d, const double* x, const double* base,
+                                      double* out, double* acc, double* w0, double* w1) {
+  std::vector<pg::ChainStep> v;
+  const double* cur = x;
+  double* ws[2] = {w0, w1};
+  for (int k = 1; k <= d; ++k) {
+    const bool last = k == d;
+    const int flags = (k == 1 ? PG_PASS_FIRST : 0) | (last ? 0 : PG_PASS_WRITE_W);
+    double* nxt = ws[k & 1];
+    v.push_back(pg::ChainStep{pg::PG_CHAIN_POLY, cur, k > 1 ? acc : nullptr, last ? base : nullptr,
+                              last ? out : acc, last ? nullptr : nxt, y[0], y[k], flags, 0.0, 0.0,
+                              0.0});
+    cur = nxt;
+  }
+  return v;
 }
 
 void record(pg_event* e, void* st) {
@@ -108,6 +128,22 @@ PG_API int pg_event_elapsed(pg_event* start, pg_event* end, float* ms) {
   });
 }
 
+PG_API int pg_wrapped_apply(const pg_matrix* mat, const double* y, int d, const double* d_x,
+                            double* d_t, double* d_z, double* d_acc, double* d_w0, double* d_w1,
+                            pg_workspace* ws, void* stream) {
+  return guard([&] {
+    PG_REQUIRE(mat && y && d_x && d_t && d_z && d > 0 && d_acc && d_w0 && d_w1, PG_ERR_PARAMETER,
+               "null argument");
+    std::vector<ChainStep> steps = poly_steps(y, d, d_x, nullptr, d_t, d_acc, d_w0, d_w1);
+    steps.push_back(ChainStep{PG_CHAIN_SPMV, d_t, nullptr, nullptr, d_z, nullptr, 0.0, 0.0, 0,
+                              0.0, 0.0, 0.0});
+    if (!chain_launch(mat, steps.data(), (int)steps.size(), ws, as_stream(stream))) {
+      poly_chain(mat, y, d, d_x, nullptr, d_t, d_acc, d_w0, d_w1, stream);
+      ok(pg_spmv(mat, d_t, d_z, stream));
+    }
+  });
+}
+
 PG_API int pg_poly_chain(const pg_matrix* mat, const double* y, int d, const double* d_x,
                          const double* d_base, double* d_out, double* d_acc, double* d_w0,
                          double* d_w1, pg_event* ev_start, pg_event* ev_end, void* stream) {
@@ -148,6 +184,32 @@ void roots_chain(const pg_matrix* m, int nroot, const int* rmode, const double* 
   }
 }
 
+// The passes roots_chain issues, as chain steps.
+std::vector<ChainStep> roots_steps(int nroot, const int* rmode, const double* rc, const double* v,
+                                   double* z, double* t, double* w0, double* w1) {
+  std::vector<ChainStep> out;
+  const double* prod = v;
+  double* bufs[2] = {w0, w1};
+  int nb = 0;
+  for (int q = 0; q < nroot; ++q) {
+    const int mode = rmode[q], kind = mode & 3;
+    const bool resid = (mode & PG_ROOT_RESID) != 0;
+    PG_REQUIRE((mode & ~(3 | PG_ROOT_RESID)) == 0 && kind <= PG_ROOT_PAIR_B &&
+                   !(resid && kind == PG_ROOT_PAIR_A),
+               PG_ERR_PARAMETER, "unknown root-pass mode");
+    const double* x = kind == PG_ROOT_PAIR_B ? t : prod;
+    const double* p = kind == PG_ROOT_PAIR_B ? prod : nullptr;
+    double* w = resid ? z : (kind == PG_ROOT_PAIR_A ? t : bufs[nb]);
+    out.push_back(ChainStep{PG_CHAIN_ROOT, x, resid ? v : nullptr, p, nullptr, w, 0.0, 0.0, mode,
+                            rc[3 * q], rc[3 * q + 1], rc[3 * q + 2]});
+    if (!resid && kind != PG_ROOT_PAIR_A) {
+      prod = w;
+      nb ^= 1;
+    }
+  }
+  return out;
+}
+
 void arnoldi_step_body(const pg_matrix* mat, const double* y, int d, double* d_V, int64_t ld,
                        int j, double* d_z, double* d_t, double* d_acc, double* d_w0,
                        double* d_w1, double* d_ring, double* h_ring, pg_workspace* ws,
@@ -165,14 +227,26 @@ void arnoldi_step_body(const pg_matrix* mat, const double* y, int d, double* d_V
       PG_REQUIRE(rmode && rc && d_acc && d_w0 && d_w1, PG_ERR_PARAMETER,
                  "root plan needs its scratch vectors");
       record(ev_chain0, stream);
-      roots_chain(mat, nroot, rmode, rc, vj, d_z, d_acc, d_w0, d_w1, stream);
+      std::vector<ChainStep> steps = roots_steps(nroot, rmode, rc, vj, d_z, d_acc, d_w0, d_w1);
+      if (!chain_launch(mat, steps.data(), nroot, ws, as_stream(stream)))
+        roots_chain(mat, nroot, rmode, rc, vj, d_z, d_acc, d_w0, d_w1, stream);
       record(ev_chain1, stream);
     } else if (d >= 0) {
       PG_REQUIRE(y && d_t, PG_ERR_PARAMETER, "polynomial step needs y and t");
       record(ev_chain0, stream);
-      poly_chain(mat, y, d, vj, nullptr, d_t, d_acc, d_w0, d_w1, stream);
-      record(ev_chain1, stream);
-      ok(pg_spmv(mat, d_t, d_z, stream));
+      // the d passes and the wrapper SpMV as one dependency-driven kernel
+      // (chain.cu) when the matrix format allows; ev_chain1 then also covers
+      // the wrapper pass (pg_chain_fused)
+      std::vector<ChainStep> steps = poly_steps(y, d, vj, nullptr, d_t, d_acc, d_w0, d_w1);
+      steps.push_back(ChainStep{PG_CHAIN_SPMV, d_t, nullptr, nullptr, d_z, nullptr, 0.0, 0.0, 0,
+                                0.0, 0.0, 0.0});
+      if (d > 0 && chain_launch(mat, steps.data(), (int)steps.size(), ws, as_stream(stream))) {
+        record(ev_chain1, stream);
+      } else {
+        poly_chain(mat, y, d, vj, nullptr, d_t, d_acc, d_w0, d_w1, stream);
+        record(ev_chain1, stream);
+        ok(pg_spmv(mat, d_t, d_z, stream));
+      }
     } else {
       ok(pg_spmv(mat, vj, d_z, stream));
     }

@@ -151,6 +151,10 @@ class Shard:
                                "val_bytes", "stream_bytes", "kernel"), list(st)))
         # bytes streamed per stored matrix entry (dictionary compression: 1+1)
         self.entry_bytes = int(st[10])
+        # Arnoldi-step passes run as one dependency-driven kernel (chain.cu)
+        fused = _lib.C.c_int(0)
+        _lib.call("pg_chain_fused", h, _lib.C.byref(fused))
+        self.chain_fused = bool(fused.value)
         # small per-shard device scratch: [c1 | c2 | nsq | spare]
         self.scal = torch.zeros(2 * KMAX + 8, dtype=F64, device=device)
         self.coef = torch.zeros(KMAX, dtype=F64, device=device)
@@ -203,6 +207,15 @@ class Shard:
         buf = self.send_buf[q]
         _lib.call("pg_gather", ptr(x), ptr(sel), len(sel), ptr(buf), self.stream)
         return buf
+
+    def pass_bytes(self, vec_bytes: int) -> int:
+        """Algorithmic bytes of one SpMV pass over the stored format: the
+        matrix stream (1 B per row for the row-pattern format; else the
+        stored entry bytes + a 4-byte row length), the compulsory gather of x
+        (8 B per row) and ``vec_bytes`` per row of epilogue vectors."""
+        if self.stats["kernel"] == 5:
+            return (1 + 8 + vec_bytes) * self.n
+        return self.entry_bytes * self.nnz + (12 + vec_bytes) * self.n
 
     def close(self):
         if getattr(self, "mat", None):
@@ -504,7 +517,7 @@ class Engine:
         accounting as Engine.poly)."""
         nbytes = nbytes12 = 0
         for k, vec in enumerate(pass_vec_bytes):
-            nbytes += s.entry_bytes * s.nnz + (12 + vec) * s.n
+            nbytes += s.pass_bytes(vec)
             nbytes12 += 12 * s.nnz + (12 + vec) * s.n
         self.timer.append((ev0, ev1, nbytes, d, nbytes12))
 
@@ -542,7 +555,13 @@ class Engine:
                 rc.ctypes.data if rc is not None else None)
         # the chain (d passes + wrapper SpMV, or the nroot root passes), 3 CGS2
         # phases, normalisation
-        nlaunch = (nroot if nroot else (max(d, 1) + 1 if d >= 0 else 1)) + 4
+        # one dependency-driven kernel for the whole chain on chain_fused
+        # matrices (its timing events then also cover the wrapper SpMV)
+        fused = s.chain_fused and (nroot > 1 or d > 0)
+        if fused:
+            nlaunch = 1 + 4
+        else:
+            nlaunch = (nroot if nroot else (max(d, 1) + 1 if d >= 0 else 1)) + 4
         chained = nroot > 0 or d > 0
         graph = None
         if self._graphs_on:
@@ -575,6 +594,8 @@ class Engine:
                 vec = [8 * (1 + int((m & 3) == _lib.PG_ROOT_PAIR_B) +
                             int(bool(m & _lib.PG_ROOT_RESID))) for m in rmode]
                 timing = (c0, c1, s, nroot, vec)
+            elif fused:  # d passes + the wrapper SpMV (z write)
+                timing = (c0, c1, s, d + 1, self._chain_vec_bytes(d, False) + [8])
             else:
                 timing = (c0, c1, s, d, self._chain_vec_bytes(d, False))
         return ev, host, j + 1, timing
@@ -745,7 +766,7 @@ class Engine:
                     # compression), 4 B row length, 8 B compulsory gather of x,
                     # then the epilogue's vector traffic
                     vec = 8 * (int(k > 1) + 1 + int(not last) + int(b is not None))
-                    nbytes += s.entry_bytes * s.nnz + (12 + vec) * s.n
+                    nbytes += s.pass_bytes(vec)
                     nbytes12 += 12 * s.nnz + (12 + vec) * s.n
             if not last:
                 self.halo(nxt)
@@ -816,7 +837,7 @@ class Engine:
                     # p read (PAIR_B), y read (unless seeded from zero), y/w writes
                     vec = 8 * (int(p is not None) + int(writes_y and yin is not None)
                                + int(writes_y) + int(w is not None))
-                    nbytes += s.entry_bytes * s.nnz + (12 + vec) * s.n
+                    nbytes += s.pass_bytes(vec)
                     nbytes12 += 12 * s.nnz + (12 + vec) * s.n
             if writes_y:
                 first = False
@@ -862,7 +883,7 @@ class Engine:
                           s.stream)
                 if timing:
                     vec = 8 * (1 + int(p is not None) + int(resid))  # w, [p], [v]
-                    nbytes += s.entry_bytes * s.nnz + (12 + vec) * s.n
+                    nbytes += s.pass_bytes(vec)
                     nbytes12 += 12 * s.nnz + (12 + vec) * s.n
             if not resid:
                 self.halo(w)

@@ -485,7 +485,8 @@ def test_native_step_path_is_bitwise_the_kernel_by_kernel_path(golden, monkeypat
 
 
 @pytest.mark.parametrize("grid", [3, 5, 7, 9, 13])
-@pytest.mark.parametrize("env", [{}, {"PG_SPMV_WIN_MIN_ROW": "0"}])
+@pytest.mark.parametrize("env", [{}, {"PG_SPMV_WIN_MIN_ROW": "0"}, {"PG_SPMV_PAT": "0"},
+                                 {"PG_SPMV_PAT": "0", "PG_SPMV_WIN_MIN_ROW": "0"}])
 def test_stencil_kernels_ragged_sizes(grid, env, monkeypatch):
     """Windowed / short-row pair kernels at sizes that leave partial 32-row
     slices and partial 256-row blocks (n = g^3 for the 27-point operator, g^3

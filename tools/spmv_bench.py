@@ -45,8 +45,9 @@ VARIANTS = {
     "dict": {"PG_SPMV_WIN": "0", "PG_SPMV_PAIR": "0"},  # two 1-byte streams
     "plain": {"PG_SPMV_WIN": "0", "PG_SPMV_PAIR": "0", "PG_SPMV_DICT": "0"},  # int32 + f64
     "default": {},
+    "nopat": {"PG_SPMV_PAT": "0"},                 # pair / window kernels (no row patterns)
 }
-ENV_KEYS = ("PG_SPMV_WIN", "PG_SPMV_PAIR", "PG_SPMV_DICT", "PG_SPMV_WIN_MIN_ROW")
+ENV_KEYS = ("PG_SPMV_WIN", "PG_SPMV_PAIR", "PG_SPMV_DICT", "PG_SPMV_WIN_MIN_ROW", "PG_SPMV_PAT")
 
 
 def main():
@@ -71,8 +72,9 @@ def main():
             st = e.shards[0].stats
             dt, gbs = time_pass(e, args.reps)
             eb = st["stream_bytes"]
+            stored = e.shards[0].pass_bytes(24)  # middle pass: acc in/out + w out
             rec = dict(case=name, kernel=var, us=dt * 1e6, gbs_uncompressed_equiv=gbs,
-                       gbs_stored=(eb * A.nnz + 36 * A.nrows) / dt / 1e9,
+                       gbs_stored=stored / dt / 1e9,
                        nnz=A.nnz, n=A.nrows, padded=st["padded_nnz"], entry_bytes=eb,
                        kernel_kind=st["kernel"])
             print(json.dumps(rec), flush=True)
