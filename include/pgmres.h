@@ -89,7 +89,8 @@ PG_API int pg_matrix_destroy(pg_matrix* mat);
  *              (1 = pair dictionary, 2 = two dictionary streams, 12 = plain),
  *              that kernel (0 plain SELL, 1 two-stream dictionary, 2 pair
  *              dictionary with global gathers, 3 windowed pair TMA ring,
- *              4 pair dictionary, short uniform rows)} */
+ *              4 pair dictionary, short uniform rows, 5 row-pattern
+ *              dictionary (1 B per row), 6 windowed row patterns)} */
 PG_API int pg_matrix_stats(const pg_matrix* mat, int64_t* stats);
 
 /* ---- reduction workspace (one per stream) --------------------------------

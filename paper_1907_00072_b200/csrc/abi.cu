@@ -6,6 +6,7 @@
 // device SpMV reproduces spmv()'s per-row sequential sum (sparse.py:164-168).
 
 #include <algorithm>
+#include <iterator>
 #include <cstdint>
 #include <cstdlib>
 #include <unordered_map>
@@ -165,6 +166,7 @@ static void free_matrix(pg_matrix* m) {
   cudaFree(m->rpat);
   cudaFree(m->pat_ptr);
   cudaFree(m->pat_ent);
+  cudaFree(m->pat_mask);
   cudaSetDevice(cur);
   delete m;
 }
@@ -302,7 +304,39 @@ static void build_patterns(const SellHost& h, const std::vector<uint8_t>& p8,
     maxlen = std::max(maxlen, (int)seqs[p].size());
   }
   if ((int)ent.size() > kPatMaxEnt) return;
+  // master pattern: the most frequent one; every pattern that is an ordered
+  // subsequence of it (same pair indices, hence same values) gets its mask
+  std::vector<int64_t> count(seqs.size(), 0);
+  for (int64_t l = 0; l < nl; ++l)
+    if (h.perm[l] >= 0) ++count[rpat[l]];
+  const size_t mp = (size_t)(std::max_element(count.begin(), count.end()) - count.begin());
+  std::vector<uint32_t> mask(seqs.size(), 1u << 31);
+  const std::string& ms = seqs.empty() ? std::string() : seqs[mp];
+  if (!seqs.empty() && ms.size() <= 31) {
+    for (size_t p = 0; p < seqs.size(); ++p) {
+      uint32_t bits = 0;
+      size_t q = 0;
+      for (char c : seqs[p]) {
+        while (q < ms.size() && ms[q] != c) ++q;
+        if (q == ms.size()) {
+          bits = 1u << 31;
+          break;
+        }
+        bits |= 1u << q++;
+      }
+      mask[p] = bits;
+    }
+    m->pat_mlen = (int)ms.size();
+    for (size_t q = 0; q < ms.size(); ++q) {
+      const PairEnt& pe = ptab[(uint8_t)ms[q]];
+      m->pat_mv[q] = pe.v;
+      m->pat_mdoff[q] = pe.doff;
+      m->pat_mwoff[q] = pe.woff;
+    }
+  }
   if (ent.empty()) ent.push_back(PairEnt{});
+  if (mask.empty()) mask.push_back(1u << 31);
+  m->pat_mask = upload(mask.data(), mask.size(), m->bytes);
   m->rpat = upload(rpat.data(), rpat.size(), m->bytes);
   m->pat_ptr = upload(ptr.data(), ptr.size(), m->bytes);
   m->pat_ent = upload(ent.data(), ent.size(), m->bytes);
@@ -528,6 +562,7 @@ PG_API int pg_matrix_stats(const pg_matrix* m, int64_t* s) {
     s[9] = m->val8 ? 1 : 8;  // bytes per stored value entry
     // the kernel launch_sell picks for 16-byte aligned vectors (spmv.cu)
     s[11] = pattern_kernel(m) ? 5
+            : (m->pair8 && m->wtab && m->rpat && winpat_enabled()) ? 6
             : m->pair8 ? (m->wtab ? 3 : (m->stride8 > 0 && m->stride8 <= 256) ? 4 : 2)
                        : (m->col8 || m->val8) ? 1 : 0;
     s[10] = m->pair8 ? 1 : (s[8] + s[9]);

@@ -91,6 +91,14 @@ struct pg_matrix {
   int32_t* pat_ptr;
   void* pat_ent;
   int n_pat, pat_nent, pat_maxlen;
+  // master pattern (the most frequent row, <= 31 entries): pat_mask[p] is
+  // the bit set of master entries pattern p consists of, in order and with
+  // identical values (a boundary row of a constant-coefficient stencil), or
+  // bit 31 set when p is not such a subsequence
+  int pat_mlen;
+  double pat_mv[32];
+  int32_t pat_mdoff[32], pat_mwoff[32];
+  uint32_t* pat_mask;
   // row dependency pattern of the dependency-driven chain kernel (chain.cu):
   // the n_doff distinct column offsets col - row (n_doff <= 256, from the
   // dictionary), or n_doff = 0 and the band [dband_lo, dband_hi] of offsets
@@ -261,6 +269,8 @@ struct ChainStep {
 };
 // pg_spmv & co. run the row-pattern kernel on this matrix (spmv.cu).
 bool pattern_kernel(const pg_matrix* m);
+// pg_spmv & co. on windowed matrices stage row patterns, not pair streams.
+bool winpat_enabled();
 // Matrix format the chain kernel handles (and PG_CHAIN != 0).
 bool chain_supported(const pg_matrix* m);
 // Issue the np passes as one dependency-driven kernel on st; false (nothing

@@ -223,21 +223,68 @@ __device__ __forceinline__ void rows_pattern_batch(const int64_t (&row)[RB], con
   }
 }
 
-// Stage the pattern table in shared memory: entries first (16 B each), then
-// the n_pat + 1 offsets.  Returns the offsets' base.
+// Stage the pattern table in shared memory: entries (16 B each), then the
+// n_pat + 1 offsets, then the n_pat master masks.  Returns the offsets' base.
 __device__ __forceinline__ const int32_t* stage_patterns(unsigned char* smem,
                                                          const int32_t* __restrict__ pptr,
                                                          const PairEnt* __restrict__ pent,
-                                                         int npat, int nent) {
+                                                         int npat, int nent,
+                                                         const uint32_t* __restrict__ pmask =
+                                                             nullptr) {
   PairEnt* s_ent = reinterpret_cast<PairEnt*>(smem);
-  int32_t* s_ptr = reinterpret_cast<int32_t*>(smem + 16 * (size_t)nent);
+  int32_t* s_ptr = reinterpret_cast<int32_t*>(smem + 16 * (size_t)(nent > 0 ? nent : 1));
   for (int i = threadIdx.x; i < nent; i += blockDim.x) s_ent[i] = pent[i];
   for (int i = threadIdx.x; i <= npat; i += blockDim.x) s_ptr[i] = pptr[i];
+  if (pmask)
+    for (int i = threadIdx.x; i < npat; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(s_ptr + npat + 1)[i] = pmask[i];
   return s_ptr;
 }
 
 __host__ __device__ inline size_t pattern_smem_bytes(int npat, int nent) {
-  return 16 * (size_t)(nent > 0 ? nent : 1) + 4 * (size_t)(npat + 1);
+  return 16 * (size_t)(nent > 0 ? nent : 1) + 4 * (size_t)(npat + 1) + 4 * (size_t)npat;
+}
+
+// The master pattern as kernel parameters (pg_matrix::pat_m*): offsets and
+// values become constant-bank operands of fully unrolled code.  lb = the
+// unroll bucket (8 / 16 / 32) >= len; entries len..lb-1 are inert.
+struct PatMaster {
+  int len, lb;
+  double v[32];
+  int32_t doff[32];
+  int32_t woff[32];
+};
+
+// A row that is the master's entries `mask` (in order): the products of all
+// lb entries are formed, only the masked ones are added -- the same
+// additions, in the same order, as the row's own entry list.  WIN: x is the
+// block's shared-memory window (winrow = the row's slot); else global x
+// gathered at row + doff (masked-off entries are not loaded: they may lie
+// outside x).
+template <int LB, bool WIN, bool CG = false>
+__device__ __forceinline__ double row_sum_master(uint32_t mask, const PatMaster& pm,
+                                                 const unsigned char* winrow,
+                                                 const double* __restrict__ xr) {
+  double acc = 0.0;
+#pragma unroll
+  for (int c0 = 0; c0 < LB; c0 += 8) {
+    double xv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (WIN) {
+        xv[q] = *reinterpret_cast<const double*>(winrow + pm.woff[c0 + q]);
+      } else {
+        xv[q] = 0.0;
+        if ((mask >> (c0 + q)) & 1u) xv[q] = CG ? __ldcg(xr + pm.doff[c0 + q]) : __ldg(xr + pm.doff[c0 + q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double p = __dmul_rn(pm.v[c0 + q], xv[q]);
+      if ((mask >> (c0 + q)) & 1u) acc = __dadd_rn(acc, p);
+    }
+  }
+  return acc;
 }
 
 }  // namespace pg

@@ -26,6 +26,7 @@
 //  * sell_kernel<kRoot>: the root-product form of the polynomial (pg_root_pass).
 
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.cuh"
 #include "pipeline.cuh"
@@ -287,65 +288,39 @@ __global__ void __launch_bounds__(kSellThreads, PG_SELL_DICT_MIN_BLOCKS)
 #ifndef PG_PAT_MIN_BLOCKS
 #define PG_PAT_MIN_BLOCKS 4
 #endif
-// RB > 1: patterns of <= 8 entries, RB rows per thread batched
-// (rows_pattern_batch); RB = 1: any pattern length
-template <int MODE, int RB>
+// LB > 0: rows whose pattern is a masked subsequence of the master pattern
+// (pm, pmask) take the unrolled constant-operand path row_sum_master<LB>;
+// the others (and LB = 0) walk their pattern's table entries.
+template <int MODE, int LB>
 __global__ void __launch_bounds__(kSellThreads, PG_PAT_MIN_BLOCKS)
     sell_pat_kernel(SellArgs a, const uint8_t* __restrict__ rpat,
                     const int32_t* __restrict__ pptr, const PairEnt* __restrict__ pent, int npat,
-                    int nent, const double* __restrict__ x, Epi e, double* partials,
+                    int nent, const uint32_t* __restrict__ pmask, const PatMaster pm,
+                    const double* __restrict__ x, Epi e, double* partials,
                     unsigned int* counter, double* nsq) {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   extern __shared__ __align__(16) unsigned char smem_pat[];
-  const int32_t* s_ptr = stage_patterns(smem_pat, pptr, pent, npat, nent);
+  const int32_t* s_ptr = stage_patterns(smem_pat, pptr, pent, npat, nent, pmask);
+  const uint32_t* s_mask = reinterpret_cast<const uint32_t*>(s_ptr + npat + 1);
   const PairEnt* s_ent = reinterpret_cast<const PairEnt*>(smem_pat);
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   __syncthreads();
   double local = 0.0;
-  if (RB == 1) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t lane = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lane < a.nlanes;
-         lane += stride) {
-      const int64_t row = lane_row(a, lane);
-      if (row < 0) continue;
-      const int pid = __ldg(rpat + lane);
-      const Pre pre = epi_load<MODE>(e, x, row);
-      const double ax = row_sum_pattern<false>(s_ptr[pid], s_ptr[pid + 1], row, x, s_ent);
-      const double r = epilogue<MODE>(e, pre, row, ax);
-      if (MODE == kResid) local = __fma_rn(r, r, local);
-    }
-  } else {
-    // a block takes RB * blockDim consecutive lanes per step; thread t owns
-    // lanes base + t + j * blockDim (coalesced for each j)
-    const int64_t step = (int64_t)RB * blockDim.x;
-    for (int64_t base = (int64_t)blockIdx.x * step; base < a.nlanes;
-         base += (int64_t)gridDim.x * step) {
-      int64_t row[RB];
-      int beg[RB], end[RB];
-      Pre pre[RB];
-#pragma unroll
-      for (int j = 0; j < RB; ++j) {
-        const int64_t lane = base + threadIdx.x + (int64_t)j * blockDim.x;
-        row[j] = lane < a.nlanes ? lane_row(a, lane) : -1;
-        beg[j] = end[j] = 0;
-        if (row[j] >= 0) {
-          const int pid = __ldg(rpat + lane);
-          beg[j] = s_ptr[pid];
-          end[j] = s_ptr[pid + 1];
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < RB; ++j) pre[j] = epi_load<MODE>(e, x, row[j]);
-      double ax[RB];
-      rows_pattern_batch<RB>(row, beg, end, x, s_ent, ax,
-                             [](const double* p) { return __ldg(p); });
-#pragma unroll
-      for (int j = 0; j < RB; ++j)
-        if (row[j] >= 0) {
-          const double r = epilogue<MODE>(e, pre[j], row[j], ax[j]);
-          if (MODE == kResid) local = __fma_rn(r, r, local);
-        }
-    }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t lane = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lane < a.nlanes;
+       lane += stride) {
+    const int64_t row = lane_row(a, lane);
+    if (row < 0) continue;
+    const int pid = __ldg(rpat + lane);
+    const Pre pre = epi_load<MODE>(e, x, row);
+    double ax;
+    const uint32_t mask = LB > 0 ? s_mask[pid] : (1u << 31);
+    if (LB > 0 && !(mask >> 31))
+      ax = row_sum_master<(LB > 0 ? LB : 8), false>(mask, pm, nullptr, x + row);
+    else
+      ax = row_sum_pattern<false>(s_ptr[pid], s_ptr[pid + 1], row, x, s_ent);
+    const double r = epilogue<MODE>(e, pre, row, ax);
+    if (MODE == kResid) local = __fma_rn(r, r, local);
   }
   finish_resid<MODE>(local, partials, counter, nsq);
 }
@@ -446,7 +421,10 @@ __device__ __forceinline__ uint32_t stage_f64_tail(double* dst, const double* sr
 }
 
 // Producer side (one thread): queue row block rb into ring stage `buf`.
-template <int MODE>
+// PAT: the matrix stream is the block's row-pattern bytes (pair8 = rpat,
+// one byte per row) instead of the packed pair stream, row lengths and slice
+// widths.
+template <int MODE, bool PAT>
 __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, const Epi& e,
                                           const uint8_t* __restrict__ pair8,
                                           const double* __restrict__ x, int64_t rb,
@@ -459,9 +437,13 @@ __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, 
   const int64_t nr = min((int64_t)kWinRows, a.nrows - r0);
   const double *A, *B;
   epi_vectors<MODE>(e, x, A, B);
+  if (PAT) {  // pattern ids of the block's rows: rpat is padded to whole slices
+    p0 = r0;
+    p1 = r0 + ((nr + 15) & ~(int64_t)15);
+  }
   // pass 1: byte count (+ odd tails), so that expect_tx precedes the copies
   uint32_t bytes = (uint32_t)(p1 - p0);
-  if (kWinStageEpi)  // row lengths + slice widths (bulk unless a partial block)
+  if (kWinStageEpi && !PAT)  // row lengths + slice widths (bulk unless a partial block)
     bytes += 4u * (uint32_t)((s1 - s0) * PG_SLICE) +
              ((s1 - s0) * 4 % 16 == 0 ? 4u * (uint32_t)(s1 - s0) : 0u);
   for (int g = 0; g < wa.ng; ++g) {
@@ -473,7 +455,7 @@ __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, 
   if (kWinStageEpi) {
     if (A) bytes += stage_f64_tail(reinterpret_cast<double*>(buf + wa.off_ea), A + r0, nr);
     if (B) bytes += stage_f64_tail(reinterpret_cast<double*>(buf + wa.off_eb), B + r0, nr);
-    if ((s1 - s0) * 4 % 16 != 0)  // partial last block: slice widths copied plainly
+    if (!PAT && (s1 - s0) * 4 % 16 != 0)  // partial last block: slice widths copied plainly
       for (int64_t q = s0; q < s1; ++q) sw[q - s0] = __ldg(a.slice_w + q);
   }
   mbar_expect_tx(bar, bytes);
@@ -488,8 +470,10 @@ __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, 
   if (kWinStageEpi) {
     if (A && nr > 1) bulk_g2s(buf + wa.off_ea, A + r0, 8u * (uint32_t)(nr & ~(int64_t)1), bar);
     if (B && nr > 1) bulk_g2s(buf + wa.off_eb, B + r0, 8u * (uint32_t)(nr & ~(int64_t)1), bar);
-    bulk_g2s(buf + wa.off_rl, a.row_len + r0, 4u * (uint32_t)((s1 - s0) * PG_SLICE), bar);
-    if ((s1 - s0) * 4 % 16 == 0) bulk_g2s(sw, a.slice_w + s0, 4u * (uint32_t)(s1 - s0), bar);
+    if (!PAT) {
+      bulk_g2s(buf + wa.off_rl, a.row_len + r0, 4u * (uint32_t)((s1 - s0) * PG_SLICE), bar);
+      if ((s1 - s0) * 4 % 16 == 0) bulk_g2s(sw, a.slice_w + s0, 4u * (uint32_t)(s1 - s0), bar);
+    }
   }
 }
 
@@ -500,21 +484,39 @@ __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, 
 // through the `empty` mbarrier.  Global memory is only written (outputs).
 constexpr int kWinThreads = kWinRows + 32;
 
-template <int MODE>
 #ifndef PG_WIN_MIN_BLOCKS
 #define PG_WIN_MIN_BLOCKS 4
 #endif
+// PAT = true: row-pattern matrices (pair8 = rpat; pptr / pent / npat / nent
+// the pattern table, staged after the ring): a row is its pattern's entries,
+// each one table entry {value, window offset} (a broadcast for the warp's
+// interior rows), one window load, mul, add -- no per-entry stream.
+template <int MODE, bool PAT, int LB>
 __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
     sell_win_kernel(SellArgs a, WinArgs wa, const uint8_t* __restrict__ pair8,
                     const PairEnt* __restrict__ ptab, const double* __restrict__ x, Epi e,
-                    double* partials, unsigned int* counter, double* nsq) {
-  pdl_entry();
+                    double* partials, unsigned int* counter, double* nsq,
+                    const int32_t* __restrict__ pptr, int npat, int nent,
+                    const uint32_t* __restrict__ pmask, const PatMaster pm) {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   extern __shared__ __align__(128) unsigned char smem_win[];
-  __shared__ PairEnt s_ptab[256];
+  __shared__ PairEnt s_ptab[PAT ? 1 : 256];
   __shared__ __align__(8) uint64_t full[kWinMaxStages];
   __shared__ __align__(8) uint64_t empty[kWinMaxStages];
   const int S = wa.stages;
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_ptab[i] = ptab[i];
+  // the tables never change after matrix creation: staged before the wait
+  const int32_t* s_pptr = nullptr;
+  const PairEnt* s_pent = nullptr;
+  const uint32_t* s_mask = nullptr;
+  if (PAT) {
+    unsigned char* tab = smem_win + (size_t)S * wa.stage_bytes;
+    s_pptr = stage_patterns(tab, pptr, ptab, npat, nent, pmask);
+    s_pent = reinterpret_cast<const PairEnt*>(tab);
+    s_mask = reinterpret_cast<const uint32_t*>(s_pptr + npat + 1);
+  } else {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_ptab[i] = ptab[i];
+  }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   if (threadIdx.x == 0) {
     for (int st = 0; st < S; ++st) {
       mbar_init(&full[st], 1);
@@ -530,7 +532,7 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
       // the packed-stream bounds of the next row block are loaded one
       // iteration ahead, off the issue path
       auto bounds = [&](int64_t rb, int64_t& p0, int64_t& p1) {
-        if (rb >= wa.nblk) return;
+        if (PAT || rb >= wa.nblk) return;
         const int64_t s0 = rb * (kWinRows / PG_SLICE);
         p0 = __ldg(a.slice_ptr8 + s0);
         p1 = __ldg(a.slice_ptr8 + min(s0 + kWinRows / PG_SLICE, wa.n_slices));
@@ -543,8 +545,8 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
         const int st = it % S;
         if (it >= S) mbar_wait(&empty[st], (uint32_t)((it / S - 1) & 1));
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        win_issue<MODE>(a, wa, e, pair8, x, rb, p0, p1, smem_win + (size_t)st * wa.stage_bytes,
-                        &full[st]);
+        win_issue<MODE, PAT>(a, wa, e, pair8, x, rb, p0, p1,
+                             smem_win + (size_t)st * wa.stage_bytes, &full[st]);
         p0 = q0;
         p1 = q1;
       }
@@ -572,6 +574,32 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
         }
       }
       mbar_wait(&full[st], (uint32_t)((it / S) & 1));
+      if (PAT) {
+        if (live) {
+          if (A) pre.a = reinterpret_cast<const double*>(buf + wa.off_ea)[t];
+          if (B) pre.b = reinterpret_cast<const double*>(buf + wa.off_eb)[t];
+          const int pid = buf[wa.off_p8 + t];
+          const unsigned char* winrow = buf + 8 * t;
+          const uint32_t mask = LB > 0 ? s_mask[pid] : (1u << 31);
+          double acc = 0.0;
+          if (LB > 0 && !(mask >> 31)) {
+            acc = row_sum_master<(LB > 0 ? LB : 8), true>(mask, pm, winrow, nullptr);
+          } else {
+            const int end = s_pptr[pid + 1];
+#pragma unroll 4
+            for (int q = s_pptr[pid]; q < end; ++q) {
+              const int4 raw = reinterpret_cast<const int4*>(s_pent)[q];
+              acc = __dadd_rn(acc, __dmul_rn(__hiloint2double(raw.y, raw.x),
+                                             *reinterpret_cast<const double*>(winrow + raw.z)));
+            }
+          }
+          const double r = epilogue<MODE>(e, pre, row, acc);
+          if (MODE == kResid) local = __fma_rn(r, r, local);
+        }
+        __syncwarp();
+        if ((t & 31) == 0) mbar_arrive(&empty[st]);
+        continue;
+      }
       if (kWinStageEpi) {
         if (lane < sl) swl = reinterpret_cast<const int32_t*>(buf + wa.off_sw)[lane];
         if (live) {
@@ -625,6 +653,32 @@ static int env_or(const char* name, int dflt) {
 // The row-pattern kernel runs when the matrix has a pattern dictionary and,
 // for matrices with a window plan (long stencil rows), only when
 // PG_SPMV_PAT_WIN=1 (measured against the windowed kernel per matrix).
+// The matrix's master pattern as kernel parameters (lb = 0: none, or
+// PG_SPMV_MASTER=0).
+static PatMaster master_of(const pg_matrix* m) {
+  static int on = -1;
+  if (on < 0) on = env_or("PG_SPMV_MASTER", 1);
+  PatMaster pm;
+  std::memset(&pm, 0, sizeof pm);
+  if (!on || m->pat_mlen <= 0) return pm;
+  pm.len = m->pat_mlen;
+  pm.lb = pm.len <= 8 ? 8 : pm.len <= 16 ? 16 : 32;
+  for (int q = 0; q < pm.len; ++q) {
+    pm.v[q] = m->pat_mv[q];
+    pm.doff[q] = m->pat_mdoff[q];
+    pm.woff[q] = m->pat_mwoff[q];
+  }
+  return pm;
+}
+
+// Windowed matrices with a row-pattern dictionary take the windowed kernel's
+// pattern variant (PG_SPMV_WINPAT=0: the pair-stream variant).
+bool winpat_enabled() {
+  static int on = -1;
+  if (on < 0) on = env_or("PG_SPMV_WINPAT", 1);
+  return on != 0;
+}
+
 bool pattern_kernel(const pg_matrix* m) {
   static int on = -1, win = -1;
   if (on < 0) {
@@ -658,6 +712,7 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
   // windowed kernel: long rows (27-point: 1.6x the pair kernel); short rows
   // (7-point) keep the global-gather pair kernel, which is faster there
   const bool win_ok = m->pair8 && m->wtab && aligned;
+  const bool win_pat = win_ok && m->rpat && winpat_enabled();
   if (pattern_kernel(m)) {
     int64_t blocks = (a.nlanes + kSellThreads - 1) / kSellThreads;
     static int per_sm = -1;
@@ -665,32 +720,31 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
     const int64_t cap = (MODE == kResid) ? kMaxBlocks : (int64_t)sms[dev] * per_sm;
     if (blocks > cap) blocks = cap;
     const size_t smem = pattern_smem_bytes(m->n_pat, m->pat_nent);
-    static int rb = -1;
-    if (rb < 0) rb = env_or("PG_SPMV_PAT_RB", 2);
-    const int r = m->pat_maxlen <= 8 ? rb : 1;
-    auto kern = r >= 4 ? sell_pat_kernel<MODE, 4> : r == 2 ? sell_pat_kernel<MODE, 2>
-                                                           : sell_pat_kernel<MODE, 1>;
-    static bool attr[4][3][64] = {};
-    const int ri = r >= 4 ? 2 : r == 2 ? 1 : 0;
-    if (!attr[MODE][ri][dev]) {
+    const PatMaster pm = master_of(m);
+    auto kern = pm.lb == 8 ? sell_pat_kernel<MODE, 8> : pm.lb == 16 ? sell_pat_kernel<MODE, 16>
+              : pm.lb == 32 ? sell_pat_kernel<MODE, 32> : sell_pat_kernel<MODE, 0>;
+    static bool attr[4][4][64] = {};
+    const int li = pm.lb / 8 > 3 ? 3 : pm.lb / 8;
+    if (!attr[MODE][li][dev]) {
       PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)pattern_smem_bytes(256, kPatMaxEnt)));
-      attr[MODE][ri][dev] = true;
+      attr[MODE][li][dev] = true;
     }
     launch_k(kern, (int)blocks, kSellThreads, smem, st, a, (const uint8_t*)m->rpat,
-             (const int32_t*)m->pat_ptr, (const PairEnt*)m->pat_ent, m->n_pat, m->pat_nent, x,
-             e, part, cnt, nsq);
+             (const int32_t*)m->pat_ptr, (const PairEnt*)m->pat_ent, m->n_pat, m->pat_nent,
+             (const uint32_t*)m->pat_mask, pm, x, e, part, cnt, nsq);
   } else if (win_ok) {
     WinArgs wa;
     wa.ng = m->n_wgrp;
     wa.total = m->win_elems;
     wa.b8 = m->win_b8;
     wa.off_p8 = ((8 * wa.total + 127) / 128) * 128;
-    wa.off_ea = wa.off_p8 + wa.b8;
+    wa.off_ea = wa.off_p8 + (win_pat ? kWinRows : wa.b8);
     wa.off_eb = wa.off_ea + 8 * kWinRows;
     wa.off_rl = wa.off_eb + 8 * kWinRows;
     wa.off_sw = wa.off_rl + 4 * kWinRows;
-    wa.stage_bytes = wa.off_sw + 128;
+    wa.stage_bytes = win_pat ? wa.off_rl : wa.off_sw + 128;
+    const size_t tab_bytes = win_pat ? pattern_smem_bytes(m->n_pat, m->pat_nent) : 0;
     wa.ncols = m->ncols;
     wa.nblk = (m->nrows + kWinRows - 1) / kWinRows;
     wa.n_slices = m->n_slices;
@@ -699,36 +753,49 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
       wa.start[g] = m->wstart[g];
       wa.len[g] = m->wlen[g];
     }
-    wa.stages = kWinSmemBudget / kWinTargetBlocks / wa.stage_bytes;
+    wa.stages = (int)((kWinSmemBudget / kWinTargetBlocks - (int)tab_bytes) / wa.stage_bytes);
     if (wa.stages < 2) wa.stages = 2;
     if (wa.stages > kWinMaxStages) wa.stages = kWinMaxStages;
-    const size_t smem = (size_t)wa.stages * wa.stage_bytes;
-    auto kern = sell_win_kernel<MODE>;
-    static bool attr[4][64] = {};
-    if (!attr[MODE][dev]) {
+    const size_t smem = (size_t)wa.stages * wa.stage_bytes + tab_bytes;
+    const PatMaster pm = win_pat ? master_of(m) : PatMaster{};
+    auto kern = !win_pat      ? sell_win_kernel<MODE, false, 0>
+                : pm.lb == 8  ? sell_win_kernel<MODE, true, 8>
+                : pm.lb == 16 ? sell_win_kernel<MODE, true, 16>
+                : pm.lb == 32 ? sell_win_kernel<MODE, true, 32>
+                              : sell_win_kernel<MODE, true, 0>;
+    const int pk = !win_pat ? 0 : 1 + (pm.lb / 8 > 3 ? 3 : pm.lb / 8);
+    static bool attr[5][4][64] = {};
+    if (!attr[pk][MODE][dev]) {
       PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kWinSmemBudget));
-      attr[MODE][dev] = true;
+      attr[pk][MODE][dev] = true;
     }
     // resident grid: blocks per SM from the occupancy calculator at this
     // stage size (cached per kernel / device / size) x PG_SPMV_WIN_WAVES
-    static int occ_b[4][64] = {}, occ_n[4][64] = {};
-    if (occ_b[MODE][dev] != wa.stage_bytes) {
+    static size_t occ_b[5][4][64] = {};
+    static int occ_n[5][4][64] = {};
+    if (occ_b[pk][MODE][dev] != smem) {
       int nb = 0;
       PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kWinThreads, smem));
-      occ_n[MODE][dev] = nb > 0 ? nb : 1;
-      occ_b[MODE][dev] = wa.stage_bytes;
+      occ_n[pk][MODE][dev] = nb > 0 ? nb : 1;
+      occ_b[pk][MODE][dev] = smem;
     }
     static int waves = -1;
     if (waves < 0) {
       const char* s = std::getenv("PG_SPMV_WIN_WAVES");
       waves = s ? std::atoi(s) : 1;
     }
-    int64_t g = waves > 0 ? (int64_t)sms[dev] * occ_n[MODE][dev] * waves : wa.nblk;
+    int64_t g = waves > 0 ? (int64_t)sms[dev] * occ_n[pk][MODE][dev] * waves : wa.nblk;
     if (g > wa.nblk) g = wa.nblk;
     if (MODE == kResid && g > kMaxBlocks) g = kMaxBlocks;
-    launch_k(kern, (int)g, kWinThreads, smem, st, a, wa, (const uint8_t*)m->pair8,
-             (const PairEnt*)m->ptab, x, e, part, cnt, nsq);
+    if (win_pat)
+      launch_k(kern, (int)g, kWinThreads, smem, st, a, wa, (const uint8_t*)m->rpat,
+               (const PairEnt*)m->pat_ent, x, e, part, cnt, nsq, (const int32_t*)m->pat_ptr,
+               m->n_pat, m->pat_nent, (const uint32_t*)m->pat_mask, pm);
+    else
+      launch_k(kern, (int)g, kWinThreads, smem, st, a, wa, (const uint8_t*)m->pair8,
+               (const PairEnt*)m->ptab, x, e, part, cnt, nsq, (const int32_t*)nullptr, 0, 0,
+               (const uint32_t*)nullptr, pm);
   } else if (m->pair8) {
     static int per_sm = -1;
     if (per_sm < 0) {

@@ -213,7 +213,7 @@ class Shard:
         matrix stream (1 B per row for the row-pattern format; else the
         stored entry bytes + a 4-byte row length), the compulsory gather of x
         (8 B per row) and ``vec_bytes`` per row of epilogue vectors."""
-        if self.stats["kernel"] == 5:
+        if self.stats["kernel"] in (5, 6):
             return (1 + 8 + vec_bytes) * self.n
         return self.entry_bytes * self.nnz + (12 + vec_bytes) * self.n
 

@@ -124,6 +124,39 @@ def test_chain_pattern_kernel_matches_oracle(monkeypatch):
         op.close()
 
 
+def _lap_modified_boundary(g):
+    """2-D Laplacian whose boundary rows carry a different diagonal: their
+    row patterns are NOT masked subsequences of the interior pattern, so the
+    pattern kernels take the table walk for them (and the unrolled master
+    path for the interior rows)."""
+    h = wl.laplacian2d(g)
+    rp, ci = np.asarray(h.row_ptr), np.asarray(h.col_idx)
+    vals = np.array(h.values, dtype=np.float64)
+    for r in range(h.nrows):
+        if rp[r + 1] - rp[r] < 5:
+            for q in range(rp[r], rp[r + 1]):
+                if ci[q] == r:
+                    vals[q] = 5.0
+    return wl.CsrHost(h.nrows, h.ncols, rp, ci, vals)
+
+
+def test_pattern_master_and_table_paths_bitwise():
+    """Row-pattern kernels: interior rows through the master pattern,
+    modified boundary rows through the table walk, both windowed (27-point)
+    and global-gather (5/7-point): SpMV and p(A)v equal the oracle."""
+    from oracle import pgmres_oracle as orc
+    for h in (_lap_modified_boundary(40), _lap_modified_boundary(33), wl.aniso27(12),
+              wl.convdiff3d_7pt(11)):
+        op = pg.DeviceMatrixOperator(h, sigma=1)
+        O = orc.OracleMatrix.of(h)
+        x = wl.splitmix_uniform(9, h.nrows)
+        assert np.array_equal(op.apply(x), O.matvec(x))
+        y = np.random.default_rng(3).uniform(-1, 1, 6)
+        got = pg.apply_poly(pg.PolyCoefficients(5, y, 1.0), op, x, pg.CostCounters())
+        assert np.array_equal(got, orc.poly_eval(y, O, x, orc.Tally()))
+        op.close()
+
+
 def test_chain_full_cfg2_size(monkeypatch):
     """n = 1e6, degree 14 (the headline's effective degree): a few Arnoldi
     steps through the chain kernel equal the pass-by-pass path bit for bit."""
