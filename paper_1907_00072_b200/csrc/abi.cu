@@ -327,6 +327,8 @@ static void build_patterns(const SellHost& h, const std::vector<uint8_t>& p8,
       mask[p] = bits;
     }
     m->pat_mlen = (int)ms.size();
+    m->pat_all_master = 1;
+    for (uint32_t b : mask) m->pat_all_master &= (b >> 31) ? 0 : 1;
     for (size_t q = 0; q < ms.size(); ++q) {
       const PairEnt& pe = ptab[(uint8_t)ms[q]];
       m->pat_mv[q] = pe.v;

@@ -95,7 +95,7 @@ struct pg_matrix {
   // the bit set of master entries pattern p consists of, in order and with
   // identical values (a boundary row of a constant-coefficient stencil), or
   // bit 31 set when p is not such a subsequence
-  int pat_mlen;
+  int pat_mlen, pat_all_master;
   double pat_mv[32];
   int32_t pat_mdoff[32], pat_mwoff[32];
   uint32_t* pat_mask;

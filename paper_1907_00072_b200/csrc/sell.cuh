@@ -247,7 +247,8 @@ __host__ __device__ inline size_t pattern_smem_bytes(int npat, int nent) {
 
 // The master pattern as kernel parameters (pg_matrix::pat_m*): offsets and
 // values become constant-bank operands of fully unrolled code.  lb = the
-// unroll bucket (8 / 16 / 32) >= len; entries len..lb-1 are inert.
+// unrolled length: len itself for the common stencil rows (7, 27), else the
+// bucket 8 / 16 / 32 >= len whose entries len..lb-1 are inert.
 struct PatMaster {
   int len, lb;
   double v[32];
@@ -271,17 +272,20 @@ __device__ __forceinline__ double row_sum_master(uint32_t mask, const PatMaster&
     double xv[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
+      if (c0 + q >= LB) break;
       if (WIN) {
         xv[q] = *reinterpret_cast<const double*>(winrow + pm.woff[c0 + q]);
       } else {
         xv[q] = 0.0;
-        if ((mask >> (c0 + q)) & 1u) xv[q] = CG ? __ldcg(xr + pm.doff[c0 + q]) : __ldg(xr + pm.doff[c0 + q]);
+        if (mask & (1u << (c0 + q)))
+          xv[q] = CG ? __ldcg(xr + pm.doff[c0 + q]) : __ldg(xr + pm.doff[c0 + q]);
       }
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
+      if (c0 + q >= LB) break;
       const double p = __dmul_rn(pm.v[c0 + q], xv[q]);
-      if ((mask >> (c0 + q)) & 1u) acc = __dadd_rn(acc, p);
+      if (mask & (1u << (c0 + q))) acc = __dadd_rn(acc, p);
     }
   }
   return acc;

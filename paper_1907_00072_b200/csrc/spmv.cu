@@ -662,13 +662,18 @@ static PatMaster master_of(const pg_matrix* m) {
   std::memset(&pm, 0, sizeof pm);
   if (!on || m->pat_mlen <= 0) return pm;
   pm.len = m->pat_mlen;
-  pm.lb = pm.len <= 8 ? 8 : pm.len <= 16 ? 16 : 32;
+  pm.lb = (pm.len == 7 || pm.len == 27) ? pm.len : pm.len <= 8 ? 8 : pm.len <= 16 ? 16 : 32;
   for (int q = 0; q < pm.len; ++q) {
     pm.v[q] = m->pat_mv[q];
     pm.doff[q] = m->pat_mdoff[q];
     pm.woff[q] = m->pat_mwoff[q];
   }
   return pm;
+}
+
+// kernel-cache slot of an unrolled master length (0: none)
+static int lb_index(int lb) {
+  return lb == 7 ? 1 : lb == 8 ? 2 : lb == 16 ? 3 : lb == 27 ? 4 : lb == 32 ? 5 : 0;
 }
 
 // Windowed matrices with a row-pattern dictionary take the windowed kernel's
@@ -721,10 +726,11 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
     if (blocks > cap) blocks = cap;
     const size_t smem = pattern_smem_bytes(m->n_pat, m->pat_nent);
     const PatMaster pm = master_of(m);
-    auto kern = pm.lb == 8 ? sell_pat_kernel<MODE, 8> : pm.lb == 16 ? sell_pat_kernel<MODE, 16>
+    auto kern = pm.lb == 7 ? sell_pat_kernel<MODE, 7> : pm.lb == 8 ? sell_pat_kernel<MODE, 8>
+              : pm.lb == 16 ? sell_pat_kernel<MODE, 16> : pm.lb == 27 ? sell_pat_kernel<MODE, 27>
               : pm.lb == 32 ? sell_pat_kernel<MODE, 32> : sell_pat_kernel<MODE, 0>;
-    static bool attr[4][4][64] = {};
-    const int li = pm.lb / 8 > 3 ? 3 : pm.lb / 8;
+    static bool attr[4][6][64] = {};
+    const int li = lb_index(pm.lb);
     if (!attr[MODE][li][dev]) {
       PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)pattern_smem_bytes(256, kPatMaxEnt)));
@@ -744,7 +750,10 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
     wa.off_rl = wa.off_eb + 8 * kWinRows;
     wa.off_sw = wa.off_rl + 4 * kWinRows;
     wa.stage_bytes = win_pat ? wa.off_rl : wa.off_sw + 128;
-    const size_t tab_bytes = win_pat ? pattern_smem_bytes(m->n_pat, m->pat_nent) : 0;
+    const PatMaster pm = win_pat ? master_of(m) : PatMaster{};
+    // every pattern a masked master subsequence: the entry table is never read
+    const int tab_nent = (win_pat && pm.lb > 0 && m->pat_all_master) ? 0 : m->pat_nent;
+    const size_t tab_bytes = win_pat ? pattern_smem_bytes(m->n_pat, tab_nent) : 0;
     wa.ncols = m->ncols;
     wa.nblk = (m->nrows + kWinRows - 1) / kWinRows;
     wa.n_slices = m->n_slices;
@@ -757,14 +766,15 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
     if (wa.stages < 2) wa.stages = 2;
     if (wa.stages > kWinMaxStages) wa.stages = kWinMaxStages;
     const size_t smem = (size_t)wa.stages * wa.stage_bytes + tab_bytes;
-    const PatMaster pm = win_pat ? master_of(m) : PatMaster{};
     auto kern = !win_pat      ? sell_win_kernel<MODE, false, 0>
+                : pm.lb == 7  ? sell_win_kernel<MODE, true, 7>
                 : pm.lb == 8  ? sell_win_kernel<MODE, true, 8>
                 : pm.lb == 16 ? sell_win_kernel<MODE, true, 16>
+                : pm.lb == 27 ? sell_win_kernel<MODE, true, 27>
                 : pm.lb == 32 ? sell_win_kernel<MODE, true, 32>
                               : sell_win_kernel<MODE, true, 0>;
-    const int pk = !win_pat ? 0 : 1 + (pm.lb / 8 > 3 ? 3 : pm.lb / 8);
-    static bool attr[5][4][64] = {};
+    const int pk = !win_pat ? 0 : 1 + lb_index(pm.lb);
+    static bool attr[7][4][64] = {};
     if (!attr[pk][MODE][dev]) {
       PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kWinSmemBudget));
@@ -772,8 +782,8 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
     }
     // resident grid: blocks per SM from the occupancy calculator at this
     // stage size (cached per kernel / device / size) x PG_SPMV_WIN_WAVES
-    static size_t occ_b[5][4][64] = {};
-    static int occ_n[5][4][64] = {};
+    static size_t occ_b[7][4][64] = {};
+    static int occ_n[7][4][64] = {};
     if (occ_b[pk][MODE][dev] != smem) {
       int nb = 0;
       PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kWinThreads, smem));
@@ -791,7 +801,7 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
     if (win_pat)
       launch_k(kern, (int)g, kWinThreads, smem, st, a, wa, (const uint8_t*)m->rpat,
                (const PairEnt*)m->pat_ent, x, e, part, cnt, nsq, (const int32_t*)m->pat_ptr,
-               m->n_pat, m->pat_nent, (const uint32_t*)m->pat_mask, pm);
+               m->n_pat, tab_nent, (const uint32_t*)m->pat_mask, pm);
     else
       launch_k(kern, (int)g, kWinThreads, smem, st, a, wa, (const uint8_t*)m->pair8,
                (const PairEnt*)m->ptab, x, e, part, cnt, nsq, (const int32_t*)nullptr, 0, 0,
