@@ -59,7 +59,9 @@ struct ChainParams {
   const uint8_t* rpat;  // row-pattern body: pattern id per row and the table
   const int32_t* pptr;
   const PairEnt* pent;
+  const uint32_t* pmask;
   int npat, nent;
+  PatMaster pm;  // master pattern (pm.lb == 8: unrolled row path; else table walk)
   int64_t nrows, nlanes, stride8;
   unsigned nchunk;
   unsigned* ctl;
@@ -100,16 +102,21 @@ template <int MODE, int TS, int BODY>
 __device__ __forceinline__ void chain_rows(const ChainParams& P, const ChainPassDev& ps,
                                            int64_t c, int lane, const int (&len)[TS],
                                            const uint32_t (&w0)[TS], const uint32_t (&w1)[TS],
-                                           const PairEnt* s_tab, const int32_t* s_ptr) {
+                                           const PairEnt* s_tab, const int32_t* s_ptr,
+                                           const uint32_t* s_mask) {
 #pragma unroll
   for (int u = 0; u < TS; ++u) {
     const int64_t row = ((int64_t)c * TS + u) * PG_SLICE + lane;
     if (row < P.nrows) {
       const Pre pre = chain_pre<MODE>(ps.e, ps.x, row);
       double ax;
-      if (BODY == 1)
-        ax = row_sum_pattern<true>(s_ptr[len[u]], s_ptr[len[u] + 1], row, ps.x,
-                                                s_tab);
+      if (BODY == 1) {
+        const uint32_t mask = s_mask[len[u]];
+        if (P.pm.lb == 8 && !(mask >> 31))
+          ax = row_sum_master<8, false, true>(mask, P.pm, nullptr, ps.x + row);
+        else
+          ax = row_sum_pattern<true>(s_ptr[len[u]], s_ptr[len[u] + 1], row, ps.x, s_tab);
+      }
       else
         ax = len[u] > 0
                  ? row_sum_pair_words<true>(w0[u], w1[u], len[u], row, ps.x, s_tab)
@@ -132,8 +139,10 @@ __global__ void __launch_bounds__(kChainThreads, PG_CHAIN_MIN_BLOCKS)
   extern __shared__ __align__(16) unsigned char smem_chain[];
   const PairEnt* s_tab = reinterpret_cast<const PairEnt*>(smem_chain);
   const int32_t* s_ptr = nullptr;
+  const uint32_t* s_mask = nullptr;
   if (BODY == 1) {
-    s_ptr = stage_patterns(smem_chain, P.pptr, P.pent, P.npat, P.nent);
+    s_ptr = stage_patterns(smem_chain, P.pptr, P.pent, P.npat, P.nent, P.pmask);
+    s_mask = reinterpret_cast<const uint32_t*>(s_ptr + P.npat + 1);
   } else {
     PairEnt* t = reinterpret_cast<PairEnt*>(smem_chain);
     for (int i = threadIdx.x; i < 256; i += blockDim.x) t[i] = P.ptab[i];
@@ -192,11 +201,11 @@ __global__ void __launch_bounds__(kChainThreads, PG_CHAIN_MIN_BLOCKS)
     }
     const ChainPassDev& ps = P.p[k];
     if (ps.mode == kPoly)
-      chain_rows<kPoly, TS, BODY>(P, ps, c, lane, len, w0, w1, s_tab, s_ptr);
+      chain_rows<kPoly, TS, BODY>(P, ps, c, lane, len, w0, w1, s_tab, s_ptr, s_mask);
     else if (ps.mode == kSpmv)
-      chain_rows<kSpmv, TS, BODY>(P, ps, c, lane, len, w0, w1, s_tab, s_ptr);
+      chain_rows<kSpmv, TS, BODY>(P, ps, c, lane, len, w0, w1, s_tab, s_ptr, s_mask);
     else
-      chain_rows<kRoot, TS, BODY>(P, ps, c, lane, len, w0, w1, s_tab, s_ptr);
+      chain_rows<kRoot, TS, BODY>(P, ps, c, lane, len, w0, w1, s_tab, s_ptr, s_mask);
     // every lane's stores are ordered before lane 0's release (bar.warp.sync)
     __syncwarp();
     if (lane == 0) st_release_u64(P.flags + c, (gen << 8) | (unsigned long long)(k + 1));
@@ -292,6 +301,17 @@ bool chain_launch(const pg_matrix* m, const ChainStep* steps, int np, pg_workspa
   P.rpat = m->rpat;
   P.pptr = m->pat_ptr;
   P.pent = (const PairEnt*)m->pat_ent;
+  P.pmask = m->pat_mask;
+  P.pm.lb = 0;
+  if (body == 1 && m->pat_mlen > 0 && m->pat_mlen <= 8) {
+    P.pm.len = m->pat_mlen;
+    P.pm.lb = 8;
+    for (int q = 0; q < m->pat_mlen; ++q) {
+      P.pm.v[q] = m->pat_mv[q];
+      P.pm.doff[q] = m->pat_mdoff[q];
+      P.pm.woff[q] = m->pat_mwoff[q];
+    }
+  }
   P.npat = m->n_pat;
   P.nent = m->pat_nent;
   P.nrows = m->nrows;

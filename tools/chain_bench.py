@@ -25,7 +25,7 @@ def main():
     ap.add_argument("--degree", type=int, default=14)
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--grid", type=int, default=100)
-    ap.add_argument("--settings", default="chain=0;ts=4;ts=2;ts=1;ts=8;ts=4,dyn=1;ts=4,bps=3;ts=4,bps=2")
+    ap.add_argument("--settings", default="chain=0;chain=1,ts=4;chain=1,ts=2;chain=1,ts=1;chain=1,ts=8")
     ap.add_argument("--tag", default="")
     args = ap.parse_args()
     h = wl.convdiff3d_7pt(args.grid)
