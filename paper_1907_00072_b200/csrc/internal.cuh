@@ -252,6 +252,11 @@ inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
 
 int grid_for(int device, const void* kernel, int block, size_t smem, int64_t work_blocks);
 
+// out = x / sqrt(*nsq) and host[0..count) = ring[0..count) (host: a
+// device-usable address of pinned host memory), one kernel (ortho.cu).
+void normalize_publish(const double* x, const double* nsq, int64_t n, double* out,
+                       const double* ring, int count, double* host, cudaStream_t st);
+
 // One SpMV pass of a chain (chain.cu): x is the gathered vector; the other
 // fields are the pass's epilogue (pg_poly_pass / pg_root_pass / pg_spmv
 // arguments: acc_out doubles as the SpMV output).

@@ -506,6 +506,25 @@ __global__ void normalize_kernel(const double* __restrict__ x, const double* __r
     out[i] = __ddiv_rn(x[i], nrm);
 }
 
+// normalize_kernel + publish: block 0 also copies the step's scalar ring
+// [c1 | c2 | |w2|^2] into the caller's pinned host ring through its mapped
+// (UVA) address, so no D2H copy sits on the stream between two Arnoldi
+// steps (a copy-engine transfer there cost ~20-30 us per step).
+__global__ void normalize_publish_kernel(const double* __restrict__ x,
+                                         const double* __restrict__ nsq, int64_t n,
+                                         double* __restrict__ out, const double* __restrict__ ring,
+                                         int count, double* host) {
+  pdl_entry();
+  const double nrm = sqrt(*nsq);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = __ddiv_rn(x[i], nrm);
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) host[i] = ring[i];
+    __threadfence_system();
+  }
+}
+
 __global__ void scale_add_kernel(const double* base, double a, const double* v, int64_t n,
                                  double* out) {
   pdl_entry();
@@ -676,6 +695,15 @@ static int simple_grid(int64_t n, int threads, pg_workspace* ws) {
 }  // namespace pg
 
 using namespace pg;
+
+namespace pg {
+void normalize_publish(const double* x, const double* nsq, int64_t n, double* out,
+                       const double* ring, int count, double* host, cudaStream_t st) {
+  const int g = n > 0 ? simple_grid(n, 256, nullptr) : 1;
+  launch_k(normalize_publish_kernel, g, 256, 0, st, x, nsq, n, out, ring, count, host);
+  check_launch();
+}
+}  // namespace pg
 
 extern "C" {
 

@@ -8,6 +8,9 @@
 // the same launches in C++ (same kernels, same order, same arguments as the
 // per-kernel entry points: results are bit-identical), one call per step.
 
+#include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "internal.cuh"
@@ -184,6 +187,31 @@ void roots_chain(const pg_matrix* m, int nroot, const int* rmode, const double* 
   }
 }
 
+// Device address of a pinned host buffer (UVA mapping), cached per buffer;
+// nullptr when the buffer is not mapped, inside a graph capture before the
+// buffer was seen (no API call while capturing), or with PG_PUBLISH=0.
+double* mapped_host(double* h) {
+  static std::mutex mu;
+  static std::unordered_map<void*, void*> cache;
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("PG_PUBLISH");
+    on = e ? std::atoi(e) != 0 : 1;
+  }
+  if (!on || !h) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(h);
+  if (it != cache.end()) return static_cast<double*>(it->second);
+  if (pg::g_capturing) return nullptr;
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) {
+    cudaGetLastError();  // not mapped: clear the error, use the copy
+    d = nullptr;
+  }
+  cache.emplace(h, d);
+  return static_cast<double*>(d);
+}
+
 // The passes roots_chain issues, as chain steps.
 std::vector<ChainStep> roots_steps(int nroot, const int* rmode, const double* rc, const double* v,
                                    double* z, double* t, double* w0, double* w1) {
@@ -258,9 +286,16 @@ void arnoldi_step_body(const pg_matrix* mat, const double* y, int d, double* d_V
     ok(pg_cgs2_phase1(d_V, ld, k, d_z, n, c1, ws, stream));
     ok(pg_cgs2_phase2(d_V, ld, k, d_z, n, c1, c2, ws, stream));
     ok(pg_cgs2_phase3(d_V, ld, k, d_z, n, c1, c2, col, nsq, ws, stream));
-    ok(pg_normalize(col, nsq, n, col, stream));
-    PG_CUDA(cudaMemcpyAsync(h_ring, d_ring, sizeof(double) * (2 * PG_KMAX + 1),
-                            cudaMemcpyDeviceToHost, as_stream(stream)));
+    // normalise into column k and publish the scalars straight into the
+    // pinned host ring (no copy-engine transfer between steps), or copy them
+    double* h_dev = mapped_host(h_ring);
+    if (h_dev) {
+      normalize_publish(col, nsq, n, col, d_ring, 2 * PG_KMAX + 1, h_dev, as_stream(stream));
+    } else {
+      ok(pg_normalize(col, nsq, n, col, stream));
+      PG_CUDA(cudaMemcpyAsync(h_ring, d_ring, sizeof(double) * (2 * PG_KMAX + 1),
+                              cudaMemcpyDeviceToHost, as_stream(stream)));
+    }
     record(ev_done, stream);
 }
 

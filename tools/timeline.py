@@ -68,6 +68,10 @@ def main():
                idle_us=span - busy, gaps_over_10us=sum(g for g in gaps if g > 10),
                n_gaps_over_10us=sum(1 for g in gaps if g > 10), largest_gaps_us=big,
                memops=len(mem),
+               all_gaps_over_10us=[dict(gap_us=round(gaps[i], 1), at_kernel=i,
+                                        before=kern[i][2].split("(")[0][-30:],
+                                        after=kern[i + 1][2].split("(")[0][-30:])
+                                   for i in range(len(gaps)) if gaps[i] > 10],
                per_kernel={k: dict(n=v[0], us=round(v[1], 1)) for k, v in
                            sorted(per.items(), key=lambda kv: -kv[1][1])})
     print(json.dumps(out, indent=1))
