@@ -291,7 +291,9 @@ def run_ours(args):
     b_pin = torch.from_numpy(b_host).pin_memory()
     v0_pin = torch.from_numpy(v0_host).pin_memory()
     e2e_times = []
-    for i in range(max(1, min(args.steps, 10)) + 1):
+    # two warm-up calls: the first pinned-input solves settle the caching
+    # allocator's buffers, so the recorded step graphs' keys repeat
+    for i in range(max(1, min(args.steps, 10)) + 2):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -301,7 +303,7 @@ def run_ours(args):
         r2 = pg.solve(op, b_pin, right_prec=p2, config=cfg)
         x_host = r2.x  # CPU tensor (D2H inside the timed region)
         torch.cuda.synchronize()
-        if i > 0:  # first call is a warm-up
+        if i > 1:  # warm-up calls excluded
             e2e_times.append(time.perf_counter() - t0)
     e2e = float(np.mean(e2e_times))
     if world > 1:

@@ -107,10 +107,9 @@ def _device_power_gram(op, v0, top: int, counters: CostCounters):
     if top + 1 > KMAX:
         raise ParameterError(f"power sequence of {top + 1} columns exceeds the kernel limit {KMAX}")
     vs = e.ingest(v0)
-    nsq = e.dot(vs, vs, slot=6)
-    seed_norm = float(np.sqrt(nsq))
-    if seed_norm == 0.0:
-        raise ParameterError("seed vector v0 must be nonzero")
+    # |v0|^2 stays in device slot 6 while the power sequence and the Gram are
+    # queued: one host round trip (the Gram's) instead of two
+    e.dot(vs, vs, slot=6, fetch=False)
     P = e.cached_blocks("powers", top + 1)
     # column 0 = v0 / |v0| (exact division, as numpy's v0 / seed_norm)
     e.normalize_dev(vs, e.slot(6), [blk[0] for blk in P])
@@ -118,6 +117,9 @@ def _device_power_gram(op, v0, top: int, counters: CostCounters):
         e.count_ops(op.counters, 1)
         e.spmv([blk[k] for blk in P], [blk[k + 1] for blk in P])
     G = e.gram(P, top + 1)
+    seed_norm = float(np.sqrt(e.read_slot(6)))
+    if seed_norm == 0.0:
+        raise ParameterError("seed vector v0 must be nonzero")
     return G, seed_norm
 
 

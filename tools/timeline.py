@@ -52,6 +52,15 @@ def main():
     mem = [ev for ev in prof.events() if ev.device_type == torch.autograd.DeviceType.CUDA
            and ev.name and ("Memcpy" in ev.name or "Memset" in ev.name)]
     kern.sort()
+    # host activity around the first kernels (where the per-solve fixed gaps are)
+    t_lo = kern[0][0] - 50
+    t_hi = kern[min(40, len(kern) - 1)][1]
+    cpu = sorted((ev.time_range.start, ev.time_range.end - ev.time_range.start, ev.name)
+                 for ev in prof.events()
+                 if ev.device_type == torch.autograd.DeviceType.CPU and
+                 t_lo <= ev.time_range.start <= t_hi)
+    host_ops = [dict(t_us=round(a - kern[0][0], 1), dur_us=round(d, 1), name=nm[:60])
+                for a, d, nm in cpu if d > 5][:80]
     span = kern[-1][1] - kern[0][0]
     busy = sum(e - s for s, e, _ in kern)
     gaps = [kern[i + 1][0] - kern[i][1] for i in range(len(kern) - 1)]
@@ -67,7 +76,9 @@ def main():
     out = dict(iterations=res.iterations, kernels=len(kern), span_us=span, busy_us=busy,
                idle_us=span - busy, gaps_over_10us=sum(g for g in gaps if g > 10),
                n_gaps_over_10us=sum(1 for g in gaps if g > 10), largest_gaps_us=big,
-               memops=len(mem),
+               memops=len(mem), host_ops_first_kernels=host_ops,
+               first_kernels=[dict(t_us=round(a - kern[0][0], 1), dur_us=round(b - a, 1),
+                                   name=nm.split("(")[0][-40:]) for a, b, nm in kern[:40]],
                all_gaps_over_10us=[dict(gap_us=round(gaps[i], 1), at_kernel=i,
                                         before=kern[i][2].split("(")[0][-30:],
                                         after=kern[i + 1][2].split("(")[0][-30:])
