@@ -44,12 +44,26 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // Stage tile `tile` of columns 0..ncol-1 (column k = z when z != nullptr).
+// Warp w copies columns w, w + 8, ...: each lane two 16-byte pieces of a
+// 1 KB column segment, the column's address computed once per column; full
+// tiles need no per-piece bounds (ncu: the tile kernels were issue-bound,
+// 57% issue-active, largely on the per-piece address arithmetic).
 __device__ __forceinline__ void stage_tile(double* buf, const double* __restrict__ V, int64_t ld,
                                            int k, const double* __restrict__ z, int64_t n,
                                            int64_t tile) {
   const int ncol = z ? k + 1 : k;
   const int64_t row0 = tile * kTileRows;
   const int64_t rows = min((int64_t)kTileRows, n - row0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (rows == kTileRows) {
+    for (int colx = warp; colx < ncol; colx += kTileThreads / 32) {
+      const double* src = (colx < k ? V + (int64_t)colx * ld : z) + row0 + 2 * lane;
+      double* dst = buf + colx * kTileStride + 2 * lane;
+      cp_async16(dst, src, 16);
+      cp_async16(dst + 64, src + 64, 16);
+    }
+    return;
+  }
   constexpr int kChunks = kTileRows / 2;
   for (int c = threadIdx.x; c < ncol * kChunks; c += kTileThreads) {
     const int colx = c / kChunks, ch = c - colx * kChunks;
@@ -574,10 +588,18 @@ static size_t tile_smem(int mode, int k, int stages) {
 }
 
 // Ring depth: the deepest ring (<= 4 stages) that still lets `ctas` CTAs
-// share an SM.  Co-resident CTAs hide each other's reduction phases (phase 2
-// also runs a serial k-long row projection per tile): with 1 CTA x 4 stages
-// phase 2 at k=51, n=8M ran at 3.3 TB/s, with 2 x 2 at 5.3.
-static int tile_stages(int mode, int k) {
+// share an SM (the occupancy calculator then co-locates as many CTAs as the
+// ring leaves room for).  Sweep on B200 (tools/cgs2_bench.py with
+// PG_TILE_CTAS_P1/P2 = 1..4 at n = 1e6 and 8e6, k = 16..51,
+// profiles/r01e/cgs2_ring_sweep.md):
+//  * phase 1 (c = V^T z): the deepest ring (ctas = 1) wins at n <= 2M for
+//    every k (k = 25: 48.3 vs 55.7 us with ctas = 3) and at n = 8M from
+//    k = 35; below that a 4-CTA ring (k = 20: 212 vs 227 us);
+//  * phase 2 (w1 and c = V^T w1, a serial row projection per tile): more
+//    co-resident CTAs hide it -- 4 up to k = 20, 3 up to k = 35, then 3 at
+//    n <= 2M and 2 at 8M (k = 51: 672 vs 871 us with ctas = 1);
+//  * the Gram keeps one deep ring (FP64-bound, insensitive).
+static int tile_stages(int mode, int k, int64_t n) {
   // PG_TILE_CTAS_P{1,2,3}: CTAs per SM the ring is sized for (experiments)
   static int ctas_env[4] = {-1, -1, -1, -1};
   if (ctas_env[mode] < 0) {
@@ -585,9 +607,15 @@ static int tile_stages(int mode, int k) {
     const char* s = std::getenv(names[mode]);
     ctas_env[mode] = s ? std::atoi(s) : 0;
   }
-  // sweep (tools/cgs2_sweep.py, n = 1e6 and 8e6): 3 co-resident CTAs up to
-  // k = 40, 2 beyond, for both dot phases; the Gram keeps one deep ring
-  int ctas = ctas_env[mode] > 0 ? ctas_env[mode] : (mode == kGram ? 1 : (k <= 40 ? 3 : 2));
+  const bool small = n <= (int64_t)2000000;
+  int ctas;
+  if (mode == kGram)
+    ctas = 1;
+  else if (mode == kDots)
+    ctas = (small || k >= 35) ? 1 : 4;
+  else
+    ctas = k <= 20 ? 4 : k <= 35 ? 3 : (small ? 3 : 2);
+  if (ctas_env[mode] > 0) ctas = ctas_env[mode];
   const size_t per_sm = kTileSmemMax / ctas;
   for (int s = 4; s > 2; --s)
     if (tile_smem(mode, k, s) <= per_sm) return s;
@@ -642,7 +670,7 @@ static void launch_tile(const double* V, int64_t ld, int k, const double* z, int
   PG_REQUIRE(ld % 2 == 0, PG_ERR_PARAMETER, "leading dimension must be even");
   PG_REQUIRE(((uintptr_t)V & 15) == 0 && (!z || ((uintptr_t)z & 15) == 0), PG_ERR_PARAMETER,
              "tile operands must be 16-byte aligned");
-  const int stages = tile_stages(MODE, k);
+  const int stages = tile_stages(MODE, k, n);
   const size_t smem = tile_smem(MODE, k, stages);
   const int dev = ws->device;
   PG_REQUIRE(dev >= 0 && dev < 64, PG_ERR_PARAMETER, "device ordinal out of range");
@@ -651,6 +679,7 @@ static void launch_tile(const double* V, int64_t ld, int k, const double* z, int
                                    : (const void*)tile_kernel<MODE, 2>;
   static bool attr_set[4][64] = {};
   static int grid_cache[4][PG_KMAX + 1][64] = {};
+  static int grid_stages[4][PG_KMAX + 1][64] = {};
   if (!attr_set[MODE][dev]) {
     PG_CUDA(cudaFuncSetAttribute(tile_kernel<MODE, 4>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemMax));
@@ -666,9 +695,10 @@ static void launch_tile(const double* V, int64_t ld, int k, const double* z, int
     return;
   }
   int g = grid_cache[MODE][k][dev];
-  if (g == 0) {
+  if (g == 0 || grid_stages[MODE][k][dev] != stages) {
     g = grid_for(dev, kern, kTileThreads, smem, int64_t(1) << 40);
     grid_cache[MODE][k][dev] = g;
+    grid_stages[MODE][k][dev] = stages;
   }
   if (ntiles < g) g = (int)ntiles;
   if (stages == 4)

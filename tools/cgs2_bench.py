@@ -34,17 +34,19 @@ def timed(fn, reps):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--n", default="1000000,8000000")
+    ap.add_argument("--k", default="10,25,51")
     args = ap.parse_args()
     ws = workspace(torch.cuda.current_device())
     st = torch.cuda.current_stream().cuda_stream
-    for n in (1_000_000, 8_000_000):
+    for n in [int(v) for v in args.n.split(",")]:
         ld = _pad(n)
         V = torch.randn((52, ld), dtype=torch.float64, device="cuda")
         z = torch.randn(ld, dtype=torch.float64, device="cuda")
         out = torch.empty(ld, dtype=torch.float64, device="cuda")
         sc = torch.zeros(200, dtype=torch.float64, device="cuda")
         c1, c2, nsq = sc[:64], sc[64:128], sc[128:129]
-        for k in (10, 25, 51):
+        for k in [int(v) for v in args.k.split(",")]:
             res = {}
             res["phase1"] = timed(lambda: _lib.call("pg_cgs2_phase1", ptr(V), ld, k, ptr(z), n,
                                                     ptr(c1), ws, st), args.reps)
