@@ -670,8 +670,12 @@ class Engine:
             return out
         if v.shape[0] != self.N:
             raise DimensionMismatchError("vector length does not match operator")
+        # a pinned host source is copied in stream order (every public entry
+        # point synchronises before it returns, so the caller's buffer is read
+        # before control goes back)
+        nb = (not v.is_cuda) and v.is_pinned()
         for s, t in zip(self.shards, out):
-            t[:s.n].copy_(v[s.r0:s.r1])
+            t[:s.n].copy_(v[s.r0:s.r1], non_blocking=nb)
         return out
 
     def to_host(self, xs) -> np.ndarray:
@@ -695,8 +699,15 @@ class Engine:
         """Result in the caller's vector type: CUDA tensor -> CUDA tensor, CPU
         tensor -> CPU tensor (one D2H copy), anything else -> numpy."""
         if isinstance(like, torch.Tensor):
-            out = self.to_torch(xs)
-            return out if like.is_cuda else out.cpu()
+            if like.is_cuda:
+                return self.to_torch(xs)
+            # straight into pinned memory (cached by torch's host allocator):
+            # one direct DMA, no device-side clone, no pageable staging
+            out = xs[0][:self.shards[0].n] if len(xs) == 1 else self.to_torch(xs)
+            host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+            host.copy_(out, non_blocking=True)
+            torch.cuda.current_stream(out.device).synchronize()
+            return host
         return self.to_host(xs)
 
     # ---- kernels ----------------------------------------------------------------
