@@ -118,8 +118,12 @@ struct __align__(16) PairEnt {
 };
 // Rows per block of the windowed dictionary SpMV and its window budget
 // (elements per buffer; two buffers per block).
+// 512 rows per ring stage (544-thread blocks, 2 per SM): the per-stage
+// mbarrier hand-offs and producer issue are amortised over twice the rows of
+// the earlier 256 (cfg4-160^3 windowed row-pattern pass 61.6 -> 57.1 us;
+// 128: 110, 384: 62.5, 768: 60.8 -- tools/spmv_bench.py over build variants)
 #ifndef PG_WIN_ROWS
-#define PG_WIN_ROWS 256
+#define PG_WIN_ROWS 512
 #endif
 constexpr int kWinRows = PG_WIN_ROWS;
 constexpr int kWinMaxGroups = 32;
@@ -128,7 +132,7 @@ constexpr int kWinMaxElems = 6144;
 // stages (2..kWinMaxStages) as fit kWinTargetBlocks blocks per SM.
 constexpr int kWinMaxStages = 8;
 #ifndef PG_WIN_TARGET_BLOCKS
-#define PG_WIN_TARGET_BLOCKS 4
+#define PG_WIN_TARGET_BLOCKS 2
 #endif
 constexpr int kWinTargetBlocks = PG_WIN_TARGET_BLOCKS;
 constexpr int kWinSmemBudget = 220 * 1024;

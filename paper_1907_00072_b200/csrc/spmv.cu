@@ -485,7 +485,7 @@ __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, 
 constexpr int kWinThreads = kWinRows + 32;
 
 #ifndef PG_WIN_MIN_BLOCKS
-#define PG_WIN_MIN_BLOCKS 4
+#define PG_WIN_MIN_BLOCKS 2
 #endif
 // PAT = true: row-pattern matrices (pair8 = rpat; pptr / pent / npat / nent
 // the pattern table, staged after the ring): a row is its pattern's entries,
