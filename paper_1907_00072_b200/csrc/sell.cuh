@@ -262,10 +262,13 @@ struct PatMaster {
 // block's shared-memory window (winrow = the row's slot); else global x
 // gathered at row + doff (masked-off entries are not loaded: they may lie
 // outside x).
-template <int LB, bool WIN, bool CG = false>
+// FULL: the caller established (warp-uniformly) that every row of the warp
+// is the whole master pattern -- no per-entry mask tests.
+template <int LB, bool WIN, bool CG = false, bool FULL = false>
 __device__ __forceinline__ double row_sum_master(uint32_t mask, const PatMaster& pm,
                                                  const unsigned char* winrow,
                                                  const double* __restrict__ xr) {
+  if (FULL) mask = 0xffffffffu;
   double acc = 0.0;
 #pragma unroll
   for (int c0 = 0; c0 < LB; c0 += 8) {
@@ -277,7 +280,7 @@ __device__ __forceinline__ double row_sum_master(uint32_t mask, const PatMaster&
         xv[q] = *reinterpret_cast<const double*>(winrow + pm.woff[c0 + q]);
       } else {
         xv[q] = 0.0;
-        if (mask & (1u << (c0 + q)))
+        if (FULL || (mask & (1u << (c0 + q))))
           xv[q] = CG ? __ldcg(xr + pm.doff[c0 + q]) : __ldg(xr + pm.doff[c0 + q]);
       }
     }
@@ -285,7 +288,7 @@ __device__ __forceinline__ double row_sum_master(uint32_t mask, const PatMaster&
     for (int q = 0; q < 8; ++q) {
       if (c0 + q >= LB) break;
       const double p = __dmul_rn(pm.v[c0 + q], xv[q]);
-      if (mask & (1u << (c0 + q))) acc = __dadd_rn(acc, p);
+      if (FULL || (mask & (1u << (c0 + q)))) acc = __dadd_rn(acc, p);
     }
   }
   return acc;

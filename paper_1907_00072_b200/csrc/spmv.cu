@@ -307,15 +307,21 @@ __global__ void __launch_bounds__(kSellThreads, PG_PAT_MIN_BLOCKS)
   __syncthreads();
   double local = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // nlanes is a multiple of 32: a warp's lanes run the same iterations, so
+  // the warp-uniform "all rows are the whole master" test below is safe
+  const uint32_t full = pm.len >= 32 ? 0xffffffffu : (1u << pm.len) - 1u;
   for (int64_t lane = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lane < a.nlanes;
        lane += stride) {
     const int64_t row = lane_row(a, lane);
+    const int pid = row >= 0 ? __ldg(rpat + lane) : 0;
+    const uint32_t mask = LB > 0 ? s_mask[pid] : (1u << 31);
+    const bool all_full = LB > 0 && __all_sync(0xffffffffu, row < 0 || mask == full);
     if (row < 0) continue;
-    const int pid = __ldg(rpat + lane);
     const Pre pre = epi_load<MODE>(e, x, row);
     double ax;
-    const uint32_t mask = LB > 0 ? s_mask[pid] : (1u << 31);
-    if (LB > 0 && !(mask >> 31))
+    if (all_full)
+      ax = row_sum_master<(LB > 0 ? LB : 8), false, false, true>(mask, pm, nullptr, x + row);
+    else if (LB > 0 && !(mask >> 31))
       ax = row_sum_master<(LB > 0 ? LB : 8), false>(mask, pm, nullptr, x + row);
     else
       ax = row_sum_pattern<false>(s_ptr[pid], s_ptr[pid + 1], row, x, s_ent);
@@ -575,14 +581,18 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
       }
       mbar_wait(&full[st], (uint32_t)((it / S) & 1));
       if (PAT) {
+        const int pid = live ? buf[wa.off_p8 + t] : 0;
+        const uint32_t mask = LB > 0 ? s_mask[pid] : (1u << 31);
+        const uint32_t full = pm.len >= 32 ? 0xffffffffu : (1u << pm.len) - 1u;
+        const bool all_full = LB > 0 && __all_sync(0xffffffffu, !live || mask == full);
         if (live) {
           if (A) pre.a = reinterpret_cast<const double*>(buf + wa.off_ea)[t];
           if (B) pre.b = reinterpret_cast<const double*>(buf + wa.off_eb)[t];
-          const int pid = buf[wa.off_p8 + t];
           const unsigned char* winrow = buf + 8 * t;
-          const uint32_t mask = LB > 0 ? s_mask[pid] : (1u << 31);
           double acc = 0.0;
-          if (LB > 0 && !(mask >> 31)) {
+          if (all_full) {
+            acc = row_sum_master<(LB > 0 ? LB : 8), true, false, true>(mask, pm, winrow, nullptr);
+          } else if (LB > 0 && !(mask >> 31)) {
             acc = row_sum_master<(LB > 0 ? LB : 8), true>(mask, pm, winrow, nullptr);
           } else {
             const int end = s_pptr[pid + 1];
