@@ -48,13 +48,13 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _traffic(kernel_key: str):
+def _traffic(kernel_key: str, workload: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
-    --set full capture (profiles/ncu_traffic.json), or None."""
+    --set full capture of this workload (profiles/ncu_traffic.json), or None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(kernel_key)
+            return json.load(fh).get("per_workload", {}).get(workload, {}).get(kernel_key)
     except Exception:
         return None
 
@@ -359,7 +359,7 @@ def run_ours(args):
                 "peak_source": peak_src,
                 "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None,
-                "traffic": _traffic("poly_pass_bytes_per_launch"),
+                "traffic": _traffic("poly_pass_bytes_per_launch", conf["name"]),
                 "launches_timed": nk,
                 "kernel_s_per_step": kt / args.steps,
                 "share_of_step": kt / total if total else None,

@@ -167,6 +167,8 @@ static void free_matrix(pg_matrix* m) {
   cudaFree(m->pat_ptr);
   cudaFree(m->pat_ent);
   cudaFree(m->pat_mask);
+  cudaFree(m->opat);
+  cudaFree(m->opat_mask);
   cudaSetDevice(cur);
   delete m;
 }
@@ -345,6 +347,71 @@ static void build_patterns(const SellHost& h, const std::vector<uint8_t>& p8,
   m->n_pat = (int)seqs.size();
   m->pat_nent = (int)ptr.back();
   m->pat_maxlen = maxlen;
+}
+
+// Row offset patterns: when the values do not compress (no row-pattern
+// dictionary) but every row's column-offset sequence is one of <= 256 --
+// a variable-coefficient stencil -- one byte per row names it, so the kernel
+// needs no column stream: the master offsets are constant-bank operands and
+// only the f64 values are streamed (8 instead of 12 B per entry).  Rows that
+// are not ordered subsequences of the master keep the SELL column stream.
+// PG_SPMV_OPAT=0 disables it.
+static void build_offset_patterns(const SellHost& h, const int32_t* col, pg_matrix* m) {
+  const char* env = std::getenv("PG_SPMV_OPAT");
+  if (env && std::atoi(env) == 0) return;
+  if (m->rpat || h.max_width > 31 || m->nrows == 0) return;
+  const int64_t nl = h.n_slices * PG_SLICE;
+  std::vector<uint8_t> opat(nl, 0);
+  std::unordered_map<std::string, int> ids;
+  std::vector<std::string> seqs;
+  std::vector<int64_t> count;
+  std::string key;
+  for (int64_t s = 0; s < h.n_slices; ++s) {
+    for (int t = 0; t < PG_SLICE; ++t) {
+      const int64_t lane = s * PG_SLICE + t;
+      const int32_t r = h.perm[lane];
+      key.clear();
+      const int len = r < 0 ? 0 : h.row_len[lane];
+      for (int j = 0; j < len; ++j) {
+        const int64_t o = (int64_t)col[h.slice_ptr[s] + (int64_t)j * PG_SLICE + t] - r;
+        if (o < INT32_MIN || o > INT32_MAX) return;
+        const int32_t o32 = (int32_t)o;
+        key.append(reinterpret_cast<const char*>(&o32), 4);
+      }
+      auto it = ids.find(key);
+      if (it == ids.end()) {
+        if (ids.size() == 256) return;
+        it = ids.emplace(key, (int)seqs.size()).first;
+        seqs.push_back(key);
+        count.push_back(0);
+      }
+      opat[lane] = (uint8_t)it->second;
+      if (r >= 0) ++count[it->second];
+    }
+  }
+  const size_t mp = (size_t)(std::max_element(count.begin(), count.end()) - count.begin());
+  const std::string& ms = seqs[mp];
+  const size_t ml = ms.size() / 4;
+  if (ml == 0 || ml > 31) return;
+  std::vector<uint32_t> mask(seqs.size(), 1u << 31);
+  for (size_t p = 0; p < seqs.size(); ++p) {
+    uint32_t bits = 0;
+    size_t q = 0;
+    for (size_t e = 0; e < seqs[p].size(); e += 4) {
+      while (q < ml && std::memcmp(ms.data() + 4 * q, seqs[p].data() + e, 4) != 0) ++q;
+      if (q == ml) {
+        bits = 1u << 31;
+        break;
+      }
+      bits |= 1u << q++;
+    }
+    mask[p] = bits;
+  }
+  m->opat = upload(opat.data(), opat.size(), m->bytes);
+  m->opat_mask = upload(mask.data(), mask.size(), m->bytes);
+  m->opat_n = (int)seqs.size();
+  m->opat_mlen = (int)ml;
+  for (size_t q = 0; q < ml; ++q) std::memcpy(&m->opat_mdoff[q], ms.data() + 4 * q, 4);
 }
 
 static void build_dictionaries(const SellHost& h, const int32_t* col, const double* val,
@@ -537,6 +604,7 @@ PG_API int pg_matrix_create(int device, int64_t nrows, int64_t ncols, const int6
       m->col = upload(col.data(), (size_t)h.padded, m->bytes);
       m->val = upload(val.data(), (size_t)h.padded, m->bytes);
       build_dictionaries(h, col.data(), val.data(), m);
+      if (!m->pair8 && !m->col8 && !m->val8) build_offset_patterns(h, col.data(), m);
     } catch (...) {
       free_matrix(m);
       throw;
@@ -565,6 +633,7 @@ PG_API int pg_matrix_stats(const pg_matrix* m, int64_t* s) {
     // the kernel launch_sell picks for 16-byte aligned vectors (spmv.cu)
     s[11] = pattern_kernel(m) ? 5
             : (m->pair8 && m->wtab && m->rpat && winpat_enabled()) ? 6
+            : opat_kernel(m) ? 7
             : m->pair8 ? (m->wtab ? 3 : (m->stride8 > 0 && m->stride8 <= 256) ? 4 : 2)
                        : (m->col8 || m->val8) ? 1 : 0;
     s[10] = m->pair8 ? 1 : (s[8] + s[9]);

@@ -99,6 +99,15 @@ struct pg_matrix {
   double pat_mv[32];
   int32_t pat_mdoff[32], pat_mwoff[32];
   uint32_t* pat_mask;
+  // row OFFSET patterns (abi.cu build_offset_patterns), for matrices whose
+  // values do not compress but whose column offsets col - row form <= 256
+  // distinct row sequences (variable-coefficient stencils, cfg5): opat = 1 B
+  // per SELL lane; the master offset sequence (<= 31) and per-pattern masks as
+  // for pat_*; the values stay in the f64 SELL stream (val)
+  uint8_t* opat;
+  uint32_t* opat_mask;
+  int opat_n, opat_mlen;
+  int32_t opat_mdoff[32];
   // row dependency pattern of the dependency-driven chain kernel (chain.cu):
   // the n_doff distinct column offsets col - row (n_doff <= 256, from the
   // dictionary), or n_doff = 0 and the band [dband_lo, dband_hi] of offsets
@@ -278,6 +287,8 @@ struct ChainStep {
 };
 // pg_spmv & co. run the row-pattern kernel on this matrix (spmv.cu).
 bool pattern_kernel(const pg_matrix* m);
+// pg_spmv & co. run the offset-pattern kernel on this matrix (spmv.cu).
+bool opat_kernel(const pg_matrix* m);
 // pg_spmv & co. on windowed matrices stage row patterns, not pair streams.
 bool winpat_enabled();
 // Matrix format the chain kernel handles (and PG_CHAIN != 0).

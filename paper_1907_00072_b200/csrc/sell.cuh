@@ -294,4 +294,41 @@ __device__ __forceinline__ double row_sum_master(uint32_t mask, const PatMaster&
   return acc;
 }
 
+// A row that is the master OFFSET pattern's entries `mask` (offset-pattern
+// format: values still streamed).  vals points at the row's stored entry 0 in
+// the SELL value stream (entry j at vals[32 j]); the j-th stored value pairs
+// with the j-th set bit of mask -- the row's own order, so the sum is the
+// sequential one.  FULL: the warp's rows are all the whole master (stored
+// entry q at a compile-time offset).
+template <int LB, bool FULL>
+__device__ __forceinline__ double row_sum_omaster(uint32_t mask, const PatMaster& pm,
+                                                  const double* __restrict__ vals,
+                                                  const double* __restrict__ xr) {
+  double acc = 0.0;
+  int j = 0;
+#pragma unroll
+  for (int c0 = 0; c0 < LB; c0 += 8) {
+    double v[8], xv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (c0 + q >= LB) break;
+      v[q] = xv[q] = 0.0;
+      if (FULL) {
+        v[q] = __ldcs(vals + PG_SLICE * (c0 + q));
+        xv[q] = __ldg(xr + pm.doff[c0 + q]);
+      } else if (mask & (1u << (c0 + q))) {
+        v[q] = __ldcs(vals + PG_SLICE * j);
+        ++j;
+        xv[q] = __ldg(xr + pm.doff[c0 + q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (c0 + q >= LB) break;
+      if (FULL || (mask & (1u << (c0 + q)))) acc = __dadd_rn(acc, __dmul_rn(v[q], xv[q]));
+    }
+  }
+  return acc;
+}
+
 }  // namespace pg

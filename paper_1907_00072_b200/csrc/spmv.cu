@@ -331,6 +331,53 @@ __global__ void __launch_bounds__(kSellThreads, PG_PAT_MIN_BLOCKS)
   finish_resid<MODE>(local, partials, counter, nsq);
 }
 
+// ------------------------------------------------------ offset patterns --
+// Variable-coefficient stencils (abi.cu build_offset_patterns): 1 B per row
+// names the row's column-offset sequence; masked subsequences of the master
+// read only their values (8 B per entry, coalesced) and gather x at the
+// master's constant offsets; other rows walk the SELL column stream.
+template <int MODE, int LB>
+__global__ void __launch_bounds__(kSellThreads, PG_PAT_MIN_BLOCKS)
+    sell_opat_kernel(SellArgs a, const uint8_t* __restrict__ opat,
+                     const uint32_t* __restrict__ omask, int npat, const PatMaster pm,
+                     const double* __restrict__ x, Epi e, double* partials,
+                     unsigned int* counter, double* nsq) {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  __shared__ uint32_t s_mask[256];
+  for (int i = threadIdx.x; i < npat; i += blockDim.x) s_mask[i] = omask[i];
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  __syncthreads();
+  double local = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint32_t full = pm.len >= 32 ? 0xffffffffu : (1u << pm.len) - 1u;
+  for (int64_t lane = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lane < a.nlanes;
+       lane += stride) {
+    const int64_t row = lane_row(a, lane);
+    const int pid = row >= 0 ? __ldg(opat + lane) : 0;
+    const uint32_t mask = s_mask[pid];
+    const bool all_full = __all_sync(0xffffffffu, row < 0 || mask == full);
+    if (row < 0) continue;
+    const int64_t s = lane >> 5;
+    const int64_t base = __ldg(a.slice_ptr + s) + (lane & 31);
+    const Pre pre = epi_load<MODE>(e, x, row);
+    double ax;
+    if (all_full) {
+      ax = row_sum_omaster<LB, true>(mask, pm, a.val + base, x + row);
+    } else if (!(mask >> 31)) {
+      ax = row_sum_omaster<LB, false>(mask, pm, a.val + base, x + row);
+    } else {
+      ax = row_sum(
+          [&](int j) { return __ldcs(a.col + base + (int64_t)j * PG_SLICE); },
+          [](int raw) { return raw; },
+          [&](int j) { return __ldcs(a.val + base + (int64_t)j * PG_SLICE); },
+          __ldg(a.slice_w + s), __ldg(a.row_len + lane), x);
+    }
+    const double r = epilogue<MODE>(e, pre, row, ax);
+    if (MODE == kResid) local = __fma_rn(r, r, local);
+  }
+  finish_resid<MODE>(local, partials, counter, nsq);
+}
+
 // ---------------------------------------------------- windowed dictionary --
 // Dictionary-compressed matrices in natural row order (stencils): a block
 // owns kWinRows consecutive rows (8 slices).  Their x reads all fall inside
@@ -686,6 +733,13 @@ static int lb_index(int lb) {
   return lb == 7 ? 1 : lb == 8 ? 2 : lb == 16 ? 3 : lb == 27 ? 4 : lb == 32 ? 5 : 0;
 }
 
+// Offset-pattern kernel (PG_SPMV_OPAT_KERNEL=0: the plain SELL kernel).
+bool opat_kernel(const pg_matrix* m) {
+  static int on = -1;
+  if (on < 0) on = env_or("PG_SPMV_OPAT_KERNEL", 1);
+  return on && m->opat && m->opat_mlen > 0 && m->opat_mlen <= 31;
+}
+
 // Windowed matrices with a row-pattern dictionary take the windowed kernel's
 // pattern variant (PG_SPMV_WINPAT=0: the pair-stream variant).
 bool winpat_enabled() {
@@ -816,6 +870,21 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
       launch_k(kern, (int)g, kWinThreads, smem, st, a, wa, (const uint8_t*)m->pair8,
                (const PairEnt*)m->ptab, x, e, part, cnt, nsq, (const int32_t*)nullptr, 0, 0,
                (const uint32_t*)nullptr, pm);
+  } else if (opat_kernel(m)) {
+    int64_t blocks = (a.nlanes + kSellThreads - 1) / kSellThreads;
+    static int per_sm = -1;
+    if (per_sm < 0) per_sm = env_or("PG_SPMV_PAT_BLOCKS_PER_SM", PG_PAT_MIN_BLOCKS);
+    const int64_t cap = (MODE == kResid) ? kMaxBlocks : (int64_t)sms[dev] * per_sm;
+    if (blocks > cap) blocks = cap;
+    PatMaster pm;
+    std::memset(&pm, 0, sizeof pm);
+    pm.len = m->opat_mlen;
+    for (int q = 0; q < pm.len; ++q) pm.doff[q] = m->opat_mdoff[q];
+    const int len = pm.len;
+    auto kern = len == 9 ? sell_opat_kernel<MODE, 9> : len <= 8 ? sell_opat_kernel<MODE, 8>
+              : len <= 16 ? sell_opat_kernel<MODE, 16> : sell_opat_kernel<MODE, 32>;
+    launch_k(kern, (int)blocks, kSellThreads, 0, st, a, (const uint8_t*)m->opat,
+             (const uint32_t*)m->opat_mask, m->opat_n, pm, x, e, part, cnt, nsq);
   } else if (m->pair8) {
     static int per_sm = -1;
     if (per_sm < 0) {

@@ -2,7 +2,7 @@
 
   python tools/ncu_summarize.py launches <launches.csv> <out.md>
       per-kernel share of one solve from the --metrics gpu__time_duration.sum pass
-  python tools/ncu_summarize.py full <report.ncu-rep> <out.md> [--traffic-json profiles/ncu_traffic.json]
+  python tools/ncu_summarize.py full <report.ncu-rep> <out.md> [--traffic-json profiles/ncu_traffic.json] [--workload NAME]
       key --set full metrics per captured launch; the DRAM bytes of the fused
       polynomial pass go to ncu_traffic.json (bench.py's roofline.traffic)
 """
@@ -63,7 +63,7 @@ def launches(path, out):
     print("\n".join(lines))
 
 
-def full(rep, out, traffic_json=None):
+def full(rep, out, traffic_json=None, workload=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -93,8 +93,12 @@ def full(rep, out, traffic_json=None):
         except Exception:
             pass
         if poly:
-            data["poly_pass_bytes_per_launch"] = sum(poly) / len(poly)
-            data["source"] = rep
+            if workload:  # per-workload entry (bench.py reads its own config's)
+                data.setdefault("per_workload", {})[workload] = {
+                    "poly_pass_bytes_per_launch": sum(poly) / len(poly), "source": rep}
+            else:
+                data["poly_pass_bytes_per_launch"] = sum(poly) / len(poly)
+                data["source"] = rep
         json.dump(data, open(traffic_json, "w"), indent=1)
 
 
@@ -104,4 +108,5 @@ if __name__ == "__main__":
         launches(sys.argv[2], sys.argv[3])
     else:
         tj = sys.argv[sys.argv.index("--traffic-json") + 1] if "--traffic-json" in sys.argv else None
-        full(sys.argv[2], sys.argv[3], tj)
+        wk = sys.argv[sys.argv.index("--workload") + 1] if "--workload" in sys.argv else None
+        full(sys.argv[2], sys.argv[3], tj, wk)
