@@ -90,7 +90,8 @@ PG_API int pg_matrix_destroy(pg_matrix* mat);
  *              that kernel (0 plain SELL, 1 two-stream dictionary, 2 pair
  *              dictionary with global gathers, 3 windowed pair TMA ring,
  *              4 pair dictionary, short uniform rows, 5 row-pattern
- *              dictionary (1 B per row), 6 windowed row patterns)} */
+ *              dictionary (1 B per row), 6 windowed row patterns, 7 offset
+ *              patterns (1 B per row + f64 values))} */
 PG_API int pg_matrix_stats(const pg_matrix* mat, int64_t* stats);
 
 /* ---- reduction workspace (one per stream) --------------------------------

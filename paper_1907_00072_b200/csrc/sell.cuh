@@ -263,7 +263,8 @@ struct PatMaster {
 // gathered at row + doff (masked-off entries are not loaded: they may lie
 // outside x).
 // FULL: the caller established (warp-uniformly) that every row of the warp
-// is the whole master pattern -- no per-entry mask tests.
+// is the whole master pattern and that LB == pm.len -- no per-entry mask
+// tests, every one of the LB entries added.
 template <int LB, bool WIN, bool CG = false, bool FULL = false>
 __device__ __forceinline__ double row_sum_master(uint32_t mask, const PatMaster& pm,
                                                  const unsigned char* winrow,
@@ -298,8 +299,8 @@ __device__ __forceinline__ double row_sum_master(uint32_t mask, const PatMaster&
 // format: values still streamed).  vals points at the row's stored entry 0 in
 // the SELL value stream (entry j at vals[32 j]); the j-th stored value pairs
 // with the j-th set bit of mask -- the row's own order, so the sum is the
-// sequential one.  FULL: the warp's rows are all the whole master (stored
-// entry q at a compile-time offset).
+// sequential one.  FULL: the warp's rows are all the whole master and
+// LB == pm.len (stored entry q at a compile-time offset).
 template <int LB, bool FULL>
 __device__ __forceinline__ double row_sum_omaster(uint32_t mask, const PatMaster& pm,
                                                   const double* __restrict__ vals,

@@ -315,7 +315,10 @@ __global__ void __launch_bounds__(kSellThreads, PG_PAT_MIN_BLOCKS)
     const int64_t row = lane_row(a, lane);
     const int pid = row >= 0 ? __ldg(rpat + lane) : 0;
     const uint32_t mask = LB > 0 ? s_mask[pid] : (1u << 31);
-    const bool all_full = LB > 0 && __all_sync(0xffffffffu, row < 0 || mask == full);
+    // FULL rows only for an exact-length instantiation: a bucket's inert tail
+    // entries must not be added
+    const bool all_full =
+        LB > 0 && pm.len == LB && __all_sync(0xffffffffu, row < 0 || mask == full);
     if (row < 0) continue;
     const Pre pre = epi_load<MODE>(e, x, row);
     double ax;
@@ -355,7 +358,8 @@ __global__ void __launch_bounds__(kSellThreads, PG_PAT_MIN_BLOCKS)
     const int64_t row = lane_row(a, lane);
     const int pid = row >= 0 ? __ldg(opat + lane) : 0;
     const uint32_t mask = s_mask[pid];
-    const bool all_full = __all_sync(0xffffffffu, row < 0 || mask == full);
+    // FULL rows only for an exact-length instantiation (see sell_pat_kernel)
+    const bool all_full = pm.len == LB && __all_sync(0xffffffffu, row < 0 || mask == full);
     if (row < 0) continue;
     const int64_t s = lane >> 5;
     const int64_t base = __ldg(a.slice_ptr + s) + (lane & 31);
@@ -631,7 +635,8 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
         const int pid = live ? buf[wa.off_p8 + t] : 0;
         const uint32_t mask = LB > 0 ? s_mask[pid] : (1u << 31);
         const uint32_t full = pm.len >= 32 ? 0xffffffffu : (1u << pm.len) - 1u;
-        const bool all_full = LB > 0 && __all_sync(0xffffffffu, !live || mask == full);
+        const bool all_full =
+            LB > 0 && pm.len == LB && __all_sync(0xffffffffu, !live || mask == full);
         if (live) {
           if (A) pre.a = reinterpret_cast<const double*>(buf + wa.off_ea)[t];
           if (B) pre.b = reinterpret_cast<const double*>(buf + wa.off_eb)[t];

@@ -157,6 +157,57 @@ def test_pattern_master_and_table_paths_bitwise():
         op.close()
 
 
+@pytest.mark.parametrize("grid", [5, 17, 64, 101])
+def test_offset_pattern_kernel_bitwise(grid):
+    """Variable-coefficient stencils (cfg5's 9-point recirculating-wind
+    operator): values do not compress, the column offsets do -- the offset-
+    pattern kernel (1 B per row + f64 values; master path, masked boundary
+    rows) gives the oracle's SpMV, p(A)v and residual bit for bit."""
+    from oracle import pgmres_oracle as orc
+    h = wl.convdiff2d_9pt(grid)
+    op = pg.DeviceMatrixOperator(h, sigma=1)
+    # tiny grids have <= 256 distinct values: the (value) row-pattern format
+    many = len(np.unique(np.asarray(h.values))) > 256
+    assert op.engine.shards[0].stats["kernel"] == (7 if many else 5)
+    O = orc.OracleMatrix.of(h)
+    x = wl.splitmix_uniform(7, h.nrows)
+    assert np.array_equal(op.apply(x), O.matvec(x))
+    y = np.random.default_rng(2).uniform(-1, 1, 5)
+    got = pg.apply_poly(pg.PolyCoefficients(4, y, 1.0), op, x, pg.CostCounters())
+    assert np.array_equal(got, orc.poly_eval(y, O, x, orc.Tally()))
+    e = op.engine
+    b = wl.splitmix_uniform(8, h.nrows)
+    rs = e.vecs()
+    e.residual(e.ingest(x), e.ingest(b), rs)
+    assert np.array_equal(e.to_host(rs), b - O.matvec(x))
+    op.close()
+
+
+def test_pattern_kernels_bucketed_master_with_nonfinite_x():
+    """Masters shorter than their unroll bucket (5-point rows in the 8-entry
+    bucket, both pattern formats): the bucket's inert tail entries are never
+    added -- a non-finite x entry in a row's own slot must not leak into
+    rows that do not reference it, and finite results stay bitwise."""
+    from oracle import pgmres_oracle as orc
+    h = wl.laplacian2d(48)
+    rp, ci = np.asarray(h.row_ptr), np.asarray(h.col_idx)
+    for vals in (np.asarray(h.values, dtype=np.float64),
+                 np.random.default_rng(1).uniform(-1, 1, len(ci))):
+        m = wl.CsrHost(h.nrows, h.ncols, rp, ci, vals)
+        op = pg.DeviceMatrixOperator(m, sigma=1)
+        O = orc.OracleMatrix.of(m)
+        x = wl.splitmix_uniform(4, m.nrows)
+        assert np.array_equal(op.apply(x), O.matvec(x))
+        x[100] = np.inf
+        with np.errstate(invalid="ignore"):
+            want = O.matvec(x)
+        got = op.apply(x)
+        assert np.array_equal(np.isnan(got), np.isnan(want))
+        fin = np.isfinite(want)
+        assert np.array_equal(got[fin], want[fin])
+        op.close()
+
+
 def test_chain_full_cfg2_size(monkeypatch):
     """n = 1e6, degree 14 (the headline's effective degree): a few Arnoldi
     steps through the chain kernel equal the pass-by-pass path bit for bit."""
