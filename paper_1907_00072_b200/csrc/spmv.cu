@@ -37,11 +37,56 @@ namespace pg {
 
 // Sequential row sum over the row's entries.  cp(j) loads the raw column
 // entry j (an int32 column, or a 1-byte dictionary index), dec(raw) turns it
-// into a column, vp(j) loads value j.
+// into a column, vp(j) loads value j.  Software-pipelined one chunk ahead:
+// chunk j+1's index / value loads (bounded by the uniform slice width) are
+// issued before chunk j's gathers (bounded by this row's length), so a chunk
+// costs one gather round trip instead of an index round trip followed by a
+// gather round trip.  PG_SELL_PIPE=0 restores the unpipelined loop.
+#ifndef PG_SELL_PIPE
+#define PG_SELL_PIPE 1
+#endif
 template <class ColPtr, class Dec, class ValPtr>
 __device__ __forceinline__ double row_sum(ColPtr cp, Dec dec, ValPtr vp, int w, int len,
                                           const double* __restrict__ x) {
   double acc = 0.0;
+#if PG_SELL_PIPE
+  {
+    int c[kUnroll];
+    double v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      c[u] = 0;
+      v[u] = 0.0;
+      if (u < w) {
+        c[u] = cp(u);
+        v[u] = vp(u);
+      }
+    }
+    for (int j = 0; j < w; j += kUnroll) {
+      int cn[kUnroll];
+      double vn[kUnroll], xv[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        cn[u] = 0;
+        vn[u] = 0.0;
+        if (j + kUnroll + u < w) {
+          cn[u] = cp(j + kUnroll + u);
+          vn[u] = vp(j + kUnroll + u);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) xv[u] = (j + u < len) ? __ldg(x + dec(c[u])) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (j + u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        c[u] = cn[u];
+        v[u] = vn[u];
+      }
+    }
+  }
+#else
   for (int j = 0; j < w; j += kUnroll) {
     double v[kUnroll], xv[kUnroll];
     int c[kUnroll];
@@ -63,6 +108,7 @@ __device__ __forceinline__ double row_sum(ColPtr cp, Dec dec, ValPtr vp, int w, 
     for (int u = 0; u < kUnroll; ++u)
       if (j + u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
   }
+#endif
   return acc;
 }
 
