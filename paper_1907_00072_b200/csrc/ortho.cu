@@ -22,8 +22,15 @@
 
 namespace pg {
 
+// Tile heights: 128 rows, or 256 for narrower bases (tile_rows_for): at
+// n = 1e6, k = 25 phase 1 48.5 -> 43.2 us and phase 2 57.1 -> 51.0 with 256;
+// at k >= 40 the taller tiles' shallower rings lose (72.8 vs 64.8 us).
 constexpr int kTileRows = 128;
-constexpr int kTileStride = kTileRows + 2;  // 16-B aligned column stride (doubles)
+template <int TR>
+struct TileShape {
+  static constexpr int kStride = TR + 2;  // 16-B aligned column stride (doubles)
+};
+constexpr int kTileStride = TileShape<kTileRows>::kStride;
 constexpr int kTileThreads = 256;
 constexpr int kWarps = kTileThreads / 32;
 constexpr int kColsPerWarp = (PG_KMAX + kWarps - 1) / kWarps;               // 8
@@ -48,30 +55,32 @@ __device__ __forceinline__ void cp_async_wait() {
 // 1 KB column segment, the column's address computed once per column; full
 // tiles need no per-piece bounds (ncu: the tile kernels were issue-bound,
 // 57% issue-active, largely on the per-piece address arithmetic).
+template <int TR>
 __device__ __forceinline__ void stage_tile(double* buf, const double* __restrict__ V, int64_t ld,
                                            int k, const double* __restrict__ z, int64_t n,
                                            int64_t tile) {
+  constexpr int kStride = TileShape<TR>::kStride;
   const int ncol = z ? k + 1 : k;
-  const int64_t row0 = tile * kTileRows;
-  const int64_t rows = min((int64_t)kTileRows, n - row0);
+  const int64_t row0 = tile * TR;
+  const int64_t rows = min((int64_t)TR, n - row0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (rows == kTileRows) {
+  if (rows == TR) {
     for (int colx = warp; colx < ncol; colx += kTileThreads / 32) {
       const double* src = (colx < k ? V + (int64_t)colx * ld : z) + row0 + 2 * lane;
-      double* dst = buf + colx * kTileStride + 2 * lane;
-      cp_async16(dst, src, 16);
-      cp_async16(dst + 64, src + 64, 16);
+      double* dst = buf + colx * kStride + 2 * lane;
+#pragma unroll
+      for (int h = 0; h < TR / 64; ++h) cp_async16(dst + 64 * h, src + 64 * h, 16);
     }
     return;
   }
-  constexpr int kChunks = kTileRows / 2;
+  constexpr int kChunks = TR / 2;
   for (int c = threadIdx.x; c < ncol * kChunks; c += kTileThreads) {
     const int colx = c / kChunks, ch = c - colx * kChunks;
     const double* src = (colx < k ? V + (int64_t)colx * ld : z) + row0 + 2 * ch;
     const int64_t valid = rows - 2 * ch;
     int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
     if (bytes == 0) src = V ? V : z;  // not dereferenced; keep the address legal
-    cp_async16(buf + colx * kTileStride + 2 * ch, src, bytes);
+    cp_async16(buf + colx * kStride + 2 * ch, src, bytes);
   }
 }
 
@@ -104,24 +113,25 @@ __device__ __forceinline__ double row_proj(int k, const double* c, Load load) {
   return t;
 }
 
-template <int MODE, int STAGES>
+template <int MODE, int STAGES, int TR>
 __global__ void __launch_bounds__(kTileThreads)
     tile_kernel(const double* __restrict__ V, int64_t ld, int k, const double* __restrict__ z,
                 int64_t n, const double* __restrict__ c1, double* partials,
                 unsigned int* counter, double* out) {
   pdl_entry();
+  constexpr int kStr = TileShape<TR>::kStride;
   extern __shared__ __align__(16) double smem[];
   __shared__ double c1s[PG_KMAX];
   const bool has_z = (MODE != kGram);
   const int ncol = has_z ? k + 1 : k;
-  const int buf_elems = ncol * kTileStride;
+  const int buf_elems = ncol * kStr;
   double* w1s = smem + STAGES * buf_elems;  // kUpdDots only
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   if (MODE == kUpdDots)
     for (int i = threadIdx.x; i < k; i += kTileThreads) c1s[i] = c1[i];
 
-  const int64_t ntiles = (n + kTileRows - 1) / kTileRows;
+  const int64_t ntiles = (n + TR - 1) / TR;
   int64_t tile = blockIdx.x;
 
   // per-thread accumulators
@@ -153,7 +163,7 @@ __global__ void __launch_bounds__(kTileThreads)
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     const int64_t t = tile + (int64_t)s * gridDim.x;
-    if (t < ntiles) stage_tile(smem + s * buf_elems, V, ld, k, has_z ? z : nullptr, n, t);
+    if (t < ntiles) stage_tile<TR>(smem + s * buf_elems, V, ld, k, has_z ? z : nullptr, n, t);
     cp_async_commit();
   }
   int it = 0;
@@ -165,19 +175,19 @@ __global__ void __launch_bounds__(kTileThreads)
       // overlaps this tile's compute even with a 2-deep ring
       const int64_t t = tile + (int64_t)(STAGES - 1) * gridDim.x;
       if (t < ntiles)
-        stage_tile(smem + ((it + STAGES - 1) % STAGES) * buf_elems, V, ld, k,
+        stage_tile<TR>(smem + ((it + STAGES - 1) % STAGES) * buf_elems, V, ld, k,
                    has_z ? z : nullptr, n, t);
       cp_async_commit();
     }
     const double* S = smem + (it % STAGES) * buf_elems;
 
     if (MODE == kDots || MODE == kUpdDots) {
-      const double* vec = S + k * kTileStride;  // z column
+      const double* vec = S + k * kStr;  // z column
       if (MODE == kUpdDots) {
-        if (threadIdx.x < kTileRows) {
+        if (threadIdx.x < TR) {
           const int r = threadIdx.x;
-          const double t = row_proj(k, c1s, [&](int i) { return S[i * kTileStride + r]; });
-          w1s[r] = __dsub_rn(S[k * kTileStride + r], t);
+          const double t = row_proj(k, c1s, [&](int i) { return S[i * kStr + r]; });
+          w1s[r] = __dsub_rn(S[k * kStr + r], t);
         }
         __syncthreads();
         vec = w1s;
@@ -186,9 +196,9 @@ __global__ void __launch_bounds__(kTileThreads)
       for (int m = 0; m < kColsPerWarp; ++m) {
         const int i = warp + m * kWarps;
         if (i < k) {
-          const double* col = S + i * kTileStride;
+          const double* col = S + i * kStr;
 #pragma unroll
-          for (int q = 0; q < kTileRows / 32; ++q)
+          for (int q = 0; q < TR / 32; ++q)
             acc[m] = __fma_rn(col[lane + 32 * q], vec[lane + 32 * q], acc[m]);
         }
       }
@@ -196,11 +206,11 @@ __global__ void __launch_bounds__(kTileThreads)
 #pragma unroll
       for (int m = 0; m < kPairsPerThread; ++m) {
         if (pi[m] >= 0) {
-          const double* a = S + pi[m] * kTileStride;
-          const double* b = S + pj[m] * kTileStride;
+          const double* a = S + pi[m] * kStr;
+          const double* b = S + pj[m] * kStr;
           double hi = acc[m], lo = acc_lo[m];
 #pragma unroll 4
-          for (int r = 0; r < kTileRows; ++r) dd_fma(a[r], b[r], hi, lo);
+          for (int r = 0; r < TR; ++r) dd_fma(a[r], b[r], hi, lo);
           acc[m] = hi;
           acc_lo[m] = lo;
         }
@@ -580,11 +590,30 @@ static void check_tall(const double* V, int64_t ld, int k, int64_t n, int kmin) 
 // c1s / reduction arrays)
 constexpr size_t kTileSmemMax = 224 * 1024;
 
-static size_t tile_smem(int mode, int k, int stages) {
+static size_t tile_smem(int mode, int k, int stages, int tr = kTileRows) {
   const int ncol = (mode == kGram) ? k : k + 1;
-  size_t b = sizeof(double) * (size_t)stages * ncol * kTileStride;
-  if (mode == kUpdDots) b += sizeof(double) * kTileRows;
+  size_t b = sizeof(double) * (size_t)stages * ncol * (tr + 2);
+  if (mode == kUpdDots) b += sizeof(double) * tr;
   return b;
+}
+
+// Tile height per phase and basis width (see TileShape): 256 rows up to
+// k = 32 at n <= 2M and k = 25 beyond (phase 2 only at n <= 2M), where they
+// measured faster; 128 otherwise and for the Gram (n = 8M, k = 32: phase 1
+// 411 us with 256-row tiles vs ~340 with 128).  PG_TILE_ROWS = 128 / 256
+// forces one.
+static int tile_rows_for(int mode, int k, int64_t n) {
+  static int force = -1;
+  if (force < 0) {
+    const char* e = std::getenv("PG_TILE_ROWS");
+    force = e ? std::atoi(e) : 0;
+  }
+  if (mode == kGram) return 128;
+  if (force == 128 || force == 256) return force;
+  const bool small = n <= (int64_t)2000000;
+  if (k > 32 || (!small && k > 25)) return 128;
+  if (mode == kUpdDots && !small) return 128;
+  return 256;
 }
 
 // Ring depth: the deepest ring (<= 4 stages) that still lets `ctas` CTAs
@@ -599,7 +628,7 @@ static size_t tile_smem(int mode, int k, int stages) {
 //    co-resident CTAs hide it -- 4 up to k = 20, 3 up to k = 35, then 3 at
 //    n <= 2M and 2 at 8M (k = 51: 672 vs 871 us with ctas = 1);
 //  * the Gram keeps one deep ring (FP64-bound, insensitive).
-static int tile_stages(int mode, int k, int64_t n) {
+static int tile_stages(int mode, int k, int64_t n, int tr) {
   // PG_TILE_CTAS_P{1,2,3}: CTAs per SM the ring is sized for (experiments)
   static int ctas_env[4] = {-1, -1, -1, -1};
   if (ctas_env[mode] < 0) {
@@ -618,7 +647,7 @@ static int tile_stages(int mode, int k, int64_t n) {
   if (ctas_env[mode] > 0) ctas = ctas_env[mode];
   const size_t per_sm = kTileSmemMax / ctas;
   for (int s = 4; s > 2; --s)
-    if (tile_smem(mode, k, s) <= per_sm) return s;
+    if (tile_smem(mode, k, s, tr) <= per_sm) return s;
   return 2;
 }
 
@@ -663,6 +692,19 @@ static void launch_chunk_dots(const double* V, int64_t ld, int k, const double* 
   check_launch();
 }
 
+template <int MODE, int TR>
+static void set_tile_attrs(int dev) {
+  static bool done[64] = {};
+  if (done[dev]) return;
+  PG_CUDA(cudaFuncSetAttribute(tile_kernel<MODE, 4, TR>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemMax));
+  PG_CUDA(cudaFuncSetAttribute(tile_kernel<MODE, 3, TR>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemMax));
+  PG_CUDA(cudaFuncSetAttribute(tile_kernel<MODE, 2, TR>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemMax));
+  done[dev] = true;
+}
+
 template <int MODE>
 static void launch_tile(const double* V, int64_t ld, int k, const double* z, int64_t n,
                         const double* c1, double* out, pg_workspace* ws, cudaStream_t st) {
@@ -670,46 +712,51 @@ static void launch_tile(const double* V, int64_t ld, int k, const double* z, int
   PG_REQUIRE(ld % 2 == 0, PG_ERR_PARAMETER, "leading dimension must be even");
   PG_REQUIRE(((uintptr_t)V & 15) == 0 && (!z || ((uintptr_t)z & 15) == 0), PG_ERR_PARAMETER,
              "tile operands must be 16-byte aligned");
-  const int stages = tile_stages(MODE, k, n);
-  const size_t smem = tile_smem(MODE, k, stages);
+  const int tr = tile_rows_for(MODE, k, n);
+  const int stages = tile_stages(MODE, k, n, tr);
+  const size_t smem = tile_smem(MODE, k, stages, tr);
   const int dev = ws->device;
   PG_REQUIRE(dev >= 0 && dev < 64, PG_ERR_PARAMETER, "device ordinal out of range");
-  const void* kern = stages == 4 ? (const void*)tile_kernel<MODE, 4>
-                     : stages == 3 ? (const void*)tile_kernel<MODE, 3>
-                                   : (const void*)tile_kernel<MODE, 2>;
-  static bool attr_set[4][64] = {};
-  static int grid_cache[4][PG_KMAX + 1][64] = {};
-  static int grid_stages[4][PG_KMAX + 1][64] = {};
-  if (!attr_set[MODE][dev]) {
-    PG_CUDA(cudaFuncSetAttribute(tile_kernel<MODE, 4>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemMax));
-    PG_CUDA(cudaFuncSetAttribute(tile_kernel<MODE, 3>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemMax));
-    PG_CUDA(cudaFuncSetAttribute(tile_kernel<MODE, 2>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemMax));
-    attr_set[MODE][dev] = true;
-  }
-  const int64_t ntiles = (n + kTileRows - 1) / kTileRows;
+  if (tr == 256)
+    set_tile_attrs<MODE, 256>(dev);
+  else
+    set_tile_attrs<MODE, 128>(dev);
+  const void* kern =
+      tr == 256 ? (stages == 4   ? (const void*)tile_kernel<MODE, 4, 256>
+                   : stages == 3 ? (const void*)tile_kernel<MODE, 3, 256>
+                                 : (const void*)tile_kernel<MODE, 2, 256>)
+                : (stages == 4   ? (const void*)tile_kernel<MODE, 4, 128>
+                   : stages == 3 ? (const void*)tile_kernel<MODE, 3, 128>
+                                 : (const void*)tile_kernel<MODE, 2, 128>);
+  const int64_t ntiles = (n + tr - 1) / tr;
   if (ntiles == 0) {
     PG_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * (MODE == kGram ? 2 * k * k : k), st));
     return;
   }
-  int g = grid_cache[MODE][k][dev];
-  if (g == 0 || grid_stages[MODE][k][dev] != stages) {
+  // resident grid per (kernel, device), recomputed when the ring changes
+  static int grid_cache[2][PG_KMAX + 1][64] = {};
+  static int grid_key[2][PG_KMAX + 1][64] = {};
+  const int ti = tr == 256 ? 1 : 0;
+  int g = grid_cache[ti][k][dev];
+  if (g == 0 || grid_key[ti][k][dev] != stages) {
     g = grid_for(dev, kern, kTileThreads, smem, int64_t(1) << 40);
-    grid_cache[MODE][k][dev] = g;
-    grid_stages[MODE][k][dev] = stages;
+    grid_cache[ti][k][dev] = g;
+    grid_key[ti][k][dev] = stages;
   }
   if (ntiles < g) g = (int)ntiles;
-  if (stages == 4)
-    launch_k(tile_kernel<MODE, 4>, g, kTileThreads, smem, st, V, ld, k, z, n, c1, ws->partials,
-                                                        ws->counter, out);
-  else if (stages == 3)
-    launch_k(tile_kernel<MODE, 3>, g, kTileThreads, smem, st, V, ld, k, z, n, c1, ws->partials,
-                                                        ws->counter, out);
-  else
-    launch_k(tile_kernel<MODE, 2>, g, kTileThreads, smem, st, V, ld, k, z, n, c1, ws->partials,
-                                                        ws->counter, out);
+#define PG_TILE_LAUNCH(S, R)                                                                 \
+  launch_k(tile_kernel<MODE, S, R>, g, kTileThreads, smem, st, V, ld, k, z, n, c1,          \
+           ws->partials, ws->counter, out)
+  if (tr == 256) {
+    if (stages == 4) PG_TILE_LAUNCH(4, 256);
+    else if (stages == 3) PG_TILE_LAUNCH(3, 256);
+    else PG_TILE_LAUNCH(2, 256);
+  } else {
+    if (stages == 4) PG_TILE_LAUNCH(4, 128);
+    else if (stages == 3) PG_TILE_LAUNCH(3, 128);
+    else PG_TILE_LAUNCH(2, 128);
+  }
+#undef PG_TILE_LAUNCH
   check_launch();
 }
 
