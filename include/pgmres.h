@@ -189,6 +189,12 @@ PG_API int pg_ilu_apply(pg_ilu* ilu, const double* d_v, double* d_y, double* d_z
  *   narrow dependency pattern, PG_CHAIN != 0). */
 typedef struct pg_event pg_event;
 PG_API int pg_chain_fused(const pg_matrix* mat, int* fused);
+/* pg_power_sequence: P[:, k] = A P[:, k-1] for k = 1 .. ncols-1 (the power
+ * sequence of _power_sequence, polyprec.py:96-112; column 0 holds the unit
+ * seed), columns ld apart; one native call, the pg_spmv kernels back to back.
+ * Single-shard operators (no halo between the products). */
+PG_API int pg_power_sequence(const pg_matrix* mat, double* d_P, int64_t ld, int ncols,
+                             void* stream);
 /* pg_wrapped_apply: z = A p(A) x, t = p(A) x (PolynomialWrappedOperator.apply,
  * gmres.py:98-113) for d >= 1: the d monomial passes + the wrapper SpMV, as
  * one chain kernel when pg_chain_fused, else pass by pass; acc, w0, w1 are

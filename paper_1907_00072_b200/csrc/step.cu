@@ -147,6 +147,16 @@ PG_API int pg_wrapped_apply(const pg_matrix* mat, const double* y, int d, const 
   });
 }
 
+PG_API int pg_power_sequence(const pg_matrix* mat, double* d_P, int64_t ld, int ncols,
+                             void* stream) {
+  return guard([&] {
+    PG_REQUIRE(mat && d_P && ncols >= 1 && ld >= mat->ncols, PG_ERR_PARAMETER,
+               "bad power-sequence arguments");
+    for (int k = 1; k < ncols; ++k)
+      ok(pg_spmv(mat, d_P + (int64_t)(k - 1) * ld, d_P + (int64_t)k * ld, stream));
+  });
+}
+
 PG_API int pg_poly_chain(const pg_matrix* mat, const double* y, int d, const double* d_x,
                          const double* d_base, double* d_out, double* d_acc, double* d_w0,
                          double* d_w1, pg_event* ev_start, pg_event* ev_end, void* stream) {

@@ -731,6 +731,18 @@ class Engine:
         for s, x, y in zip(self._each(), xs, ys):
             _lib.call("pg_spmv", s.mat, ptr(x), ptr(y), s.stream)
 
+    def power_sequence(self, P, ncols: int):
+        """P[:, k] = A P[:, k-1] for k = 1 .. ncols-1 (column 0 given): one
+        native call on single-shard engines, operator applications otherwise
+        (halo before each product; M^{-1} A on ILU engines)."""
+        if self.fast_steps:
+            s = self.shards[0]
+            _lib.call("pg_power_sequence", s.mat, ptr(P[0]), s.ld, ncols, s.stream)
+            _lib.add_launches("pg_power_sequence", ncols - 1)
+            return
+        for k in range(ncols - 1):
+            self.spmv([blk[k] for blk in P], [blk[k + 1] for blk in P])
+
     def poly(self, y, vs, out, acc, w0, w1, base=None):
         """out = (base +) p(A) v with p = sum_k y_k A^k (polyprec.py:193-212);
         d = len(y)-1 fused SpMV passes.  acc, w0, w1: scratch shard vectors."""

@@ -113,9 +113,8 @@ def _device_power_gram(op, v0, top: int, counters: CostCounters):
     P = e.cached_blocks("powers", top + 1)
     # column 0 = v0 / |v0| (exact division, as numpy's v0 / seed_norm)
     e.normalize_dev(vs, e.slot(6), [blk[0] for blk in P])
-    for k in range(top):
-        e.count_ops(op.counters, 1)
-        e.spmv([blk[k] for blk in P], [blk[k + 1] for blk in P])
+    e.power_sequence(P, top + 1)
+    e.count_ops(op.counters, top)
     G = e.gram(P, top + 1)
     seed_norm = float(np.sqrt(e.read_slot(6)))
     if seed_norm == 0.0:
