@@ -72,6 +72,18 @@ PG_API int pg_sell_fill(int64_t nrows, int64_t ncols, const int64_t* row_ptr,
                         int64_t* slice_ptr, int32_t* slice_w, int32_t* row_len,
                         int32_t* perm, int32_t* col, double* val);
 
+/* ---- host-side row-pattern plan (no GPU needed; used by tests) ------------
+ * The grouping behind the row-pattern and offset-pattern formats, on CSR rows
+ * in natural order: rows with identical (column offset[, value bits])
+ * sequences share an id (first-seen order); the most frequent sequence is the
+ * master; masks[p] = bit set of master positions pattern p uses in order when
+ * it is an ordered subsequence of the master (bit 31 set otherwise; all bit
+ * 31 when the master is longer than 31).  *npat = -1 (no plan) when there are
+ * more than 256 distinct rows.  ids[nrows], masks[256] may be NULL. */
+PG_API int pg_row_patterns(int64_t nrows, const int64_t* row_ptr, const int64_t* col_idx,
+                           const double* values, int with_values, uint8_t* ids, int* npat,
+                           int* master, int* master_len, uint32_t* masks);
+
 /* ---- device operator ------------------------------------------------------
  * Replaces MatrixOperator(matrix) (gmres.py:46-60) / CsrMatrix storage.
  * Host CSR in (int64 row_ptr[nrows+1], int64 col_idx[nnz] in

@@ -70,6 +70,8 @@ _SIGNATURES = {
     "pg_event_wait": ([_p], C.c_int),
     "pg_event_elapsed": ([_p, _p, C.POINTER(C.c_float)], C.c_int),
     "pg_chain_fused": ([_p, C.POINTER(_i32)], C.c_int),
+    "pg_row_patterns": ([_i64, _p, _p, _p, _i32, _p, C.POINTER(_i32), C.POINTER(_i32),
+                         C.POINTER(_i32), _p], C.c_int),
     "pg_power_sequence": ([_p, _p, _i64, _i32, _p], C.c_int),
     "pg_wrapped_apply": ([_p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p], C.c_int),
     "pg_poly_chain": ([_p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p], C.c_int),

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <unordered_map>
 #include <cstring>
+#include <functional>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -270,6 +271,60 @@ static std::vector<int32_t> build_window_plan(const std::vector<int64_t>& offs,
 // pair stream; none when there are more than 256 patterns, a pattern longer
 // than kPatMaxLen or more than kPatMaxEnt table entries.  PG_SPMV_PAT=0
 // disables it.
+// Row-pattern planning shared by the value-pattern and offset-pattern
+// formats (and pg_row_patterns): every lane's row is a sequence of
+// fixed-size symbols (sym bytes; a pair index, or a column offset); rows are
+// grouped by identical sequence (at most 256), the most frequent sequence is
+// the master, and every sequence that is an ordered subsequence of the master
+// gets the bit set of master positions it uses (bit 31 set otherwise).
+struct PatternPlan {
+  std::vector<uint8_t> id;        // per lane
+  std::vector<std::string> seqs;  // distinct sequences, first-seen order
+  std::vector<int64_t> count;     // live lanes per sequence
+  size_t master = 0;
+  std::vector<uint32_t> mask;     // per sequence
+};
+
+template <class KeyFn>
+static bool plan_patterns(int64_t nl, size_t sym, KeyFn key, PatternPlan& P) {
+  P.id.assign(std::max<int64_t>(nl, 1), 0);
+  std::unordered_map<std::string, int> ids;
+  std::string k;
+  for (int64_t lane = 0; lane < nl; ++lane) {
+    k.clear();
+    const bool live = key(lane, k);
+    auto it = ids.find(k);
+    if (it == ids.end()) {
+      if (ids.size() == 256) return false;
+      it = ids.emplace(k, (int)P.seqs.size()).first;
+      P.seqs.push_back(k);
+      P.count.push_back(0);
+    }
+    P.id[lane] = (uint8_t)it->second;
+    if (live) ++P.count[it->second];
+  }
+  if (P.seqs.empty()) return false;
+  P.master = (size_t)(std::max_element(P.count.begin(), P.count.end()) - P.count.begin());
+  const std::string& ms = P.seqs[P.master];
+  const size_t ml = ms.size() / sym;
+  P.mask.assign(P.seqs.size(), 1u << 31);
+  if (ml > 31) return true;
+  for (size_t p = 0; p < P.seqs.size(); ++p) {
+    uint32_t bits = 0;
+    size_t q = 0;
+    for (size_t e = 0; e < P.seqs[p].size(); e += sym) {
+      while (q < ml && std::memcmp(ms.data() + sym * q, P.seqs[p].data() + e, sym) != 0) ++q;
+      if (q == ml) {
+        bits = 1u << 31;
+        break;
+      }
+      bits |= 1u << q++;
+    }
+    P.mask[p] = bits;
+  }
+  return true;
+}
+
 static void build_patterns(const SellHost& h, const std::vector<uint8_t>& p8,
                            const std::vector<int64_t>& sp8, const std::vector<PairEnt>& ptab,
                            pg_matrix* m) {
@@ -277,26 +332,17 @@ static void build_patterns(const SellHost& h, const std::vector<uint8_t>& p8,
   if (env && std::atoi(env) == 0) return;
   if (h.max_width > kPatMaxLen) return;
   const int64_t nl = h.n_slices * PG_SLICE;
-  std::vector<uint8_t> rpat(std::max<int64_t>(nl, 1), 0);
-  std::unordered_map<std::string, int> ids;
-  std::vector<std::string> seqs;
-  std::string key;
-  for (int64_t s = 0; s < h.n_slices; ++s) {
-    for (int t = 0; t < PG_SLICE; ++t) {
-      const int64_t lane = s * PG_SLICE + t;
-      key.clear();
-      const int len = h.perm[lane] < 0 ? 0 : h.row_len[lane];
-      for (int j = 0; j < len; ++j)
-        key.push_back((char)p8[(size_t)sp8[s] + (size_t)(j / 4) * 128 + 4 * t + (j & 3)]);
-      auto it = ids.find(key);
-      if (it == ids.end()) {
-        if (ids.size() == 256) return;
-        it = ids.emplace(key, (int)seqs.size()).first;
-        seqs.push_back(key);
-      }
-      rpat[lane] = (uint8_t)it->second;
-    }
-  }
+  PatternPlan P;
+  const bool ok = plan_patterns(nl, 1, [&](int64_t lane, std::string& key) {
+    const int64_t s = lane / PG_SLICE;
+    const int t = (int)(lane % PG_SLICE);
+    const int len = h.perm[lane] < 0 ? 0 : h.row_len[lane];
+    for (int j = 0; j < len; ++j)
+      key.push_back((char)p8[(size_t)sp8[s] + (size_t)(j / 4) * 128 + 4 * t + (j & 3)]);
+    return h.perm[lane] >= 0;
+  }, P);
+  if (!ok) return;
+  const std::vector<std::string>& seqs = P.seqs;
   std::vector<int32_t> ptr(seqs.size() + 1, 0);
   std::vector<PairEnt> ent;
   int maxlen = 0;
@@ -308,29 +354,12 @@ static void build_patterns(const SellHost& h, const std::vector<uint8_t>& p8,
   if ((int)ent.size() > kPatMaxEnt) return;
   // master pattern: the most frequent one; every pattern that is an ordered
   // subsequence of it (same pair indices, hence same values) gets its mask
-  std::vector<int64_t> count(seqs.size(), 0);
-  for (int64_t l = 0; l < nl; ++l)
-    if (h.perm[l] >= 0) ++count[rpat[l]];
-  const size_t mp = (size_t)(std::max_element(count.begin(), count.end()) - count.begin());
-  std::vector<uint32_t> mask(seqs.size(), 1u << 31);
-  const std::string& ms = seqs.empty() ? std::string() : seqs[mp];
-  if (!seqs.empty() && ms.size() <= 31) {
-    for (size_t p = 0; p < seqs.size(); ++p) {
-      uint32_t bits = 0;
-      size_t q = 0;
-      for (char c : seqs[p]) {
-        while (q < ms.size() && ms[q] != c) ++q;
-        if (q == ms.size()) {
-          bits = 1u << 31;
-          break;
-        }
-        bits |= 1u << q++;
-      }
-      mask[p] = bits;
-    }
+  std::vector<uint32_t> mask = P.mask;
+  const std::string& ms = seqs[P.master];
+  if (ms.size() <= 31) {
     m->pat_mlen = (int)ms.size();
     m->pat_all_master = 1;
-    for (uint32_t b : mask) m->pat_all_master &= (b >> 31) ? 0 : 1;
+    for (uint32_t bits : mask) m->pat_all_master &= (bits >> 31) ? 0 : 1;
     for (size_t q = 0; q < ms.size(); ++q) {
       const PairEnt& pe = ptab[(uint8_t)ms[q]];
       m->pat_mv[q] = pe.v;
@@ -339,9 +368,8 @@ static void build_patterns(const SellHost& h, const std::vector<uint8_t>& p8,
     }
   }
   if (ent.empty()) ent.push_back(PairEnt{});
-  if (mask.empty()) mask.push_back(1u << 31);
   m->pat_mask = upload(mask.data(), mask.size(), m->bytes);
-  m->rpat = upload(rpat.data(), rpat.size(), m->bytes);
+  m->rpat = upload(P.id.data(), P.id.size(), m->bytes);
   m->pat_ptr = upload(ptr.data(), ptr.size(), m->bytes);
   m->pat_ent = upload(ent.data(), ent.size(), m->bytes);
   m->n_pat = (int)seqs.size();
@@ -361,55 +389,28 @@ static void build_offset_patterns(const SellHost& h, const int32_t* col, pg_matr
   if (env && std::atoi(env) == 0) return;
   if (m->rpat || h.max_width > 31 || m->nrows == 0) return;
   const int64_t nl = h.n_slices * PG_SLICE;
-  std::vector<uint8_t> opat(nl, 0);
-  std::unordered_map<std::string, int> ids;
-  std::vector<std::string> seqs;
-  std::vector<int64_t> count;
-  std::string key;
-  for (int64_t s = 0; s < h.n_slices; ++s) {
-    for (int t = 0; t < PG_SLICE; ++t) {
-      const int64_t lane = s * PG_SLICE + t;
-      const int32_t r = h.perm[lane];
-      key.clear();
-      const int len = r < 0 ? 0 : h.row_len[lane];
-      for (int j = 0; j < len; ++j) {
-        const int64_t o = (int64_t)col[h.slice_ptr[s] + (int64_t)j * PG_SLICE + t] - r;
-        if (o < INT32_MIN || o > INT32_MAX) return;
-        const int32_t o32 = (int32_t)o;
-        key.append(reinterpret_cast<const char*>(&o32), 4);
-      }
-      auto it = ids.find(key);
-      if (it == ids.end()) {
-        if (ids.size() == 256) return;
-        it = ids.emplace(key, (int)seqs.size()).first;
-        seqs.push_back(key);
-        count.push_back(0);
-      }
-      opat[lane] = (uint8_t)it->second;
-      if (r >= 0) ++count[it->second];
+  PatternPlan P;
+  bool fits = true;
+  const bool ok = plan_patterns(nl, 4, [&](int64_t lane, std::string& key) {
+    const int64_t s = lane / PG_SLICE;
+    const int t = (int)(lane % PG_SLICE);
+    const int32_t r = h.perm[lane];
+    const int len = r < 0 ? 0 : h.row_len[lane];
+    for (int j = 0; j < len; ++j) {
+      const int64_t o = (int64_t)col[h.slice_ptr[s] + (int64_t)j * PG_SLICE + t] - r;
+      fits = fits && o >= INT32_MIN && o <= INT32_MAX;
+      const int32_t o32 = (int32_t)o;
+      key.append(reinterpret_cast<const char*>(&o32), 4);
     }
-  }
-  const size_t mp = (size_t)(std::max_element(count.begin(), count.end()) - count.begin());
-  const std::string& ms = seqs[mp];
+    return r >= 0;
+  }, P);
+  if (!ok || !fits) return;
+  const std::string& ms = P.seqs[P.master];
   const size_t ml = ms.size() / 4;
   if (ml == 0 || ml > 31) return;
-  std::vector<uint32_t> mask(seqs.size(), 1u << 31);
-  for (size_t p = 0; p < seqs.size(); ++p) {
-    uint32_t bits = 0;
-    size_t q = 0;
-    for (size_t e = 0; e < seqs[p].size(); e += 4) {
-      while (q < ml && std::memcmp(ms.data() + 4 * q, seqs[p].data() + e, 4) != 0) ++q;
-      if (q == ml) {
-        bits = 1u << 31;
-        break;
-      }
-      bits |= 1u << q++;
-    }
-    mask[p] = bits;
-  }
-  m->opat = upload(opat.data(), opat.size(), m->bytes);
-  m->opat_mask = upload(mask.data(), mask.size(), m->bytes);
-  m->opat_n = (int)seqs.size();
+  m->opat = upload(P.id.data(), P.id.size(), m->bytes);
+  m->opat_mask = upload(P.mask.data(), P.mask.size(), m->bytes);
+  m->opat_n = (int)P.seqs.size();
   m->opat_mlen = (int)ml;
   for (size_t q = 0; q < ml; ++q) std::memcpy(&m->opat_mdoff[q], ms.data() + 4 * q, 4);
 }
@@ -563,6 +564,34 @@ PG_API int pg_sell_fill(int64_t nrows, int64_t ncols, const int64_t* row_ptr,
     std::copy(h.row_len.begin(), h.row_len.end(), row_len);
     std::copy(h.perm.begin(), h.perm.end(), perm);
     sell_fill(h, ncols, row_ptr, col_idx, values, col, val);
+  });
+}
+
+PG_API int pg_row_patterns(int64_t nrows, const int64_t* row_ptr, const int64_t* col_idx,
+                           const double* values, int with_values, uint8_t* ids, int* npat,
+                           int* master, int* master_len, uint32_t* masks) {
+  return guard([&] {
+    PG_REQUIRE(npat && master && master_len, PG_ERR_PARAMETER, "null argument");
+    validate_csr(nrows, row_ptr);
+    PG_REQUIRE(!with_values || values, PG_ERR_PARAMETER, "values required");
+    const size_t sym = with_values ? 12 : 4;
+    PatternPlan P;
+    const bool ok = plan_patterns(nrows, sym, [&](int64_t r, std::string& key) {
+      for (int64_t q = row_ptr[r]; q < row_ptr[r + 1]; ++q) {
+        const int64_t o = col_idx[q] - r;
+        PG_REQUIRE(o >= INT32_MIN && o <= INT32_MAX, PG_ERR_PARAMETER, "offset out of range");
+        const int32_t o32 = (int32_t)o;
+        key.append(reinterpret_cast<const char*>(&o32), 4);
+        if (with_values) key.append(reinterpret_cast<const char*>(values + q), 8);
+      }
+      return true;
+    }, P);
+    *npat = ok ? (int)P.seqs.size() : -1;
+    *master = ok ? (int)P.master : -1;
+    *master_len = ok ? (int)(P.seqs[P.master].size() / sym) : 0;
+    if (!ok) return;
+    if (ids) std::copy(P.id.begin(), P.id.begin() + nrows, ids);
+    if (masks) std::copy(P.mask.begin(), P.mask.end(), masks);
   });
 }
 

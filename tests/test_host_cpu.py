@@ -364,3 +364,85 @@ def test_leja_order_pairs_and_start():
     assert p0.steps == () and p0.y0 == 2.0
     with pytest.raises(pg.ParameterError):
         pg.apply_poly(p0, None, np.zeros(1), pg.CostCounters(), form="chebyshev")
+
+
+# ---------------------------------------------------------------------------
+# row-pattern planning (the grouping behind the row-pattern and offset-pattern
+# matrix formats; host-only entry point, no GPU)
+# ---------------------------------------------------------------------------
+def _row_patterns(h, with_values=True):
+    rp = np.ascontiguousarray(h.row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(h.col_idx, dtype=np.int64)
+    va = np.ascontiguousarray(h.values, dtype=np.float64)
+    ids = np.zeros(h.nrows, dtype=np.uint8)
+    masks = np.zeros(256, dtype=np.uint32)
+    npat, master, mlen = C.c_int(0), C.c_int(0), C.c_int(0)
+    _lib.call("pg_row_patterns", h.nrows, rp.ctypes.data, ci.ctypes.data, va.ctypes.data,
+              int(with_values), ids.ctypes.data, C.byref(npat), C.byref(master), C.byref(mlen),
+              masks.ctypes.data)
+    return npat.value, master.value, mlen.value, ids, masks[:max(npat.value, 0)]
+
+
+def _expected_mask(h, row, master_row):
+    """Bits of the master row's (offset, value) entries a row uses, in order
+    (bit 31 when it is not an ordered subsequence)."""
+    def seq(r):
+        a, b = int(h.row_ptr[r]), int(h.row_ptr[r + 1])
+        return [(int(h.col_idx[q]) - r, float(h.values[q])) for q in range(a, b)]
+    ms, bits, q = seq(master_row), 0, 0
+    for e in seq(row):
+        while q < len(ms) and ms[q] != e:
+            q += 1
+        if q == len(ms):
+            return 1 << 31
+        bits |= 1 << q
+        q += 1
+    return bits
+
+
+def test_row_patterns_laplacian_boundary_rows_are_master_subsequences():
+    """2-D 5-point Laplacian: 9 row patterns (4 corners, 4 edges, interior);
+    the interior row is the master and every boundary row is an ordered
+    subsequence of it (Dirichlet rows drop neighbours) -- the property the
+    unrolled master path of the pattern kernels relies on."""
+    g = 8
+    h = wl.laplacian2d(g)
+    npat, master, mlen, ids, masks = _row_patterns(h)
+    assert npat == 9 and mlen == 5
+    interior = g + 1  # (1, 1)
+    assert ids[interior] == master
+    for r in range(h.nrows):
+        assert masks[ids[r]] == _expected_mask(h, r, interior)
+    assert masks[ids[0]] == 0b11100  # corner (0, 0): offsets 0, +1, +g
+    assert all(m >> 31 == 0 for m in masks)
+
+
+def test_row_patterns_values_and_offsets():
+    """A boundary diagonal that differs from the interior one breaks the
+    (offset, value) subsequence but not the offset-only one (the offset-pattern
+    format, for variable-coefficient stencils)."""
+    h = wl.laplacian2d(8)
+    vals = np.array(h.values, dtype=np.float64)
+    rp, ci = np.asarray(h.row_ptr), np.asarray(h.col_idx)
+    for r in range(h.nrows):
+        if rp[r + 1] - rp[r] < 5:
+            vals[rp[r]:rp[r + 1]][ci[rp[r]:rp[r + 1]] == r] = 5.0
+    m = wl.CsrHost(h.nrows, h.ncols, rp, ci, vals)
+    npat, master, mlen, ids, masks = _row_patterns(m)
+    assert npat == 9 and mlen == 5
+    assert sum(1 for x in masks if x >> 31) == 8  # every boundary pattern
+    npat_o, _, mlen_o, _, masks_o = _row_patterns(m, with_values=False)
+    assert npat_o == 9 and mlen_o == 5 and all(x >> 31 == 0 for x in masks_o)
+
+
+def test_row_patterns_stencils_and_random():
+    """3-D 7- and 27-point stencils: 27 patterns (low / interior / high per
+    dimension), masters of 7 and 27 entries; a random sparse matrix has more
+    than 256 distinct rows (no plan)."""
+    for h, ml in ((wl.convdiff3d_7pt(6), 7), (wl.aniso27(6), 27)):
+        npat, _, mlen, _, masks = _row_patterns(h)
+        assert (npat, mlen) == (27, ml)
+        assert all(x >> 31 == 0 for x in masks)
+    r = wl.random_lognormal(2000, seed=3)
+    assert _row_patterns(r)[0] == -1
+    assert _row_patterns(r, with_values=False)[0] == -1
