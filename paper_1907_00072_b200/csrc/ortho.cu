@@ -663,19 +663,26 @@ static int chunk_grid(const void* kernel, int slot, int dev, int64_t n) {
   return g;
 }
 
-// Kernel choice per basis width (tools/cgs2_bench.py on B200): the warp-chunk
-// kernels win while the basis is narrow (k <= 12: fixed launch / reduction
-// costs dominate and their full occupancy hides them); past that the
-// shared-memory tile kernels (phases 1-2) and the row-streaming phase 3 reach
-// a higher fraction of HBM.  PG_CGS2_TILE=1 / PG_CGS2_CHUNK_KMAX override.
-static bool use_tile_cgs2(int k) {
+// Kernel choice per phase and basis width (tools/cgs2_bench.py on B200,
+// n = 1e6): the warp-chunk kernels win while the basis is narrow (fixed
+// launch / reduction costs dominate and their full occupancy hides them);
+// past that the shared-memory tile kernels (phases 1-2) and the row-streaming
+// phase 3 reach a higher fraction of HBM.  With the 256-row tiles the
+// cross-overs are k = 6 for phase 1 (k = 9: 17.7 vs 24.1 us), k = 9 for
+// phase 2 (21.8 vs 23.4) and k = 12 for phase 3 (24.1 vs 25.0).  All of them
+// project w1 with the same sequential FMA order, so phases 2 and 3 may use
+// different kernel families and still agree bit for bit.  PG_CGS2_TILE=1 /
+// PG_CGS2_CHUNK_KMAX (all phases) override.
+static bool use_tile_cgs2(int k, int phase = 3) {
   static int force_tile = -1, chunk_kmax = -1;
   if (force_tile < 0) {
     force_tile = std::getenv("PG_CGS2_TILE") != nullptr;
     const char* s = std::getenv("PG_CGS2_CHUNK_KMAX");
-    chunk_kmax = s ? std::atoi(s) : 12;
+    chunk_kmax = s ? std::atoi(s) : -1;
   }
-  return force_tile == 1 || k > chunk_kmax;
+  if (force_tile == 1) return true;
+  if (chunk_kmax >= 0) return k > chunk_kmax;
+  return k > (phase == 1 ? 5 : phase == 2 ? 8 : 11);
 }
 
 template <int MODE>
@@ -789,7 +796,7 @@ PG_API int pg_cgs2_phase1(const double* d_V, int64_t ld, int k, const double* d_
   return guard([&] {
     check_tall(d_V, ld, k, n, 1);
     PG_REQUIRE(d_z && d_c1, PG_ERR_PARAMETER, "null argument");
-    if (!use_tile_cgs2(k))
+    if (!use_tile_cgs2(k, 1))
       launch_chunk_dots<1>(d_V, ld, k, d_z, n, nullptr, d_c1, ws, as_stream(stream));
     else
       launch_tile<kDots>(d_V, ld, k, d_z, n, nullptr, d_c1, ws, as_stream(stream));
@@ -801,7 +808,7 @@ PG_API int pg_cgs2_phase2(const double* d_V, int64_t ld, int k, const double* d_
   return guard([&] {
     check_tall(d_V, ld, k, n, 1);
     PG_REQUIRE(d_z && d_c1 && d_c2, PG_ERR_PARAMETER, "null argument");
-    if (!use_tile_cgs2(k))
+    if (!use_tile_cgs2(k, 2))
       launch_chunk_dots<2>(d_V, ld, k, d_z, n, d_c1, d_c2, ws, as_stream(stream));
     else
       launch_tile<kUpdDots>(d_V, ld, k, d_z, n, d_c1, d_c2, ws, as_stream(stream));
