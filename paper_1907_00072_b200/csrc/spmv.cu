@@ -642,16 +642,21 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
       };
       int64_t p0 = 0, p1 = 0, q0 = 0, q1 = 0;
       bounds(blockIdx.x, p0, p1);
-      int it = 0;
-      for (int64_t rb = blockIdx.x; rb < wa.nblk; rb += gridDim.x, ++it) {
+      // ring slot and its reuse round kept as running counters (no integer
+      // division by the runtime stage count per row block)
+      int st = 0, round = 0;
+      for (int64_t rb = blockIdx.x; rb < wa.nblk; rb += gridDim.x) {
         bounds(rb + gridDim.x, q0, q1);
-        const int st = it % S;
-        if (it >= S) mbar_wait(&empty[st], (uint32_t)((it / S - 1) & 1));
+        if (round > 0) mbar_wait(&empty[st], (uint32_t)((round - 1) & 1));
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         win_issue<MODE, PAT>(a, wa, e, pair8, x, rb, p0, p1,
                              smem_win + (size_t)st * wa.stage_bytes, &full[st]);
         p0 = q0;
         p1 = q1;
+        if (++st == S) {
+          st = 0;
+          ++round;
+        }
       }
     }
   } else {
@@ -659,10 +664,18 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
     epi_vectors<MODE>(e, x, A, B);
     const int t = threadIdx.x;
     const int sl = t >> 5;  // slice of this thread's row inside the block
-    int it = 0;
-    for (int64_t rb = blockIdx.x; rb < wa.nblk; rb += gridDim.x, ++it) {
-      const int st = it % S;
-      const unsigned char* buf = smem_win + (size_t)st * wa.stage_bytes;
+    int st = 0;
+    uint32_t phase = 0;
+    const unsigned char* buf = smem_win;
+    for (int64_t rb = blockIdx.x; rb < wa.nblk; rb += gridDim.x) {
+      if (rb != blockIdx.x) {  // next ring slot (running counters, no division)
+        buf += wa.stage_bytes;
+        if (++st == S) {
+          st = 0;
+          phase ^= 1u;
+          buf = smem_win;
+        }
+      }
       const int64_t row = rb * kWinRows + t;
       const bool live = row < a.nrows;
       const int lane = t & 31;
@@ -676,7 +689,7 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
           pre = epi_load<MODE>(e, x, row);
         }
       }
-      mbar_wait(&full[st], (uint32_t)((it / S) & 1));
+      mbar_wait(&full[st], phase);
       if (PAT) {
         const int pid = live ? buf[wa.off_p8 + t] : 0;
         const uint32_t mask = LB > 0 ? s_mask[pid] : (1u << 31);
