@@ -445,7 +445,15 @@ __global__ void __launch_bounds__(kSellThreads, PG_PAT_MIN_BLOCKS)
 #ifndef PG_WIN_STAGE_EPI
 #define PG_WIN_STAGE_EPI 1
 #endif
-constexpr bool kWinStageEpi = PG_WIN_STAGE_EPI;
+constexpr bool kWinStageEpiPair = PG_WIN_STAGE_EPI;
+// Row-pattern stages leave the epilogue operands to the row threads (coalesced
+// loads issued before the stage wait): the smaller stage buys a deeper ring
+// (cfg4-160^3 pass 49.9 -> 49.0 us)
+#ifndef PG_WIN_PAT_STAGE_EPI
+#define PG_WIN_PAT_STAGE_EPI 0
+#endif
+template <bool PAT>
+constexpr bool kWinStageEpi = PAT ? (bool)PG_WIN_PAT_STAGE_EPI : kWinStageEpiPair;
 
 struct WinArgs {
   int ng, total, b8, stages;
@@ -546,7 +554,7 @@ __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, 
   }
   // pass 1: byte count (+ odd tails), so that expect_tx precedes the copies
   uint32_t bytes = (uint32_t)(p1 - p0);
-  if (kWinStageEpi && !PAT)  // row lengths + slice widths (bulk unless a partial block)
+  if (kWinStageEpi<PAT> && !PAT)  // row lengths + slice widths (bulk unless a partial block)
     bytes += 4u * (uint32_t)((s1 - s0) * PG_SLICE) +
              ((s1 - s0) * 4 % 16 == 0 ? 4u * (uint32_t)(s1 - s0) : 0u);
   for (int g = 0; g < wa.ng; ++g) {
@@ -555,7 +563,7 @@ __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, 
     if (vb > va) bytes += stage_f64_tail(win + wa.start[g] + (va - ga), x + va, vb - va);
   }
   int32_t* sw = reinterpret_cast<int32_t*>(buf + wa.off_sw);
-  if (kWinStageEpi) {
+  if (kWinStageEpi<PAT>) {
     if (A) bytes += stage_f64_tail(reinterpret_cast<double*>(buf + wa.off_ea), A + r0, nr);
     if (B) bytes += stage_f64_tail(reinterpret_cast<double*>(buf + wa.off_eb), B + r0, nr);
     if (!PAT && (s1 - s0) * 4 % 16 != 0)  // partial last block: slice widths copied plainly
@@ -570,7 +578,7 @@ __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, 
       bulk_g2s(win + wa.start[g] + (va - ga), x + va, 8u * (uint32_t)n2, bar);
   }
   if (p1 > p0) bulk_g2s(buf + wa.off_p8, pair8 + p0, (uint32_t)(p1 - p0), bar);
-  if (kWinStageEpi) {
+  if (kWinStageEpi<PAT>) {
     if (A && nr > 1) bulk_g2s(buf + wa.off_ea, A + r0, 8u * (uint32_t)(nr & ~(int64_t)1), bar);
     if (B && nr > 1) bulk_g2s(buf + wa.off_eb, B + r0, 8u * (uint32_t)(nr & ~(int64_t)1), bar);
     if (!PAT) {
@@ -681,11 +689,11 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
       const int lane = t & 31;
       int swl = 0, len = 0;
       Pre pre{0.0, 0.0};
-      if (!kWinStageEpi) {  // per-row operands from global, overlapping the wait
+      if (!kWinStageEpi<PAT>) {  // per-row operands from global, overlapping the wait
         const int64_t s0 = rb * (kWinRows / PG_SLICE);
         if (lane < sl && s0 + lane < wa.n_slices) swl = __ldg(a.slice_w + s0 + lane);
         if (live) {
-          len = __ldg(a.row_len + row);
+          if (!PAT) len = __ldg(a.row_len + row);
           pre = epi_load<MODE>(e, x, row);
         }
       }
@@ -697,8 +705,8 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
         const bool all_full =
             LB > 0 && pm.len == LB && __all_sync(0xffffffffu, !live || mask == full);
         if (live) {
-          if (A) pre.a = reinterpret_cast<const double*>(buf + wa.off_ea)[t];
-          if (B) pre.b = reinterpret_cast<const double*>(buf + wa.off_eb)[t];
+          if (kWinStageEpi<PAT> && A) pre.a = reinterpret_cast<const double*>(buf + wa.off_ea)[t];
+          if (kWinStageEpi<PAT> && B) pre.b = reinterpret_cast<const double*>(buf + wa.off_eb)[t];
           const unsigned char* winrow = buf + 8 * t;
           double acc = 0.0;
           if (all_full) {
@@ -721,7 +729,7 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
         if ((t & 31) == 0) mbar_arrive(&empty[st]);
         continue;
       }
-      if (kWinStageEpi) {
+      if (kWinStageEpi<PAT>) {
         if (lane < sl) swl = reinterpret_cast<const int32_t*>(buf + wa.off_sw)[lane];
         if (live) {
           len = reinterpret_cast<const int32_t*>(buf + wa.off_rl)[t];
@@ -877,7 +885,9 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
     wa.off_eb = wa.off_ea + 8 * kWinRows;
     wa.off_rl = wa.off_eb + 8 * kWinRows;
     wa.off_sw = wa.off_rl + 4 * kWinRows;
-    wa.stage_bytes = win_pat ? wa.off_rl : wa.off_sw + 128;
+    // row-pattern stages: window + pattern ids (+ the epilogue operands when
+    // they ride in the ring)
+    wa.stage_bytes = win_pat ? (kWinStageEpi<true> ? wa.off_rl : wa.off_ea) : wa.off_sw + 128;
     const PatMaster pm = win_pat ? master_of(m) : PatMaster{};
     // every pattern a masked master subsequence: the entry table is never read
     const int tab_nent = (win_pat && pm.lb > 0 && m->pat_all_master) ? 0 : m->pat_nent;
