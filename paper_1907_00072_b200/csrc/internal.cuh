@@ -131,8 +131,12 @@ struct __align__(16) PairEnt {
 // mbarrier hand-offs and producer issue are amortised over twice the rows of
 // the earlier 256 (cfg4-160^3 windowed row-pattern pass 61.6 -> 57.1 us;
 // 128: 110, 384: 62.5, 768: 60.8 -- tools/spmv_bench.py over build variants)
+// r01i: 1024-row stages swept by 512 row threads (two rows each) for the
+// row-pattern variant (cfg4-160^3 49.6 -> 43.8 us; 768 rows / 384 threads 44.3).
+// The pair-stream windowed kernel sums one row per thread, so with two rows
+// per thread pattern-less windowed matrices take the global-gather pair kernel.
 #ifndef PG_WIN_ROWS
-#define PG_WIN_ROWS 512
+#define PG_WIN_ROWS 1024
 #endif
 constexpr int kWinRows = PG_WIN_ROWS;
 constexpr int kWinMaxGroups = 32;

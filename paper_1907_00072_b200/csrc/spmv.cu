@@ -593,7 +593,15 @@ __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, 
 // one row per thread from shared memory only -- matrix stream, x window,
 // epilogue operands, row lengths all arrive by TMA -- and release the stage
 // through the `empty` mbarrier.  Global memory is only written (outputs).
-constexpr int kWinThreads = kWinRows + 32;
+// Row threads per block; a row-pattern stage of kWinRows rows gives each
+// row thread kWinRows / kWinRowThreads rows (pair-stream stages: one).
+#ifndef PG_WIN_ROW_THREADS
+#define PG_WIN_ROW_THREADS 512
+#endif
+constexpr int kWinRowThreads = PG_WIN_ROW_THREADS;
+constexpr int kWinRPT = kWinRows / kWinRowThreads;
+static_assert(kWinRows % kWinRowThreads == 0, "stage rows must be whole row-thread sweeps");
+constexpr int kWinThreads = kWinRowThreads + 32;
 
 #ifndef PG_WIN_MIN_BLOCKS
 #define PG_WIN_MIN_BLOCKS 2
@@ -631,14 +639,14 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
   if (threadIdx.x == 0) {
     for (int st = 0; st < S; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], kWinRows / 32);
+      mbar_init(&empty[st], kWinRowThreads / 32);
     }
     mbar_fence_init();
   }
   __syncthreads();
   double local = 0.0;
   const int warp = threadIdx.x >> 5;
-  if (warp == kWinRows / 32) {
+  if (warp == kWinRowThreads / 32) {
     if ((threadIdx.x & 31) == 0) {
       // the packed-stream bounds of the next row block are loaded one
       // iteration ahead, off the issue path
@@ -684,6 +692,56 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
           buf = smem_win;
         }
       }
+      if (PAT) {
+        // kWinRPT rows per thread (t, t + kWinRowThreads, ...): epilogue
+        // operands requested before the stage wait, rows summed after it
+        Pre pre[kWinRPT];
+#pragma unroll
+        for (int h = 0; h < kWinRPT; ++h) {
+          const int64_t row = rb * kWinRows + t + h * kWinRowThreads;
+          pre[h] = Pre{0.0, 0.0};
+          if (!kWinStageEpi<PAT> && row < a.nrows) pre[h] = epi_load<MODE>(e, x, row);
+        }
+        mbar_wait(&full[st], phase);
+#pragma unroll
+        for (int h = 0; h < kWinRPT; ++h) {
+          const int th = t + h * kWinRowThreads;  // row slot inside the stage
+          const int64_t row = rb * kWinRows + th;
+          const bool live = row < a.nrows;
+          const int pid = live ? buf[wa.off_p8 + th] : 0;
+          const uint32_t mask = LB > 0 ? s_mask[pid] : (1u << 31);
+          const uint32_t full = pm.len >= 32 ? 0xffffffffu : (1u << pm.len) - 1u;
+          const bool all_full =
+              LB > 0 && pm.len == LB && __all_sync(0xffffffffu, !live || mask == full);
+          if (live) {
+            if (kWinStageEpi<PAT> && A)
+              pre[h].a = reinterpret_cast<const double*>(buf + wa.off_ea)[th];
+            if (kWinStageEpi<PAT> && B)
+              pre[h].b = reinterpret_cast<const double*>(buf + wa.off_eb)[th];
+            const unsigned char* winrow = buf + 8 * th;
+            double acc = 0.0;
+            if (all_full) {
+              acc = row_sum_master<(LB > 0 ? LB : 8), true, false, true>(mask, pm, winrow,
+                                                                          nullptr);
+            } else if (LB > 0 && !(mask >> 31)) {
+              acc = row_sum_master<(LB > 0 ? LB : 8), true>(mask, pm, winrow, nullptr);
+            } else {
+              const int end = s_pptr[pid + 1];
+#pragma unroll 4
+              for (int q = s_pptr[pid]; q < end; ++q) {
+                const int4 raw = reinterpret_cast<const int4*>(s_pent)[q];
+                acc = __dadd_rn(acc, __dmul_rn(__hiloint2double(raw.y, raw.x),
+                                               *reinterpret_cast<const double*>(winrow + raw.z)));
+              }
+            }
+            const double r = epilogue<MODE>(e, pre[h], row, acc);
+            if (MODE == kResid) local = __fma_rn(r, r, local);
+          }
+        }
+        __syncwarp();
+        if ((t & 31) == 0) mbar_arrive(&empty[st]);
+        continue;
+      }
       const int64_t row = rb * kWinRows + t;
       const bool live = row < a.nrows;
       const int lane = t & 31;
@@ -693,42 +751,11 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
         const int64_t s0 = rb * (kWinRows / PG_SLICE);
         if (lane < sl && s0 + lane < wa.n_slices) swl = __ldg(a.slice_w + s0 + lane);
         if (live) {
-          if (!PAT) len = __ldg(a.row_len + row);
+          len = __ldg(a.row_len + row);
           pre = epi_load<MODE>(e, x, row);
         }
       }
       mbar_wait(&full[st], phase);
-      if (PAT) {
-        const int pid = live ? buf[wa.off_p8 + t] : 0;
-        const uint32_t mask = LB > 0 ? s_mask[pid] : (1u << 31);
-        const uint32_t full = pm.len >= 32 ? 0xffffffffu : (1u << pm.len) - 1u;
-        const bool all_full =
-            LB > 0 && pm.len == LB && __all_sync(0xffffffffu, !live || mask == full);
-        if (live) {
-          if (kWinStageEpi<PAT> && A) pre.a = reinterpret_cast<const double*>(buf + wa.off_ea)[t];
-          if (kWinStageEpi<PAT> && B) pre.b = reinterpret_cast<const double*>(buf + wa.off_eb)[t];
-          const unsigned char* winrow = buf + 8 * t;
-          double acc = 0.0;
-          if (all_full) {
-            acc = row_sum_master<(LB > 0 ? LB : 8), true, false, true>(mask, pm, winrow, nullptr);
-          } else if (LB > 0 && !(mask >> 31)) {
-            acc = row_sum_master<(LB > 0 ? LB : 8), true>(mask, pm, winrow, nullptr);
-          } else {
-            const int end = s_pptr[pid + 1];
-#pragma unroll 4
-            for (int q = s_pptr[pid]; q < end; ++q) {
-              const int4 raw = reinterpret_cast<const int4*>(s_pent)[q];
-              acc = __dadd_rn(acc, __dmul_rn(__hiloint2double(raw.y, raw.x),
-                                             *reinterpret_cast<const double*>(winrow + raw.z)));
-            }
-          }
-          const double r = epilogue<MODE>(e, pre, row, acc);
-          if (MODE == kResid) local = __fma_rn(r, r, local);
-        }
-        __syncwarp();
-        if ((t & 31) == 0) mbar_arrive(&empty[st]);
-        continue;
-      }
       if (kWinStageEpi<PAT>) {
         if (lane < sl) swl = reinterpret_cast<const int32_t*>(buf + wa.off_sw)[lane];
         if (live) {
@@ -852,8 +879,9 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
   const bool aligned = al16(x) && al16(e.acc_in) && al16(e.base) && al16(e.b);
   // windowed kernel: long rows (27-point: 1.6x the pair kernel); short rows
   // (7-point) keep the global-gather pair kernel, which is faster there
-  const bool win_ok = m->pair8 && m->wtab && aligned;
-  const bool win_pat = win_ok && m->rpat && winpat_enabled();
+  const bool win_pat = m->pair8 && m->wtab && aligned && m->rpat && winpat_enabled();
+  // the pair-stream windowed kernel sums one row per thread per stage
+  const bool win_ok = m->pair8 && m->wtab && aligned && (win_pat || kWinRPT == 1);
   if (pattern_kernel(m)) {
     int64_t blocks = (a.nlanes + kSellThreads - 1) / kSellThreads;
     static int per_sm = -1;
