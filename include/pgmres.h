@@ -285,6 +285,29 @@ PG_API int pg_scale_add(const double* d_base, double a, const double* d_v, int64
 PG_API int pg_gather(const double* d_x, const int32_t* d_idx, int64_t m, double* d_out,
                      void* stream);
 
+/* ---- reference-order reductions for the degree decision ---------------------
+ * The reference's Cholesky pass/fail and auto_degree choice (polyprec.py:60-93,
+ * 150-190) are decided by the rounding of the seed norm and of the Gram matrix,
+ * i.e. by the summation order of the BLAS numpy calls (np.linalg.norm -> ddot,
+ * polyprec.py:46-51; AV.T @ AV -> syrk, polyprec.py:115-122).  These evaluate
+ * both in OpenBLAS 0.3.30's x86-64 order (csrc/blasorder.cu):
+ * pg_dot_blas: d_out[0] = x.y as OpenBLAS ddot with `nthreads` (1..32) chunks
+ *   (one chunk when n <= 10000) -- bit-identical to numpy's x.dot(y) on a host
+ *   whose OpenBLAS runs `nthreads` threads with the SkylakeX/Haswell kernel.
+ * pg_gram_blas: upper triangle (packed row-major, (i,j) i<=j) of P^T P over
+ *   the ncols columns of P, rows in syrk K-blocks of 384 (halving rule for the
+ *   last two), one FMA chain per entry and block, blocks added in order.  For
+ *   a row-block shard [g0, g0+n) of N rows: d_state_in (NULL for the first
+ *   shard) and d_state_out hold 2*npairs doubles, [open block chains | sum of
+ *   completed blocks]; the last shard's sum is the Gram.  d_scratch holds
+ *   pg_gram_blas_scratch() doubles.  in and out must not alias. */
+PG_API int pg_dot_blas(const double* d_x, const double* d_y, int64_t n, int nthreads,
+                       double* d_out, void* stream);
+PG_API int pg_gram_blas_scratch(int64_t n, int64_t g0, int64_t N, int ncols, int64_t* doubles);
+PG_API int pg_gram_blas(const double* d_P, int64_t ld, int ncols, int64_t n, int64_t g0,
+                        int64_t N, const double* d_state_in, double* d_state_out,
+                        double* d_scratch, void* stream);
+
 /* ---- host routines (CPU, synchronous) --------------------------------------
  * The small dense steps the reference keeps on the host, natively:
  * pg_host_cholesky_solve: dense_cholesky (polyprec.py:60-93) of the leading

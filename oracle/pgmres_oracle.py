@@ -21,6 +21,8 @@ results are bit-identical to the reference.
 from __future__ import annotations
 
 import math
+import os
+import subprocess
 
 import numpy as np
 
@@ -395,6 +397,87 @@ def auto_deg_from_gram(Gfull, cap):
         if np.all(np.isfinite(yy)):
             best = (d, yy)
     return best
+
+
+# ---------------------------------------------------------------------------
+# reference-order (OpenBLAS) reductions of the degree decision -- C restatement
+# in oracle/blasorder.c, built into oracle/_ref/libblasorder.so
+# ---------------------------------------------------------------------------
+_BLAS = None
+ORACLE_DIR = os.path.dirname(os.path.abspath(__file__))
+BLAS_LIB = os.path.join(ORACLE_DIR, "_ref", "libblasorder.so")
+
+
+def build_blasorder(force: bool = False) -> str:
+    """gcc oracle/blasorder.c -> oracle/_ref/libblasorder.so (test infrastructure)."""
+    src = os.path.join(ORACLE_DIR, "blasorder.c")
+    if force or not os.path.exists(BLAS_LIB) or os.path.getmtime(BLAS_LIB) < os.path.getmtime(src):
+        os.makedirs(os.path.dirname(BLAS_LIB), exist_ok=True)
+        tmp = BLAS_LIB + ".tmp"
+        subprocess.run(["gcc", "-O2", "-shared", "-fPIC", "-ffp-contract=off", src, "-o", tmp,
+                        "-lm"], check=True)
+        os.replace(tmp, BLAS_LIB)
+    return BLAS_LIB
+
+
+def _blas():
+    global _BLAS
+    if _BLAS is None:
+        import ctypes
+        lib = ctypes.CDLL(build_blasorder())
+        lib.oracle_blas_ddot.restype = ctypes.c_double
+        lib.oracle_blas_ddot.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_int]
+        lib.oracle_blas_gram.restype = None
+        lib.oracle_blas_gram.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                         ctypes.c_int64, ctypes.c_void_p]
+        _BLAS = lib
+    return _BLAS
+
+
+def blas_ddot(x, y, nthreads: int = 8) -> float:
+    """x.y in OpenBLAS ddot order with ``nthreads`` threads (numpy's x.dot(y)
+    on the build host)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    return float(_blas().oracle_blas_ddot(len(x), x.ctypes.data, y.ctypes.data, nthreads))
+
+
+def blas_gram(P) -> np.ndarray:
+    """P^T P in OpenBLAS syrk K-block order (numpy's A.T @ A, full tiles)."""
+    P = np.ascontiguousarray(P, dtype=np.float64)
+    n, k = P.shape
+    G = np.zeros((k, k))
+    _blas().oracle_blas_gram(n, k, P.ctypes.data, k, G.ctypes.data)
+    return G
+
+
+def seed_blas(v0, nthreads: int = 8):
+    """_unit_seed (polyprec.py:46-51) with the norm in OpenBLAS order."""
+    v0 = np.asarray(v0, dtype=np.float64)
+    nrm = float(np.sqrt(blas_ddot(v0, v0, nthreads)))
+    return v0 / nrm, nrm
+
+
+def gram_full_blas(op, v0, top, nthreads: int = 8):
+    """Full Gram of [v, Av, ..., A^top v] in reference (OpenBLAS) order, and
+    the seed norm.  Column 0 pairs give rhs = AV^T v."""
+    v, nrm = seed_blas(v0, nthreads)
+    return blas_gram(power_columns(op, v, top)), nrm
+
+
+def degree_decision_blas(Gfull, deg):
+    """(build_poly(deg) failing pivot or 0, auto_degree(cap=deg) degree) from a
+    full Gram of deg+2 columns, with the reference's Cholesky loop."""
+    G = Gfull[1:deg + 2, 1:deg + 2]
+    rhs = Gfull[1:deg + 2, 0]
+    try:
+        chol_solve(G, rhs)
+        piv = 0
+    except CholeskyFailureOracle as exc:
+        piv = exc.pivot
+    best = auto_deg_from_gram(Gfull, deg)
+    return piv, (best[0] if best else 0)
 
 
 def min_res_poly(op, v0, deg, tally):

@@ -58,6 +58,9 @@ _SIGNATURES = {
     "pg_normalize": ([_p, _p, _i64, _p, _p], C.c_int),
     "pg_gram": ([_p, _i64, _i32, _i64, _p, _p, _p], C.c_int),
     "pg_gemv": ([_p, _i64, _i32, _p, _i64, _p, _p], C.c_int),
+    "pg_dot_blas": ([_p, _p, _i64, _i32, _p, _p], C.c_int),
+    "pg_gram_blas_scratch": ([_i64, _i64, _i64, _i32, _pi64], C.c_int),
+    "pg_gram_blas": ([_p, _i64, _i32, _i64, _i64, _i64, _p, _p, _p, _p], C.c_int),
     "pg_dot": ([_p, _p, _i64, _p, _p, _p], C.c_int),
     "pg_scale_add": ([_p, _d, _p, _i64, _p, _p], C.c_int),
     "pg_gather": ([_p, _p, _i64, _p, _p], C.c_int),
@@ -137,7 +140,7 @@ def check(code: int, what: str = ""):
 LAUNCHING = frozenset({
     "pg_spmv", "pg_poly_pass", "pg_root_pass", "pg_residual", "pg_cgs2_phase1", "pg_cgs2_phase2",
     "pg_cgs2_phase3", "pg_normalize", "pg_gram", "pg_gemv", "pg_dot", "pg_scale_add",
-    "pg_gather", "pg_ilu_apply",
+    "pg_gather", "pg_ilu_apply", "pg_dot_blas",
 })
 #: per-entry-point launch tally (bench.py reports it as gpu_launches)
 LAUNCH_COUNT: dict = {}

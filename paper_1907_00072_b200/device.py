@@ -131,6 +131,7 @@ class Shard:
         self.plan = HaloPlan(ghosts, plan_recv(ghosts, offsets, self.n))
         self.n_ext = self.n + len(ghosts)
         self.ld = _pad(self.n_ext)
+        self.offsets = np.asarray(offsets, dtype=np.int64)
         cols_local = localize_columns(cols_global, self.r0, self.r1, ghosts)
         self.sigma = choose_sigma(row_ptr) if sigma is None else int(sigma)
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
@@ -1050,6 +1051,80 @@ class Engine:
                 lo = lo + ((hi - (s - bb)) + (x - bb))
                 hi = s
         return (hi + lo).reshape(ncols, ncols)
+
+    # ---- reference-order reductions (csrc/blasorder.cu) -------------------------
+    def dot_blas(self, xs, ys, slot: int, nthreads: int):
+        """Global x.y in OpenBLAS ddot order (np.linalg.norm's squared sum,
+        polyprec.py:46-51) into every shard's device slot ``slot``.  The order
+        is defined on the global vector, so with several shards the vectors are
+        first gathered onto shard 0's device (once per polynomial build)."""
+        outs = self.slot(slot)
+        s0 = self.shards[0]
+        if self.P == 1 and not self.comm.distributed:
+            _lib.call("pg_dot_blas", ptr(xs[0]), ptr(ys[0]), s0.n, nthreads, ptr(outs[0]),
+                      s0.stream)
+            return
+        gx = self._gather_global(xs)
+        gy = gx if ys is xs else self._gather_global(ys)
+        s0.activate()
+        _lib.call("pg_dot_blas", ptr(gx), ptr(gy), self.N, nthreads, ptr(outs[0]), s0.stream)
+        for o in outs[1:]:
+            o.copy_(outs[0].to(o.device))
+
+    def _gather_global(self, xs) -> torch.Tensor:
+        """The global vector on shard 0's device (rank-local device when
+        distributed: an all_gather of the row blocks)."""
+        s0 = self.shards[0]
+        if not self.comm.distributed:
+            return torch.cat([t[:s.n].to(s0.device) for s, t in zip(self.shards, xs)])
+        comm = self.comm
+        sizes = [int(v) for v in np.diff(s0.offsets)]
+        m = max(sizes)
+        src = torch.zeros(m, dtype=F64, device=s0.device)
+        src[:s0.n].copy_(xs[0][:s0.n])
+        if comm.staged:
+            src = src.cpu()
+        parts = [torch.zeros_like(src) for _ in range(comm.world)]
+        comm.dist.all_gather(parts, src, group=comm.group)
+        return torch.cat([p[:sz] for p, sz in zip(parts, sizes)]).to(s0.device)
+
+    def gram_blas(self, Ps, ncols) -> np.ndarray:
+        """Gram matrix of the first ncols columns in OpenBLAS syrk order
+        (polyprec.py:115-122 through numpy's A.T @ A).  The shards run in row
+        order, each continuing the previous one's open K-block chains and
+        running sum (pg_gram_blas state), so G is bit-identical for any row
+        partition.  Returns the full symmetric (ncols, ncols) host matrix."""
+        npairs = ncols * (ncols + 1) // 2
+        state = None
+        comm = self.comm
+        if comm.distributed and comm.rank > 0:
+            dev = self.shards[0].device
+            buf = torch.zeros(2 * npairs, dtype=F64, device="cpu" if comm.staged else dev)
+            comm.dist.recv(buf, comm.rank - 1, group=comm.group)
+            state = buf.to(dev)
+        for s, P in zip(self._each(), Ps):
+            need = _lib.C.c_int64(0)
+            _lib.call("pg_gram_blas_scratch", s.n, s.r0, self.N, ncols, _lib.C.byref(need))
+            scratch = torch.empty(max(int(need.value), 1), dtype=F64, device=s.device)
+            out = torch.empty(2 * npairs, dtype=F64, device=s.device)
+            sin = state.to(s.device) if state is not None else None
+            _lib.call("pg_gram_blas", ptr(P), s.ld, ncols, s.n, s.r0, self.N,
+                      ptr(sin) if sin is not None else None, ptr(out), ptr(scratch), s.stream)
+            _lib.add_launches("pg_gram_blas", 2)
+            state = out
+        if comm.distributed:
+            if comm.rank + 1 < comm.world:
+                comm.dist.send(state.cpu() if comm.staged else state, comm.rank + 1,
+                               group=comm.group)
+            last = state.cpu() if comm.staged else state.clone()
+            comm.dist.broadcast(last, comm.world - 1, group=comm.group)
+            state = last
+        packed = state[npairs:].cpu().numpy()
+        G = np.zeros((ncols, ncols))
+        iu = np.triu_indices(ncols)
+        G[iu] = packed
+        G.T[iu] = packed
+        return G
 
     def copy(self, src, dst):
         for s, a, b in zip(self.shards, src, dst):

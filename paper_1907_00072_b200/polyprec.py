@@ -14,6 +14,7 @@ the accumulator in its epilogue, bit-identical to the reference.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -93,9 +94,28 @@ def _engine(op):
     return eng
 
 
-def _device_power_gram(op, v0, top: int, counters: CostCounters):
+#: How the degree decision's arithmetic is evaluated (polyprec.py:60-93):
+#:  "reference" (default) -- the seed norm and the Gram matrix in the summation
+#:     order of the reference's BLAS calls (OpenBLAS ddot / syrk, csrc/
+#:     blasorder.cu) and the reference's own Cholesky loop, so build_poly's
+#:     pass/fail and auto_degree's choice are the reference's;
+#:  "exact" -- a double-double Gram and a compensated Cholesky: the decision
+#:     exact arithmetic takes, independent of any BLAS (opt-in).
+DECISIONS = ("reference", "exact")
+#: OpenBLAS thread count of the host whose ddot order the seed norm follows
+#: (the build container that recorded tests/golden: 8)
+BLAS_THREADS = int(os.environ.get("PG_BLAS_THREADS", "8"))
+
+
+def _check_decision(decision: str):
+    if decision not in DECISIONS:
+        raise ParameterError(f"unknown decision arithmetic {decision!r} (expected {DECISIONS})")
+
+
+def _device_power_gram(op, v0, top: int, counters: CostCounters, decision: str = "reference"):
     """Unit seed, then the ``top``+1 power columns on the device and their
     full Gram matrix on the host.  Returns (Gram (top+1)^2, seed_norm)."""
+    _check_decision(decision)
     e = _engine(op)
     if isinstance(v0, torch.Tensor):
         if v0.shape != (op.dimension,) and not (e.comm.distributed and v0.shape == (e.local_n,)):
@@ -109,13 +129,16 @@ def _device_power_gram(op, v0, top: int, counters: CostCounters):
     vs = e.ingest(v0)
     # |v0|^2 stays in device slot 6 while the power sequence and the Gram are
     # queued: one host round trip (the Gram's) instead of two
-    e.dot(vs, vs, slot=6, fetch=False)
+    if decision == "reference":
+        e.dot_blas(vs, vs, slot=6, nthreads=BLAS_THREADS)
+    else:
+        e.dot(vs, vs, slot=6, fetch=False)
     P = e.cached_blocks("powers", top + 1)
     # column 0 = v0 / |v0| (exact division, as numpy's v0 / seed_norm)
     e.normalize_dev(vs, e.slot(6), [blk[0] for blk in P])
     e.power_sequence(P, top + 1)
     e.count_ops(op.counters, top)
-    G = e.gram(P, top + 1)
+    G = e.gram_blas(P, top + 1) if decision == "reference" else e.gram(P, top + 1)
     seed_norm = float(np.sqrt(e.read_slot(6)))
     if seed_norm == 0.0:
         raise ParameterError("seed vector v0 must be nonzero")
@@ -129,23 +152,35 @@ def _normal_equations(Gfull: np.ndarray, deg: int, counters: CostCounters) -> Gr
     return GramSystem(Gfull[1:deg + 2, 1:deg + 2].copy(), Gfull[1:deg + 2, 0].copy())
 
 
+def _factor(system: GramSystem, decision: str):
+    """(y, failed 1-based pivot or 0): the reference's Cholesky loop
+    (dense_cholesky, polyprec.py:60-93) or the native compensated one."""
+    if decision == "exact":
+        return _lib.host_cholesky(system.G, system.rhs)
+    try:
+        return dense_cholesky(system), 0
+    except CholeskyFailure as exc:
+        return None, exc.pivot
+
+
 def build_poly(op, v0, deg: int, counters: CostCounters,
-               seed_mode: str = "unspecified") -> PolyCoefficients:
+               seed_mode: str = "unspecified", decision: str = "reference") -> PolyCoefficients:
     """Degree-``deg`` minimum-residual polynomial (polyprec.py:125-147):
-    deg+1 device SpMVs, 2 dots, host Cholesky."""
+    deg+1 device SpMVs, 2 dots, host Cholesky.  ``decision`` selects the
+    arithmetic of the pass/fail decision (``DECISIONS``)."""
     if deg < 0:
         raise ParameterError("polynomial degree must be non-negative")
-    Gfull, seed_norm = _device_power_gram(op, v0, deg + 1, counters)
+    Gfull, seed_norm = _device_power_gram(op, v0, deg + 1, counters, decision)
     counters.scalar_dots += 1
     full = _normal_equations(Gfull, deg, counters)
-    y, pivot = _lib.host_cholesky(full.G, full.rhs)
+    y, pivot = _factor(full, decision)
     if pivot:
         raise CholeskyFailure(pivot)
     return PolyCoefficients(deg, y, seed_norm, seed_mode)
 
 
 def auto_degree(op, v0, cap: int = DEFAULT_DEGREE_CAP, counters: CostCounters | None = None,
-                seed_mode: str = "unspecified") -> PolyCoefficients:
+                seed_mode: str = "unspecified", decision: str = "reference") -> PolyCoefficients:
     """Largest degree <= cap whose Gram system factors (polyprec.py:150-190):
     one shared power sequence of cap+1 SpMVs, nested Gram blocks re-factored on
     the host, degree-0 fallback."""
@@ -153,27 +188,37 @@ def auto_degree(op, v0, cap: int = DEFAULT_DEGREE_CAP, counters: CostCounters | 
         raise ParameterError("degree cap must be at least 1")
     if counters is None:
         counters = CostCounters()
-    Gfull, seed_norm = _device_power_gram(op, v0, cap + 1, counters)
+    Gfull, seed_norm = _device_power_gram(op, v0, cap + 1, counters, decision)
     counters.scalar_dots += 1
-    return _select_degree(_normal_equations(Gfull, cap, counters), cap, seed_norm, seed_mode)
+    return _select_degree(_normal_equations(Gfull, cap, counters), cap, seed_norm, seed_mode,
+                          decision)
 
 
-def _select_degree(full: GramSystem, cap: int, seed_norm: float, seed_mode: str):
+def _select_degree(full: GramSystem, cap: int, seed_norm: float, seed_mode: str,
+                   decision: str = "reference"):
     """auto_degree's selection (polyprec.py:171-190): the largest d <= cap
     whose order-(d+1) Gram block factors with finite y, each order factored
-    on its own as the reference does -- natively (pg_host_degree_select,
-    top-down, stopping at the first success), then the degree-0 rule."""
-    d, y = _lib.host_degree_select(full.G, full.rhs, cap)
+    on its own as the reference does, then the degree-0 rule.  "reference":
+    the reference's loop over every d with its Cholesky; "exact": natively
+    (pg_host_degree_select, top-down, stopping at the first success)."""
+    if decision == "exact":
+        d, y = _lib.host_degree_select(full.G, full.rhs, cap)
+    else:
+        d, y = -1, None
+        for dd in range(1, cap + 1):
+            yy, piv = _factor(GramSystem(full.G[:dd + 1, :dd + 1], full.rhs[:dd + 1]), decision)
+            if not piv and np.all(np.isfinite(yy)):
+                d, y = dd, yy
     if d >= 1:
         return PolyCoefficients(d, y, seed_norm, seed_mode)
-    y0, pivot = _lib.host_cholesky(full.G[:1, :1], full.rhs[:1])
+    y0, pivot = _factor(GramSystem(full.G[:1, :1], full.rhs[:1]), decision)
     if pivot:
         y0 = np.zeros(1)  # op v0 vanished; p = 0 (polyprec.py:186-187)
     return PolyCoefficients(0, y0, seed_norm, seed_mode)
 
 
 def build_poly_or_auto(op, v0, deg: int, counters: CostCounters,
-                       seed_mode: str = "unspecified"):
+                       seed_mode: str = "unspecified", decision: str = "reference"):
     """Degree policy for requested degrees beyond what the power basis can
     build: the degree-``deg`` polynomial if its Gram system
     factors, else auto-degree selection with cap ``deg``.  Returns
@@ -186,18 +231,17 @@ def build_poly_or_auto(op, v0, deg: int, counters: CostCounters,
     The reference has no such helper; the CPU baseline runs the same policy
     (oracle.degree_policy_shared)."""
     if deg < 1:
-        return build_poly(op, v0, deg, counters, seed_mode), None
-    # the tall-skinny kernels take PG_KMAX columns: a request past that is
-    # decided on the leading KMAX-2 degrees (a failing leading Gram block
-    # fails every larger one; in practice the exact decision stops near 20)
-    deg = min(deg, KMAX - 2)
-    Gfull, seed_norm = _device_power_gram(op, v0, deg + 1, counters)
+        return build_poly(op, v0, deg, counters, seed_mode, decision), None
+    if deg + 2 > KMAX:
+        raise ParameterError(f"degree {deg} needs {deg + 2} power columns; the tall-skinny "
+                             f"kernels take at most {KMAX}")
+    Gfull, seed_norm = _device_power_gram(op, v0, deg + 1, counters, decision)
     counters.scalar_dots += 1
     full = _normal_equations(Gfull, deg, counters)
-    y, pivot = _lib.host_cholesky(full.G, full.rhs)
+    y, pivot = _factor(full, decision)
     if not pivot:
         return PolyCoefficients(deg, y, seed_norm, seed_mode), None
-    return _select_degree(full, deg, seed_norm, seed_mode), pivot
+    return _select_degree(full, deg, seed_norm, seed_mode, decision), pivot
 
 
 def build_poly_arnoldi(op, v0, deg: int, counters: CostCounters | None = None,
