@@ -7,6 +7,7 @@ counters by the reference's laws, history rows in the same format.  GPU only."""
 import json
 import os
 
+import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
