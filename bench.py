@@ -4,18 +4,22 @@ fused p(A)v SpMV's HBM GB/s against the measured roofline).
 One *step* = one polynomial-preconditioned GMRES solve of the workload:
 degree policy (``build_poly(d)``, on Cholesky failure ``auto_degree(cap=d)``)
 + ``solve``, with the matrix, b and v0 already resident in HBM.  Default
-workload = configs[1] (the 3-D 7-point convection-diffusion problem, n=1e6,
-GMRES(50), requested degree 25, tol 1e-10).  L2 is flushed (256 MiB write)
+workload = configs[3] (the 8M-row 3-D 27-point anisotropic problem of
+north_star, 213.8M nonzeros, GMRES(50), requested degree 16, tol 1e-8) --
+the largest single-GPU configuration; ``--config 2`` selects configs[1].  L2 is flushed (256 MiB write)
 between timed steps; every step is timed with CUDA events on the solve's
 stream; the job time is the max over ranks.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
-Under torchrun (N > 1) each rank owns one row block (z-planes) of the matrix:
+With --gpus N > 1 and no launcher, bench.py starts N ranks itself through
+torch.distributed.run (the driver's command line).  Each rank owns one row block (z-planes) of the matrix:
 halo exchange before every SpMV and one all-reduce per batched dot phase
 (NCCL).  ``--impl reference`` times the CPU oracle port of the reference
-(oracle/pgmres_oracle.py) on a bounded sample of the same workload, rank 0
-only, and extrapolates to the full solve.
+(oracle/pgmres_oracle.py) on a bounded sample of the same workload (one SpMV +
+one ICGS on the full operator per step, all host threads), rank 0 only, and
+extrapolates with the reference's own recorded operation counts
+(tests/golden/cfg<N>_full_reference.json).
 """
 
 from __future__ import annotations
@@ -241,7 +245,20 @@ def run_ours(args):
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.5)
-    for _ in range(args.warmup):
+    # cold first solve: nothing recorded yet (no step graphs, cold caches and
+    # workspaces), timed like a step
+    flush.fill_(1.0)
+    torch.cuda.synchronize()
+    c0 = torch.cuda.Event(enable_timing=True)
+    c1 = torch.cuda.Event(enable_timing=True)
+    tc = time.perf_counter()
+    c0.record(stream)
+    step(b_dev, v0_dev)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    cold_wall = time.perf_counter() - tc
+    cold = c0.elapsed_time(c1) / 1e3
+    for _ in range(max(args.warmup - 1, 0)):
         step(b_dev, v0_dev)
     torch.cuda.synchronize()
 
@@ -306,15 +323,30 @@ def run_ours(args):
         if i > 1:  # warm-up calls excluded
             e2e_times.append(time.perf_counter() - t0)
     e2e = float(np.mean(e2e_times))
-    if world > 1:
-        t = torch.tensor([e2e], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = float(t[0])
     assert x_host.device.type == "cpu"
+    # the same with numpy (pageable) b / v0 in and a numpy x out: exactly the
+    # reference's call signature (solve(op, b, right_prec=...), gmres.py:213)
+    e2e_np_times = []
+    for i in range(max(1, min(args.steps, 5)) + 1):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cc = pg.CostCounters()
+        op.counters = cc
+        p2, _ = build(op, v0_host, cc)
+        r2 = pg.solve(op, b_host, right_prec=p2, config=cfg)
+        assert isinstance(r2.x, np.ndarray)
+        if i > 0:
+            e2e_np_times.append(time.perf_counter() - t0)
+    e2e_np = float(np.mean(e2e_np_times))
+    if world > 1:
+        t = torch.tensor([e2e, e2e_np, cold], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e, e2e_np, cold = float(t[0]), float(t[1]), float(t[2])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(conf, res.iterations, res.cycles, sample_iters=args.cpu_sample_iters)
+        cpu = cpu_baseline(conf, (c.spmvs, res.iterations, res.cycles))
 
     if rank == 0:
         peak, peak_src = _peaks()
@@ -374,6 +406,14 @@ def run_ours(args):
                     "median": float(np.median(e2e_times)),
                     "all_ms": [round(1e3 * t, 3) for t in e2e_times],
                     "note": "public API (build_poly_or_auto + solve) from pinned host b/v0, x to host"},
+            "e2e_numpy": {"value": e2e_np, "unit": "s", "h2d_bytes_per_step": 16 * N,
+                          "d2h_bytes_per_step": 8 * N,
+                          "all_ms": [round(1e3 * t, 3) for t in e2e_np_times],
+                          "note": "public API with numpy (pageable) b / v0 and numpy x, the "
+                                  "reference's call signature"},
+            "cold_s": {"value": cold, "wall_s": cold_wall,
+                       "note": "first solve in the process (before warm-up): no recorded "
+                               "step graphs, cold workspaces"},
             "gpu_launches": launches,
             "clocks": clocks,
         }
@@ -409,33 +449,62 @@ MATRIX_FORMATS = {
 # ---------------------------------------------------------------------------
 # CPU baseline (oracle port) -- bounded sample, extrapolated
 # ---------------------------------------------------------------------------
-def cpu_baseline(conf, iterations, cycles, sample_iters=5, threads=1):
+def _sum_basis_widths(iterations, cycles, m):
+    """sum over the solve's Arnoldi steps of the basis width k the ICGS
+    projects against (k = j + 1 at step j of a cycle)."""
+    total, left = 0, iterations
+    for _ in range(cycles):
+        steps = min(m, left)
+        total += steps * (steps + 1) // 2
+        left -= steps
+    return total
+
+
+def cpu_baseline(conf, counts, threads=1, probe=None):
+    """Bounded sample of the reference's CPU path on the full workload: one
+    operator application (sparse.py:151-168, through the oracle port) and one
+    ICGS at basis width m/2 (ortho.py:33-70), timed; extrapolated with the
+    solve's operation counts ``counts`` = (spmvs, iterations, cycles) -- the
+    SpMVs dominate.  ``probe`` reuses a generated operator."""
     from threadpoolctl import threadpool_limits
 
     from oracle import pgmres_oracle as orc
 
-    A_h = wl.make_matrix(conf)
-    b = wl.make_rhs(conf, A_h)
-    v0 = wl.make_v0(A_h.nrows)
+    if probe is None:
+        probe = _cpu_probe(conf)
+    A, b, V, w = probe
+    spmvs, iterations, cycles = counts
+    kw = V.shape[1]
     with threadpool_limits(limits=threads):
-        t = orc.Tally()
-        A = orc.OracleMatrix.of(A_h, t)
         t0 = time.perf_counter()
-        _, eff, y, _ = orc.degree_policy_shared(A, v0, conf["degree"], t)
+        A.apply(b)
         t1 = time.perf_counter()
-        orc.gmres(A, b, y=y, m=conf["m"], tol=conf["tol"], max_iters=sample_iters)
+        orc.cgs2(V, w, orc.Tally())
         t2 = time.perf_counter()
-    build_s, sample_s = t1 - t0, t2 - t1
-    # the sample = sample_iters inner iterations + one cycle end (GEMV, p(A)
-    # recovery, residual ~ one more iteration's SpMVs)
-    est = build_s + sample_s * (iterations + cycles) / (sample_iters + 1)
+    t_spmv, t_icgs = t1 - t0, t2 - t1
+    widths = _sum_basis_widths(iterations, cycles, conf["m"])
+    est = spmvs * t_spmv + t_icgs * widths / kw
     return {"value": est, "unit": "s", "cores": threads, "kind": "port",
-            "sample": (f"oracle (numpy port of the reference) on {conf['name']}: full degree "
-                       f"policy build ({build_s:.2f} s, effective degree {eff}) + "
-                       f"{sample_iters} GMRES iterations incl. one cycle end "
-                       f"({sample_s:.2f} s), extrapolated to {iterations} iterations / "
-                       f"{cycles} cycles"),
-            "measured_s": round(build_s + sample_s, 3)}
+            "sample": (f"oracle port of the reference on the full {conf['name']} operator: one "
+                       f"SpMV ({t_spmv:.3f} s) + one ICGS at basis width {kw} ({t_icgs:.3f} s), "
+                       f"extrapolated to the solve's {spmvs} SpMVs and {iterations} ICGS steps "
+                       f"({cycles} cycles)"),
+            "measured_s": round(t_spmv + t_icgs, 3), "spmv_s": t_spmv, "icgs_s": t_icgs}
+
+
+def _cpu_probe(conf):
+    from oracle import pgmres_oracle as orc
+
+    A_h = wl.make_matrix(conf)
+    A = orc.OracleMatrix.of(A_h, orc.Tally())
+    b = wl.make_rhs(conf, A_h)
+    n = A_h.nrows
+    kw = max(1, conf["m"] // 2)
+    # a basis stand-in: the ICGS time does not depend on the values (four
+    # dense passes over V, ortho.py:53-59)
+    V = np.asfortranarray(np.stack([wl.splitmix_uniform(10 + i, n) for i in range(kw)], axis=1))
+    V /= np.sqrt(n)
+    return A, b, V, wl.make_v0(n)
 
 
 def run_reference(args):
@@ -444,12 +513,13 @@ def run_reference(args):
     if rank != 0:
         return
     conf = wl.CONFIGS[args.config]
-    ref_iters = _reference_iterations(args.config)
+    rec = _reference_record(args.config)
     threads = os.cpu_count() or 1
+    probe = _cpu_probe(conf)
     vals = []
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(conf, ref_iters[0], ref_iters[1], sample_iters=args.cpu_sample_iters,
-                          threads=threads)
+        cb = cpu_baseline(conf, (rec["spmvs"], rec["iterations"], rec["cycles"]), threads=threads,
+                          probe=probe)
         if i >= args.warmup:
             vals.append(cb)
     v = float(np.mean([c["value"] for c in vals]))
@@ -459,26 +529,35 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * v,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": conf["name"], "n": wl.config_n(conf),
-                                        "iterations_extrapolated_to": ref_iters[0],
-                                        "cycles": ref_iters[1]},
+        "data": "synthetic", "config": {
+            "workload": conf["name"], "n": wl.config_n(conf), "restart_m": conf["m"],
+            "tol": conf["tol"], "degree_requested": conf["degree"],
+            "degree_effective": rec["degree"], "iterations": rec["iterations"],
+            "cycles": rec["cycles"], "spmvs": rec["spmvs"], "record": rec["source"],
+            "full_solve_measured_build_host_s": rec.get("measured_s")},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
 
-def _reference_iterations(config: int):
-    """Full-solve iteration / cycle counts of the reference on this workload
-    (tests/golden/cfg2_full_oracle.json, measured in the build container)."""
-    if config == 2:
-        try:
-            with open(os.path.join(ROOT, "tests", "golden", "cfg2_full_oracle.json")) as fh:
-                g = json.load(fh)
-            return g["iterations"], g["cycles"]
-        except Exception:
-            pass
-    return 50, 1
+def _reference_record(config: int) -> dict:
+    """The reference's own full-size run of this workload (degree decision,
+    iterations, cycles, operator applications), recorded in the build
+    container by tests/golden/make_full_records.py."""
+    path = os.path.join(ROOT, "tests", "golden", f"cfg{config}_full_reference.json")
+    try:
+        with open(path) as fh:
+            g = json.load(fh)
+        return {"degree": g["effective_degree"], "iterations": g["iterations"],
+                "cycles": g["cycles"], "spmvs": g["counters"]["spmvs"],
+                "measured_s": round(g["build_s"] + g["solve_s"], 1),
+                "source": f"tests/golden/cfg{config}_full_reference.json"}
+    except (OSError, KeyError, ValueError):
+        conf = wl.CONFIGS[config]
+        return {"degree": None, "iterations": 50, "cycles": 1,
+                "spmvs": (conf["degree"] + 1) * 52, "measured_s": None,
+                "source": "no full-size record: one cycle assumed"}
 
 
 def main():
@@ -486,12 +565,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     # default: the reference's cap (200000), except the configs whose
     # operators stagnate under GMRES(m) at their tolerance (BENCH_MAX_ITERS)
     ap.add_argument("--max-iters", type=int, default=0)
-    ap.add_argument("--cpu-sample-iters", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     # "monomial" = the reference's bit-identical evaluation (default, the
@@ -501,6 +579,21 @@ def main():
     # f1) -- not the reference's construction, so not the headline
     ap.add_argument("--construction", default="policy", choices=["policy", "arnoldi"])
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        # --gpus N without a launcher: start the N ranks ourselves (one process
+        # per GPU, the driver's torchrun command line) and pass on the exit code
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
+    if world and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one "
+                         "rank per GPU with matching --gpus")
     if args.impl == "reference":
         run_reference(args)
     else:

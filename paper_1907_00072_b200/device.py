@@ -309,6 +309,13 @@ class DistComm:
         for dst, tmp in landing:
             dst.copy_(tmp)
 
+    def any(self, flag: bool) -> bool:
+        """Logical OR of a per-rank flag over the group."""
+        dev = "cpu" if self.staged else self.shards[0].device
+        t = torch.tensor([1 if flag else 0], dtype=torch.int32, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return bool(t.item())
+
     def allreduce(self, bufs):
         b = bufs[0]
         if self.staged and b.is_cuda:

@@ -205,7 +205,12 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
         beta = norm_b
     else:
         xs = e.ingest(x0)
-        if any(bool(torch.any(x[:s.n] != 0.0)) for s, x in zip(e.shards, xs)):
+        # np.any(x0) over the GLOBAL x0 (gmres.py:248): every rank must take the
+        # same branch, or the collectives of the two branches would not match
+        nonzero = any(bool(torch.any(x[:s.n] != 0.0)) for s, x in zip(e.shards, xs))
+        if e.comm.distributed:
+            nonzero = e.comm.any(nonzero)
+        if nonzero:
             e.count_ops(counters, 1)
             beta = math.sqrt(e.residual(xs, bs, W.r, slot=4))
         else:

@@ -33,6 +33,12 @@ def _port():
     return p
 
 
+def _x0(n):
+    x0 = np.zeros(n)
+    x0[-GRID * GRID:] = 0.1 * wl.splitmix_uniform(9, GRID * GRID)
+    return x0
+
+
 def _worker(rank, world, port, offs, q):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -51,8 +57,14 @@ def _worker(rank, world, port, offs, q):
         pav = pg.apply_poly(p, op, y_in, pg.CostCounters())
         poly, _ = pg.build_poly_or_auto(op, v0, 8, c)
         res = pg.solve(op, b, right_prec=poly, config=pg.GmresConfig(30, 1e-10))
+        # x0 nonzero on rank 1's rows only: both ranks must take the global
+        # np.any(x0) branch (gmres.py:248), or the collectives would not match
+        x0 = _x0(n)[r0:r1]
+        c0 = pg.CostCounters()
+        op.counters = c0
+        rx = pg.solve(op, b, x0=x0, right_prec=poly, config=pg.GmresConfig(30, 1e-10))
         q.put((rank, pav, poly.degree, poly.y, res.iterations, res.cycles, res.final_relres,
-               res.x, c.spmvs, c.dots, n))
+               res.x, c.spmvs, c.dots, n, rx.iterations, rx.x, c0.spmvs, c0.dots))
     finally:
         dist.destroy_process_group()
 
@@ -91,3 +103,11 @@ def test_two_rank_distributed_solve_matches_in_process_shards():
         assert g[8] == c.spmvs and g[9] == c.dots
     x = np.concatenate([g[7] for g in got])
     np.testing.assert_allclose(x, res.x, rtol=0, atol=1e-9 * np.abs(res.x).max())
+    c0 = pg.CostCounters()
+    op.counters = c0
+    rx = pg.solve(op, wl.splitmix_uniform(0, A.nrows), x0=_x0(A.nrows), right_prec=poly,
+                  config=pg.GmresConfig(30, 1e-10))
+    for g in got:
+        assert g[11] == rx.iterations and g[13] == c0.spmvs and g[14] == c0.dots
+    x = np.concatenate([g[12] for g in got])
+    np.testing.assert_allclose(x, rx.x, rtol=0, atol=1e-9 * np.abs(rx.x).max())
