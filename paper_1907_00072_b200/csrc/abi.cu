@@ -660,7 +660,10 @@ PG_API int pg_matrix_stats(const pg_matrix* m, int64_t* s) {
     s[8] = m->col8 ? 1 : 4;  // bytes per stored column entry
     s[9] = m->val8 ? 1 : 8;  // bytes per stored value entry
     // the kernel launch_sell picks for 16-byte aligned vectors (spmv.cu)
-    s[11] = pattern_kernel(m) ? 5
+    int mk;
+    int64_t mS, mg;
+    s[11] = march_shape(m, &mk, &mS, &mg) ? 8
+            : pattern_kernel(m) ? 5
             : (m->pair8 && m->wtab && m->rpat && winpat_enabled()) ? 6
             : opat_kernel(m) ? 7
             : m->pair8 ? (m->wtab ? 3 : (m->stride8 > 0 && m->stride8 <= 256) ? 4 : 2)

@@ -289,6 +289,9 @@ struct ChainStep {
   int flags;
   double c1, c2, c3;
 };
+// The plane-marching stencil kernel handles this matrix (march.cu): kind
+// (27, 7, 9, 5), plane stride S and row stride g of its master pattern.
+bool march_shape(const pg_matrix* m, int* kind, int64_t* S, int64_t* g);
 // pg_spmv & co. run the row-pattern kernel on this matrix (spmv.cu).
 bool pattern_kernel(const pg_matrix* m);
 // pg_spmv & co. run the offset-pattern kernel on this matrix (spmv.cu).

@@ -332,4 +332,10 @@ __device__ __forceinline__ double row_sum_omaster(uint32_t mask, const PatMaster
   return acc;
 }
 
+// Plane-marching SpMV (march.cu): issues the pass and returns true when the
+// matrix is a row-pattern stencil it handles (march_shape), else false.
+template <int MODE>
+bool march_launch(const pg_matrix* m, const double* x, Epi e, pg_workspace* ws, double* nsq,
+                  cudaStream_t st);
+
 }  // namespace pg

@@ -870,6 +870,8 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
   }
   const int dev = m->device;
   PG_REQUIRE(dev >= 0 && dev < 64, PG_ERR_PARAMETER, "device ordinal out of range");
+  // stencil row patterns: the plane-marching kernel (march.cu)
+  if (march_launch<MODE>(m, x, e, ws, nsq, st)) return;
   double* part = ws ? ws->partials : nullptr;
   unsigned* cnt = ws ? ws->counter : nullptr;
   static int sms[64] = {};

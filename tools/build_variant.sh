@@ -7,7 +7,7 @@ root=$(cd "$(dirname "$0")/.." && pwd)
 out=$root/variants_tmp/$name
 mkdir -p "$out"
 flags="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden,-ffp-contract=off -I $root/include"
-for f in abi spmv ortho host ilu step chain; do
+for f in abi spmv ortho host ilu step chain blasorder march; do
   nvcc $flags "$@" -c "$root/paper_1907_00072_b200/csrc/$f.cu" -o "$out/$f.o" &
 done
 wait
