@@ -241,9 +241,11 @@ static std::vector<int32_t> build_window_plan(const std::vector<int64_t>& offs,
   int64_t b8 = 0;
   for (int64_t s0 = 0; s0 < n_slices; s0 += per_blk)
     b8 = std::max(b8, sp8[std::min(s0 + per_blk, n_slices)] - sp8[s0]);
-  // window | pair stream | 2 epilogue operand slices | row lengths | widths
-  const int64_t stage = ((8 * total + 127) / 128) * 128 + b8 + 20 * kWinRows + 128;
-  if (stage > kWinMaxStageBytes) return {};
+  // a row-pattern stage is the window + one pattern id per row; a pair-stream
+  // stage adds the stream, 2 epilogue operand slices, row lengths and widths
+  const int64_t win_bytes = ((8 * total + 127) / 128) * 128;
+  if (win_bytes + kWinRows > kWinMaxStageBytes) return {};
+  m->win_pair_fits = win_bytes + b8 + 20 * kWinRows + 128 <= kWinMaxStageBytes;
   std::vector<int32_t> wtab(256, 0);
   int32_t start = 0;
   for (size_t g = 0; g < lo.size(); ++g) {

@@ -82,6 +82,7 @@ struct pg_matrix {
   void* ptab;          // [256] PairEnt {value, window byte offset, column offset}
   int n_wgrp, win_elems;
   int win_b8;          // largest per-block byte span of each packed stream
+  int win_pair_fits;   // the pair-stream stage (window + stream + operands) fits a ring slot
   int32_t wlo[32], wstart[32], wlen[32];
   // row-pattern dictionary (abi.cu build_patterns): every row is one of
   // n_pat <= 256 distinct sequences of (column offset, value) pairs; rpat is

@@ -429,14 +429,14 @@ __global__ void __launch_bounds__(kSellThreads, PG_PAT_MIN_BLOCKS)
 }
 
 // ---------------------------------------------------- windowed dictionary --
-// Dictionary-compressed matrices in natural row order (stencils): a block
-// owns kWinRows consecutive rows (8 slices).  Their x reads all fall inside
+// Dictionary-compressed matrices in natural row order (stencils): a ring
+// stage holds kWinRows consecutive rows (kWinRows / 32 slices).  Their x reads all fall inside
 // the few group windows of the matrix's window plan (abi.cu
 // build_window_plan), and their packed index words are one contiguous byte
 // range per stream.  One thread streams all of it for the block's next row
 // blocks into a shared-memory ring (WinArgs::stages deep) with cp.async.bulk (TMA)
 // completing on an mbarrier, so a stage carries ~15-35 KB of loads in flight
-// per copy batch; the 256 row threads then sum their rows from shared memory
+// per copy batch; the row threads then sum their rows from shared memory
 // only.  Window elements outside [0, ncols) are never referenced by a stored
 // entry and are simply not copied.  Same sequential mul-then-add order per
 // row: bitwise equal to the other kernels.
@@ -588,11 +588,13 @@ __device__ __forceinline__ void win_issue(const SellArgs& a, const WinArgs& wa, 
   }
 }
 
-// Warp-specialised: warp 8 is the producer (one lane issues the copies of
-// the block's row blocks as soon as a ring stage is released), warps 0-7 sum
-// one row per thread from shared memory only -- matrix stream, x window,
-// epilogue operands, row lengths all arrive by TMA -- and release the stage
-// through the `empty` mbarrier.  Global memory is only written (outputs).
+// Warp-specialised: the last warp (kWinRowThreads / 32) is the producer (one
+// lane issues the copies of the block's row blocks as soon as a ring stage is
+// released); the kWinRowThreads row threads sum kWinRPT rows each from shared
+// memory (row-pattern stages: pattern ids + x window by TMA, epilogue
+// operands from global before the wait; pair-stream stages, one row per
+// thread: stream, window, operands, row lengths all by TMA) and release the
+// stage through the `empty` mbarrier.
 // Row threads per block; a row-pattern stage of kWinRows rows gives each
 // row thread kWinRows / kWinRowThreads rows (pair-stream stages: one).
 #ifndef PG_WIN_ROW_THREADS
@@ -617,6 +619,7 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
                     double* partials, unsigned int* counter, double* nsq,
                     const int32_t* __restrict__ pptr, int npat, int nent,
                     const uint32_t* __restrict__ pmask, const PatMaster pm) {
+  static_assert(PAT || kWinRPT == 1, "the pair-stream stage sums one row per thread");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   extern __shared__ __align__(128) unsigned char smem_win[];
   __shared__ PairEnt s_ptab[PAT ? 1 : 256];
@@ -882,8 +885,10 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
   // windowed kernel: long rows (27-point: 1.6x the pair kernel); short rows
   // (7-point) keep the global-gather pair kernel, which is faster there
   const bool win_pat = m->pair8 && m->wtab && aligned && m->rpat && winpat_enabled();
-  // the pair-stream windowed kernel sums one row per thread per stage
-  const bool win_ok = m->pair8 && m->wtab && aligned && (win_pat || kWinRPT == 1);
+  // the pair-stream windowed kernel sums one row per thread per stage (it is
+  // not built when the stage holds kWinRPT > 1 rows per thread)
+  const bool win_ok =
+      m->pair8 && m->wtab && aligned && (win_pat || (kWinRPT == 1 && m->win_pair_fits));
   if (pattern_kernel(m)) {
     int64_t blocks = (a.nlanes + kSellThreads - 1) / kSellThreads;
     static int per_sm = -1;
@@ -934,7 +939,11 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
     if (wa.stages < 2) wa.stages = 2;
     if (wa.stages > kWinMaxStages) wa.stages = kWinMaxStages;
     const size_t smem = (size_t)wa.stages * wa.stage_bytes + tab_bytes;
-    auto kern = !win_pat      ? sell_win_kernel<MODE, false, 0>
+    using WinKern = decltype(&sell_win_kernel<MODE, true, 0>);
+    WinKern pair_kern = nullptr;
+    if constexpr (kWinRPT == 1) pair_kern = sell_win_kernel<MODE, false, 0>;
+    PG_REQUIRE(win_pat || pair_kern, PG_ERR_PARAMETER, "pair-stream windowed kernel not built");
+    auto kern = !win_pat      ? pair_kern
                 : pm.lb == 7  ? sell_win_kernel<MODE, true, 7>
                 : pm.lb == 8  ? sell_win_kernel<MODE, true, 8>
                 : pm.lb == 16 ? sell_win_kernel<MODE, true, 16>
@@ -964,6 +973,11 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
       waves = s ? std::atoi(s) : 1;
     }
     int64_t g = waves > 0 ? (int64_t)sms[dev] * occ_n[pk][MODE][dev] * waves : wa.nblk;
+    // PG_SPMV_WIN_GRID caps the grid (tests: many row blocks per CTA, so the
+    // ring's slot reuse, empty-barrier waits and phase flips all run)
+    static int gcap = -1;
+    if (gcap < 0) gcap = env_or("PG_SPMV_WIN_GRID", 0);
+    if (gcap > 0 && g > gcap) g = gcap;
     if (g > wa.nblk) g = wa.nblk;
     if (MODE == kResid && g > kMaxBlocks) g = kMaxBlocks;
     if (win_pat)

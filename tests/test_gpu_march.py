@@ -134,3 +134,24 @@ assert (op.engine.shards[0].stats["kernel"] == 8) == (os.environ["PG_SPMV_MARCH"
         outs.append((out.split()[1], np.load(path)))
     assert outs[0][0] == outs[1][0]
     assert np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_windowed_ring_wraps_bitwise_in_every_mode():
+    """The windowed TMA-ring kernel with its grid capped at 2 CTAs
+    (PG_SPMV_WIN_GRID): every CTA sweeps many row blocks, so the ring's slot
+    reuse, empty-barrier waits and phase flips run in SpMV, the fused
+    polynomial pass, the residual and the root-product passes -- all bitwise
+    (ragged last stage included)."""
+    code = """
+import sys; sys.path.insert(0, 'tests'); import test_gpu_march as t
+import paper_1907_00072_b200 as pg
+from paper_1907_00072_b200 import workloads as wl
+for g in (20, 23, 31):
+    h = wl.aniso27(g)
+    assert pg.DeviceMatrixOperator(h).engine.shards[0].stats["kernel"] == 6
+    t._check(h)
+    t._check(h, 2)
+print("ok")
+"""
+    for cap in ("1", "2", "3"):
+        assert "ok" in _run_isolated({"PG_SPMV_MARCH": "0", "PG_SPMV_WIN_GRID": cap}, code)
