@@ -47,6 +47,7 @@ extern "C" {
 
 typedef struct pg_matrix pg_matrix;
 typedef struct pg_workspace pg_workspace;
+typedef struct pg_dist pg_dist;
 
 /* ---- library / errors -------------------------------------------------- */
 PG_API int pg_version(void); /* ABI version, currently 1 */
@@ -240,6 +241,53 @@ PG_API int pg_step_graph_create(const pg_matrix* mat, const double* y, int d, do
                                 const double* rc, pg_graph** out);
 PG_API int pg_graph_launch(pg_graph* graph, void* stream);
 PG_API int pg_graph_destroy(pg_graph* graph);
+
+/* ---- row-block shards over NCCL (csrc/dist.cu; SURVEY §8 row e) ------------
+ * One process per GPU.  The halo exchange before every SpMV pass and the
+ * batched CGS2 reductions run as NCCL operations issued from C on the solve's
+ * stream (libnccl dlopen'ed at run time), so an Arnoldi step stays one native
+ * call or one recorded graph per device.  Reductions all-gather every rank's
+ * partials and sum them in rank order: identical on every rank and bitwise
+ * the in-process multi-shard result.  The reference is single-process
+ * (SPEC.md:13); this replaces no reference call but `solve`'s inner loop
+ * (gmres.py:282-316) across shards.
+ * pg_nccl_unique_id: 128-byte ncclUniqueId (rank 0; broadcast it yourself).
+ * pg_dist_create: communicator of `nranks` ranks on `device`.
+ * pg_dist_set_halo: this shard's plan -- sends: peer, count and the local
+ *   rows to pack (concatenated in send order); receives: peer, ghost offset
+ *   (a contiguous range of every vector) and count.
+ * pg_dist_halo: fill d_x's ghost slots.  pg_dist_allreduce: rank-order sum of
+ *   count (<= 2*PG_KMAX + 8) doubles in place.
+ * pg_arnoldi_step_dist / pg_step_graph_create_dist / pg_poly_chain_dist /
+ * pg_power_sequence_dist: pg_arnoldi_step & co. with those exchanges between
+ * the kernels (the operand's ghosts are filled by the call itself). */
+PG_API int pg_nccl_unique_id(void* out, size_t len);
+PG_API int pg_dist_create(const void* uid, int nranks, int rank, int device, pg_dist** out);
+PG_API int pg_dist_set_halo(pg_dist* dist, int nsend, const int* send_peer,
+                            const int64_t* send_count, const int32_t* send_idx, int nrecv,
+                            const int* recv_peer, const int64_t* recv_off,
+                            const int64_t* recv_count);
+PG_API int pg_dist_destroy(pg_dist* dist);
+PG_API int pg_dist_halo(pg_dist* dist, double* d_x, void* stream);
+PG_API int pg_dist_allreduce(pg_dist* dist, double* d_buf, int count, void* stream);
+PG_API int pg_arnoldi_step_dist(const pg_matrix* mat, const double* y, int d, double* d_V,
+                                int64_t ld, int j, double* d_z, double* d_t, double* d_acc,
+                                double* d_w0, double* d_w1, double* d_ring, double* h_ring,
+                                pg_workspace* ws, pg_event* ev_done, pg_event* ev_chain0,
+                                pg_event* ev_chain1, int nroot, const int* rmode, const double* rc,
+                                pg_dist* dist, void* stream);
+PG_API int pg_step_graph_create_dist(const pg_matrix* mat, const double* y, int d, double* d_V,
+                                     int64_t ld, int j, double* d_z, double* d_t, double* d_acc,
+                                     double* d_w0, double* d_w1, double* d_ring, double* h_ring,
+                                     pg_workspace* ws, pg_event* ev_done, pg_event* ev_chain0,
+                                     pg_event* ev_chain1, int nroot, const int* rmode,
+                                     const double* rc, pg_dist* dist, pg_graph** out);
+PG_API int pg_poly_chain_dist(const pg_matrix* mat, const double* y, int d, double* d_x,
+                              const double* d_base, double* d_out, double* d_acc, double* d_w0,
+                              double* d_w1, pg_event* ev_start, pg_event* ev_end, pg_dist* dist,
+                              void* stream);
+PG_API int pg_power_sequence_dist(const pg_matrix* mat, double* d_P, int64_t ld, int ncols,
+                                  pg_dist* dist, void* stream);
 
 /* r = b - A x and the partial sum of r^2 into d_nsq[0] (gmres.py:334-335). */
 PG_API int pg_residual(const pg_matrix* mat, const double* d_x, const double* d_b,

@@ -15,7 +15,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libpgmres.so")
 BUILD = os.path.join(ROOT, "build", "pgmres")
 
-SOURCES = ["abi.cu", "spmv.cu", "ortho.cu", "host.cu", "ilu.cu", "step.cu", "chain.cu", "blasorder.cu", "march.cu"]
+SOURCES = ["abi.cu", "spmv.cu", "ortho.cu", "host.cu", "ilu.cu", "step.cu", "chain.cu", "blasorder.cu", "march.cu", "dist.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -23,6 +23,20 @@ NVCC_FLAGS = [
     "-Xptxas", "-v",
     "-I", INCLUDE,
 ]
+
+
+def _nccl_include():
+    """nccl.h for the types of csrc/dist.cu (libnccl itself is dlopen'ed at
+    run time): torch's wheel copy, else the system header."""
+    try:
+        import nvidia.nccl as nn
+        for base in list(getattr(nn, "__path__", [])):
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except ImportError:
+        pass
+    return "/usr/include"
 
 
 def _nvcc():
@@ -50,7 +64,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", src, "-o", obj]
+        cmd = [nvcc, *NVCC_FLAGS, "-I", _nccl_include(), "-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
@@ -61,7 +75,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
         objs = list(ex.map(compile_one, srcs))
     tmp = LIB + ".tmp"
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{res.stderr}")

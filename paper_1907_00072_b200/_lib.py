@@ -84,6 +84,18 @@ _SIGNATURES = {
                               _p, _p, _i32, _p, _p, C.POINTER(_p)], C.c_int),
     "pg_graph_launch": ([_p, _p], C.c_int),
     "pg_graph_destroy": ([_p], C.c_int),
+    "pg_nccl_unique_id": ([_p, C.c_size_t], C.c_int),
+    "pg_dist_create": ([_p, _i32, _i32, _i32, C.POINTER(_p)], C.c_int),
+    "pg_dist_set_halo": ([_p, _i32, _p, _p, _p, _i32, _p, _p, _p], C.c_int),
+    "pg_dist_destroy": ([_p], C.c_int),
+    "pg_dist_halo": ([_p, _p, _p], C.c_int),
+    "pg_dist_allreduce": ([_p, _p, _i32, _p], C.c_int),
+    "pg_arnoldi_step_dist": ([_p, _p, _i32, _p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p,
+                              _p, _p, _i32, _p, _p, _p, _p], C.c_int),
+    "pg_step_graph_create_dist": ([_p, _p, _i32, _p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _p,
+                                   _p, _p, _p, _i32, _p, _p, _p, C.POINTER(_p)], C.c_int),
+    "pg_poly_chain_dist": ([_p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], C.c_int),
+    "pg_power_sequence_dist": ([_p, _p, _i64, _i32, _p, _p], C.c_int),
     "pg_ilu0_factor": ([_i64, _p, _p, _p, _d, _p, _p, _pi64, C.POINTER(C.c_int)], C.c_int),
     "pg_ilu_create": ([_i32, _i64, _p, _p, _p, _p, C.POINTER(_p)], C.c_int),
     "pg_ilu_destroy": ([_p], C.c_int),

@@ -511,15 +511,6 @@ static void build_dictionaries(const SellHost& h, const int32_t* col, const doub
   }
 }
 
-struct DeviceScope {
-  int prev = 0;
-  explicit DeviceScope(int dev) {
-    PG_CUDA(cudaGetDevice(&prev));
-    PG_CUDA(cudaSetDevice(dev));
-  }
-  ~DeviceScope() { cudaSetDevice(prev); }
-};
-
 }  // namespace pg
 
 using namespace pg;

@@ -247,6 +247,22 @@ __device__ __forceinline__ void pdl_entry() {
 }
 
 bool pdl_enabled();
+
+// Distributed shards (dist.cu): fill x's ghost slots from the neighbours;
+// sum count doubles over the ranks in rank order, in place.  No-ops for a
+// null communicator.
+void dist_halo(pg_dist* d, double* x, cudaStream_t st);
+void dist_allreduce(pg_dist* d, double* buf, int count, cudaStream_t st);
+
+// Make `dev` current for a scope (restores the caller's device).
+struct DeviceScope {
+  int prev = 0;
+  explicit DeviceScope(int dev) {
+    PG_CUDA(cudaGetDevice(&prev));
+    PG_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceScope() { cudaSetDevice(prev); }
+};
 // true while this thread records launches into a CUDA graph
 extern thread_local bool g_capturing;
 

@@ -31,9 +31,12 @@ void ok(int code) {
   }
 }
 
-// d fused monomial passes, out = (base +) p(A) x  (Engine.poly)
+// d fused monomial passes, out = (base +) p(A) x  (Engine.poly); with a
+// distributed shard (dist) the ghost slots of each pass's operand are filled
+// first (dist.cu; x itself must already hold its ghosts)
 void poly_chain(const pg_matrix* m, const double* y, int d, const double* x, const double* base,
-                double* out, double* acc, double* w0, double* w1, void* st) {
+                double* out, double* acc, double* w0, double* w1, void* st,
+                pg_dist* dist = nullptr) {
   if (d == 0) {
     ok(pg_scale_add(base, y[0], x, m->nrows, out, st));
     return;
@@ -44,6 +47,7 @@ void poly_chain(const pg_matrix* m, const double* y, int d, const double* x, con
     const bool last = k == d;
     const int flags = (k == 1 ? PG_PASS_FIRST : 0) | (last ? 0 : PG_PASS_WRITE_W);
     double* nxt = ws[k & 1];
+    if (k > 1) pg::dist_halo(dist, const_cast<double*>(cur), pg::as_stream(st));
     ok(pg_poly_pass(m, cur, k > 1 ? acc : nullptr, last ? base : nullptr, last ? out : acc,
                     last ? nullptr : nxt, y[0], y[k], flags, st));
     cur = nxt;
@@ -178,7 +182,8 @@ namespace {
 // temporary t, REAL / PAIR_B the next product (ping-pong w0 / w1), the
 // PG_ROOT_RESID pass writes z.
 void roots_chain(const pg_matrix* m, int nroot, const int* rmode, const double* rc,
-                 const double* v, double* z, double* t, double* w0, double* w1, void* st) {
+                 const double* v, double* z, double* t, double* w0, double* w1, void* st,
+                 pg_dist* dist = nullptr) {
   const double* prod = v;
   double* bufs[2] = {w0, w1};
   int nb = 0;
@@ -186,6 +191,7 @@ void roots_chain(const pg_matrix* m, int nroot, const int* rmode, const double* 
     const int mode = rmode[q], kind = mode & 3;
     const bool resid = (mode & PG_ROOT_RESID) != 0;
     const double* x = kind == PG_ROOT_PAIR_B ? t : prod;
+    if (q > 0) pg::dist_halo(dist, const_cast<double*>(x), pg::as_stream(st));
     const double* p = kind == PG_ROOT_PAIR_B ? prod : nullptr;
     double* w = resid ? z : (kind == PG_ROOT_PAIR_A ? t : bufs[nb]);
     ok(pg_root_pass(m, x, p, resid ? v : nullptr, nullptr, w, rc[3 * q], rc[3 * q + 1],
@@ -252,22 +258,26 @@ void arnoldi_step_body(const pg_matrix* mat, const double* y, int d, double* d_V
                        int j, double* d_z, double* d_t, double* d_acc, double* d_w0,
                        double* d_w1, double* d_ring, double* h_ring, pg_workspace* ws,
                        pg_event* ev_done, pg_event* ev_chain0, pg_event* ev_chain1,
-                       int nroot, const int* rmode, const double* rc, void* stream) {
+                       int nroot, const int* rmode, const double* rc, void* stream,
+                       pg_dist* dist = nullptr) {
+    cudaStream_t cst = as_stream(stream);
     PG_REQUIRE(mat && d_V && d_z && d_ring && h_ring && ws && ev_done, PG_ERR_PARAMETER,
                "null argument");
     const int k = j + 1;
-    PG_REQUIRE(j >= 0 && k < PG_KMAX && ld >= mat->nrows, PG_ERR_PARAMETER,
+    PG_REQUIRE(j >= 0 && k < PG_KMAX && ld >= mat->ncols, PG_ERR_PARAMETER,
                "step index out of range");
     const int64_t n = mat->nrows;
     const double* vj = d_V + (int64_t)j * ld;
+    // the operand's ghost slots (distributed shards; no-op otherwise)
+    dist_halo(dist, const_cast<double*>(vj), cst);
     // z = A p(A) v_j  (gmres.py:112-113, 283), or z = A v_j without a polynomial
     if (nroot > 0) {
       PG_REQUIRE(rmode && rc && d_acc && d_w0 && d_w1, PG_ERR_PARAMETER,
                  "root plan needs its scratch vectors");
       record(ev_chain0, stream);
       std::vector<ChainStep> steps = roots_steps(nroot, rmode, rc, vj, d_z, d_acc, d_w0, d_w1);
-      if (!chain_launch(mat, steps.data(), nroot, ws, as_stream(stream)))
-        roots_chain(mat, nroot, rmode, rc, vj, d_z, d_acc, d_w0, d_w1, stream);
+      if (dist || !chain_launch(mat, steps.data(), nroot, ws, cst))
+        roots_chain(mat, nroot, rmode, rc, vj, d_z, d_acc, d_w0, d_w1, stream, dist);
       record(ev_chain1, stream);
     } else if (d >= 0) {
       PG_REQUIRE(y && d_t, PG_ERR_PARAMETER, "polynomial step needs y and t");
@@ -278,11 +288,12 @@ void arnoldi_step_body(const pg_matrix* mat, const double* y, int d, double* d_V
       std::vector<ChainStep> steps = poly_steps(y, d, vj, nullptr, d_t, d_acc, d_w0, d_w1);
       steps.push_back(ChainStep{PG_CHAIN_SPMV, d_t, nullptr, nullptr, d_z, nullptr, 0.0, 0.0, 0,
                                 0.0, 0.0, 0.0});
-      if (d > 0 && chain_launch(mat, steps.data(), (int)steps.size(), ws, as_stream(stream))) {
+      if (!dist && d > 0 && chain_launch(mat, steps.data(), (int)steps.size(), ws, cst)) {
         record(ev_chain1, stream);
       } else {
-        poly_chain(mat, y, d, vj, nullptr, d_t, d_acc, d_w0, d_w1, stream);
+        poly_chain(mat, y, d, vj, nullptr, d_t, d_acc, d_w0, d_w1, stream, dist);
         record(ev_chain1, stream);
+        dist_halo(dist, d_t, cst);
         ok(pg_spmv(mat, d_t, d_z, stream));
       }
     } else {
@@ -293,9 +304,13 @@ void arnoldi_step_body(const pg_matrix* mat, const double* y, int d, double* d_V
     double* c2 = d_ring + PG_KMAX;
     double* nsq = d_ring + 2 * PG_KMAX;
     double* col = d_V + (int64_t)k * ld;
+    // distributed: one batched reduction per phase (all-gather + rank-order sum)
     ok(pg_cgs2_phase1(d_V, ld, k, d_z, n, c1, ws, stream));
+    dist_allreduce(dist, c1, k, cst);
     ok(pg_cgs2_phase2(d_V, ld, k, d_z, n, c1, c2, ws, stream));
+    dist_allreduce(dist, c2, k, cst);
     ok(pg_cgs2_phase3(d_V, ld, k, d_z, n, c1, c2, col, nsq, ws, stream));
+    dist_allreduce(dist, nsq, 1, cst);
     // normalise into column k and publish the scalars straight into the
     // pinned host ring (no copy-engine transfer between steps), or copy them
     double* h_dev = mapped_host(h_ring);
@@ -315,6 +330,52 @@ struct pg_graph {
   cudaGraphExec_t exec;
   int device;
 };
+
+namespace {
+
+// Record body(stream) into an instantiated graph: stream capture on a private
+// stream; launches inside carry plain edges, event records become external
+// nodes (record()), NCCL operations are captured like kernels.
+template <class Body>
+void capture_step(const pg_matrix* mat, pg_graph** out, Body body) {
+  PG_REQUIRE(out && mat, PG_ERR_PARAMETER, "null argument");
+  *out = nullptr;
+  int prev = 0;
+  PG_CUDA(cudaGetDevice(&prev));
+  PG_CUDA(cudaSetDevice(mat->device));
+  cudaStream_t cs = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t err = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  if (err == cudaSuccess) err = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  if (err != cudaSuccess) {
+    if (cs) cudaStreamDestroy(cs);
+    cudaSetDevice(prev);
+    throw Error(PG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(err));
+  }
+  g_capturing = true;
+  try {
+    body(static_cast<void*>(cs));
+  } catch (...) {
+    g_capturing = false;
+    cudaStreamEndCapture(cs, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    cudaStreamDestroy(cs);
+    cudaSetDevice(prev);
+    throw;
+  }
+  g_capturing = false;
+  err = cudaStreamEndCapture(cs, &graph);
+  if (err == cudaSuccess) err = cudaGraphInstantiate(&exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  cudaStreamDestroy(cs);
+  cudaSetDevice(prev);
+  if (err != cudaSuccess)
+    throw Error(PG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(err));
+  *out = new pg_graph{exec, mat->device};
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -336,42 +397,10 @@ PG_API int pg_step_graph_create(const pg_matrix* mat, const double* y, int d, do
                                 pg_event* ev_chain1, int nroot, const int* rmode,
                                 const double* rc, pg_graph** out) {
   return guard([&] {
-    PG_REQUIRE(out && mat, PG_ERR_PARAMETER, "null argument");
-    *out = nullptr;
-    int prev = 0;
-    PG_CUDA(cudaGetDevice(&prev));
-    PG_CUDA(cudaSetDevice(mat->device));
-    cudaStream_t cs = nullptr;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    cudaError_t err = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
-    if (err == cudaSuccess) err = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
-    if (err != cudaSuccess) {
-      if (cs) cudaStreamDestroy(cs);
-      cudaSetDevice(prev);
-      throw Error(PG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(err));
-    }
-    g_capturing = true;
-    try {
+    capture_step(mat, out, [&](void* cs) {
       arnoldi_step_body(mat, y, d, d_V, ld, j, d_z, d_t, d_acc, d_w0, d_w1, d_ring, h_ring, ws,
                         ev_done, ev_chain0, ev_chain1, nroot, rmode, rc, cs);
-    } catch (...) {
-      g_capturing = false;
-      cudaStreamEndCapture(cs, &graph);
-      if (graph) cudaGraphDestroy(graph);
-      cudaStreamDestroy(cs);
-      cudaSetDevice(prev);
-      throw;
-    }
-    g_capturing = false;
-    err = cudaStreamEndCapture(cs, &graph);
-    if (err == cudaSuccess) err = cudaGraphInstantiate(&exec, graph, 0);
-    if (graph) cudaGraphDestroy(graph);
-    cudaStreamDestroy(cs);
-    cudaSetDevice(prev);
-    if (err != cudaSuccess)
-      throw Error(PG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(err));
-    *out = new pg_graph{exec, mat->device};
+    });
   });
 }
 
@@ -387,6 +416,69 @@ PG_API int pg_graph_destroy(pg_graph* g) {
     if (!g) return;
     cudaGraphExecDestroy(g->exec);
     delete g;
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Distributed shards (dist.cu): the same calls with the halo exchanges and the
+// batched CGS2 reductions issued in between, on the same stream.
+// ---------------------------------------------------------------------------
+extern "C" {
+
+PG_API int pg_arnoldi_step_dist(const pg_matrix* mat, const double* y, int d, double* d_V,
+                                int64_t ld, int j, double* d_z, double* d_t, double* d_acc,
+                                double* d_w0, double* d_w1, double* d_ring, double* h_ring,
+                                pg_workspace* ws, pg_event* ev_done, pg_event* ev_chain0,
+                                pg_event* ev_chain1, int nroot, const int* rmode, const double* rc,
+                                pg_dist* dist, void* stream) {
+  return guard([&] {
+    PG_REQUIRE(dist, PG_ERR_PARAMETER, "communicator is null");
+    arnoldi_step_body(mat, y, d, d_V, ld, j, d_z, d_t, d_acc, d_w0, d_w1, d_ring, h_ring, ws,
+                      ev_done, ev_chain0, ev_chain1, nroot, rmode, rc, stream, dist);
+  });
+}
+
+PG_API int pg_step_graph_create_dist(const pg_matrix* mat, const double* y, int d, double* d_V,
+                                     int64_t ld, int j, double* d_z, double* d_t, double* d_acc,
+                                     double* d_w0, double* d_w1, double* d_ring, double* h_ring,
+                                     pg_workspace* ws, pg_event* ev_done, pg_event* ev_chain0,
+                                     pg_event* ev_chain1, int nroot, const int* rmode,
+                                     const double* rc, pg_dist* dist, pg_graph** out) {
+  return guard([&] {
+    PG_REQUIRE(dist, PG_ERR_PARAMETER, "communicator is null");
+    capture_step(mat, out, [&](void* cs) {
+      arnoldi_step_body(mat, y, d, d_V, ld, j, d_z, d_t, d_acc, d_w0, d_w1, d_ring, h_ring, ws,
+                        ev_done, ev_chain0, ev_chain1, nroot, rmode, rc, cs, dist);
+    });
+  });
+}
+
+PG_API int pg_poly_chain_dist(const pg_matrix* mat, const double* y, int d, double* d_x,
+                              const double* d_base, double* d_out, double* d_acc, double* d_w0,
+                              double* d_w1, pg_event* ev_start, pg_event* ev_end, pg_dist* dist,
+                              void* stream) {
+  return guard([&] {
+    PG_REQUIRE(mat && y && d_x && d_out && d >= 0 && dist, PG_ERR_PARAMETER, "null argument");
+    PG_REQUIRE(d == 0 || (d_acc && d_w0 && d_w1), PG_ERR_PARAMETER, "scratch vectors required");
+    record(ev_start, stream);
+    if (d > 0) dist_halo(dist, d_x, as_stream(stream));
+    poly_chain(mat, y, d, d_x, d_base, d_out, d_acc, d_w0, d_w1, stream, dist);
+    record(ev_end, stream);
+  });
+}
+
+PG_API int pg_power_sequence_dist(const pg_matrix* mat, double* d_P, int64_t ld, int ncols,
+                                  pg_dist* dist, void* stream) {
+  return guard([&] {
+    PG_REQUIRE(mat && d_P && ncols >= 1 && ld >= mat->ncols && dist, PG_ERR_PARAMETER,
+               "bad power-sequence arguments");
+    for (int k = 1; k < ncols; ++k) {
+      double* src = d_P + (int64_t)(k - 1) * ld;
+      dist_halo(dist, src, as_stream(stream));
+      ok(pg_spmv(mat, src, d_P + (int64_t)k * ld, stream));
+    }
   });
 }
 

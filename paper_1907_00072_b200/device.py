@@ -270,7 +270,15 @@ class SoloComm:
 class DistComm:
     """One shard per process; torch.distributed (NCCL for CUDA tensors, gloo
     for the CPU host-logic tests).  Halo: one batched send/recv round of
-    boundary entries per SpMV.  Dots: one all-reduce per batched phase."""
+    boundary entries per SpMV.  Reductions: every rank's partials are
+    all-gathered and summed in rank order -- the SoloComm order, identical on
+    every rank, independent of NCCL's algorithm choice.
+
+    With the NCCL backend the same exchanges also exist natively (``native``,
+    a ``pg_dist`` communicator of csrc/dist.cu): the solver's Arnoldi steps,
+    polynomial chains and power sequences then issue their halos and CGS2
+    reductions from C between the kernels, one native call (or recorded
+    graph) per step.  PG_DIST_NATIVE=0 keeps the torch-issued exchanges."""
 
     distributed = True
 
@@ -285,6 +293,40 @@ class DistComm:
         # host (host-logic tests, and several ranks sharing one GPU in the GPU
         # tests -- host-mediated, so no kernel ever waits on another rank)
         self.staged = dist.get_backend(group) == "gloo"
+        self.native = None
+
+    def open_native(self):
+        """Create the pg_dist communicator (NCCL backend only) and install
+        this shard's halo plan.  Collective: every rank calls it."""
+        if self.staged or os.environ.get("PG_DIST_NATIVE", "1") == "0":
+            return
+        uid = _lib.C.create_string_buffer(128)
+        if self.rank == 0:
+            _lib.call("pg_nccl_unique_id", uid, 128)
+        obj = [uid.raw if self.rank == 0 else None]
+        self.dist.broadcast_object_list(obj, src=0, group=self.group)
+        raw = _lib.C.create_string_buffer(obj[0], 128)
+        s = self.shards[0]
+        h = _lib.C.c_void_p()
+        _lib.call("pg_dist_create", raw, self.world, self.rank, s.dev_ord, _lib.C.byref(h))
+        self.native = h
+        sp = sorted(s.plan.send)
+        send_peer = np.asarray(sp, dtype=np.int32)
+        send_cnt = np.asarray([len(s.plan.send[q]) for q in sp], dtype=np.int64)
+        send_idx = (np.concatenate([s.plan.send[q] for q in sp]).astype(np.int32)
+                    if sp else np.zeros(1, np.int32))
+        rp = sorted(s.plan.recv)
+        recv_peer = np.asarray(rp, dtype=np.int32)
+        recv_off = np.asarray([s.plan.recv[q][0] for q in rp], dtype=np.int64)
+        recv_cnt = np.asarray([s.plan.recv[q][1] for q in rp], dtype=np.int64)
+        _lib.call("pg_dist_set_halo", h, len(sp), send_peer.ctypes.data, send_cnt.ctypes.data,
+                  send_idx.ctypes.data, len(rp), recv_peer.ctypes.data, recv_off.ctypes.data,
+                  recv_cnt.ctypes.data)
+
+    def close(self):
+        if self.native is not None:
+            _lib.call("pg_dist_destroy", self.native)
+            self.native = None
 
     def halo(self, xs):
         dist = self.dist
@@ -317,13 +359,15 @@ class DistComm:
         return bool(t.item())
 
     def allreduce(self, bufs):
+        """In-place sum over the ranks: all-gather, then ((b0 + b1) + b2) ..."""
         b = bufs[0]
-        if self.staged and b.is_cuda:
-            h = b.cpu()
-            self.dist.all_reduce(h, group=self.group)
-            b.copy_(h)
-        else:
-            self.dist.all_reduce(b, group=self.group)
+        src = b.cpu() if (self.staged and b.is_cuda) else b
+        parts = [torch.empty_like(src) for _ in range(self.world)]
+        self.dist.all_gather(parts, src.contiguous(), group=self.group)
+        total = parts[0].clone()
+        for p in parts[1:]:
+            total += p
+        b.copy_(total)
 
 
 def exchange_send_lists(shards, comm):
@@ -467,12 +511,15 @@ class Engine:
                   np.asarray(block.values), offs, sigma)
         comm = DistComm([s], group)
         exchange_send_lists([s], comm)
+        comm.open_native()
         return cls([s], comm, int(offs[-1]))
 
     def close(self):
         if self.ilu is not None:
             _lib.call("pg_ilu_destroy", self.ilu)
             self.ilu = None
+        if self.comm.distributed:
+            self.comm.close()
         for s in self.shards:
             s.close()
 
@@ -515,7 +562,13 @@ class Engine:
     def fast_steps(self) -> bool:
         """Whole Arnoldi steps / polynomial chains as one native call
         (pg_arnoldi_step / pg_poly_chain): single shard, plain SpMV operator."""
-        return self._fast and self.P == 1 and not self.comm.distributed and self.ilu is None
+        return (self._fast and self.P == 1 and self.ilu is None
+                and (not self.comm.distributed or self.native_dist is not None))
+
+    @property
+    def native_dist(self):
+        """The pg_dist communicator of a distributed engine, or None."""
+        return getattr(self.comm, "native", None)
 
     def _chain_events(self):
         if self.timer is None:
@@ -586,8 +639,12 @@ class Engine:
                 c0 = PgEvent(s.dev_ord) if chained else None
                 c1 = PgEvent(s.dev_ord) if chained else None
                 h = _lib.C.c_void_p()
-                _lib.call("pg_step_graph_create", *args, c0.h if c0 else None,
-                          c1.h if c1 else None, *tail, _lib.C.byref(h))
+                if self.native_dist is not None:
+                    _lib.call("pg_step_graph_create_dist", *args, c0.h if c0 else None,
+                              c1.h if c1 else None, *tail, self.native_dist, _lib.C.byref(h))
+                else:
+                    _lib.call("pg_step_graph_create", *args, c0.h if c0 else None,
+                              c1.h if c1 else None, *tail, _lib.C.byref(h))
                 graph = self._graphs[key] = _StepGraph(h, c0, c1)
             elif graph is None:
                 self._graph_seen.add(key)
@@ -596,8 +653,12 @@ class Engine:
             c0, c1 = graph.c0, graph.c1
         else:
             c0, c1 = self._chain_events() if chained else (None, None)
-            _lib.call("pg_arnoldi_step", *args, c0.h if c0 else None, c1.h if c1 else None,
-                      *tail, s.stream)
+            if self.native_dist is not None:
+                _lib.call("pg_arnoldi_step_dist", *args, c0.h if c0 else None,
+                          c1.h if c1 else None, *tail, self.native_dist, s.stream)
+            else:
+                _lib.call("pg_arnoldi_step", *args, c0.h if c0 else None, c1.h if c1 else None,
+                          *tail, s.stream)
         _lib.add_launches("pg_arnoldi_step", nlaunch)
         timing = None
         if c0 is not None and self.timer is not None:
@@ -745,7 +806,11 @@ class Engine:
         (halo before each product; M^{-1} A on ILU engines)."""
         if self.fast_steps:
             s = self.shards[0]
-            _lib.call("pg_power_sequence", s.mat, ptr(P[0]), s.ld, ncols, s.stream)
+            if self.native_dist is not None:
+                _lib.call("pg_power_sequence_dist", s.mat, ptr(P[0]), s.ld, ncols,
+                          self.native_dist, s.stream)
+            else:
+                _lib.call("pg_power_sequence", s.mat, ptr(P[0]), s.ld, ncols, s.stream)
             _lib.add_launches("pg_power_sequence", ncols - 1)
             return
         for k in range(ncols - 1):
@@ -763,9 +828,16 @@ class Engine:
             yarr = np.asarray(y, dtype=np.float64)
             c0, c1 = self._chain_events() if d > 0 else (None, None)
             b = base[0] if base is not None else None
-            _lib.call("pg_poly_chain", s.mat, yarr.ctypes.data, d, ptr(vs[0]),
-                      ptr(b) if b is not None else None, ptr(out[0]), ptr(acc[0]), ptr(w0[0]),
-                      ptr(w1[0]), c0.h if c0 else None, c1.h if c1 else None, s.stream)
+            if self.native_dist is not None:
+                _lib.call("pg_poly_chain_dist", s.mat, yarr.ctypes.data, d, ptr(vs[0]),
+                          ptr(b) if b is not None else None, ptr(out[0]), ptr(acc[0]),
+                          ptr(w0[0]), ptr(w1[0]), c0.h if c0 else None, c1.h if c1 else None,
+                          self.native_dist, s.stream)
+            else:
+                _lib.call("pg_poly_chain", s.mat, yarr.ctypes.data, d, ptr(vs[0]),
+                          ptr(b) if b is not None else None, ptr(out[0]), ptr(acc[0]),
+                          ptr(w0[0]), ptr(w1[0]), c0.h if c0 else None, c1.h if c1 else None,
+                          s.stream)
             _lib.add_launches("pg_poly_chain", max(d, 1))
             if c0 is not None:
                 self._time_chain(c0, c1, s, d, self._chain_vec_bytes(d, base is not None))
