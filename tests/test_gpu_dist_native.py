@@ -57,9 +57,9 @@ _lib.call("pg_dist_halo", h, ptr(x), st)
 torch.cuda.synchronize()
 xh = x.cpu().numpy()
 assert np.array_equal(xh[n:], xh[:n][idx]), "halo mismatch"
-buf = torch.from_numpy(rng.uniform(-1, 1, 137)).cuda()
+buf = torch.from_numpy(rng.uniform(-1, 1, 129)).cuda()
 ref = buf.clone()
-_lib.call("pg_dist_allreduce", h, ptr(buf), 137, st)
+_lib.call("pg_dist_allreduce", h, ptr(buf), 129, st)
 torch.cuda.synchronize()
 assert torch.equal(buf, ref)
 _lib.call("pg_dist_destroy", h)
