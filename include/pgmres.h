@@ -38,8 +38,11 @@ extern "C" {
 
 /* SELL-C-sigma slice height (one warp of rows). */
 #define PG_SLICE 32
-/* Largest basis / power-sequence width the tall-skinny kernels accept. */
+/* Largest basis / power-sequence width one tall-skinny kernel call accepts;
+ * wider bases (restart lengths up to PG_MMAX) are orthogonalized in column
+ * tiles of PG_KMAX (pg_cgs2_wide, the native step). */
 #define PG_KMAX 64
+#define PG_MMAX 256
 
 /* pg_poly_pass flags */
 #define PG_PASS_FIRST 1   /* acc = y0*x[row] + yk*(A x)[row]; acc_in unused   */
@@ -326,6 +329,17 @@ PG_API int pg_gram(const double* d_P, int64_t ld, int ncols, int64_t n, double* 
                    pg_workspace* ws, void* stream);
 PG_API int pg_gemv(const double* d_V, int64_t ld, int k, const double* d_y, int64_t n,
                    double* d_out, void* stream);
+/* out = base + sgn * (V[:, :k] y) (base may be NULL: out = sgn * V y); the
+ * column tiles of a basis wider than PG_KMAX (gmres.py:326, ortho.py:54-56). */
+PG_API int pg_gemv_acc(const double* d_V, int64_t ld, int k, const double* d_y, int64_t n,
+                       const double* d_base, double sgn, double* d_out, void* stream);
+/* CGS2 of z against a basis of k <= PG_MMAX columns in PG_KMAX-column tiles
+ * (k > PG_KMAX; ortho.py:53-59 with the reference's four passes): c1 = V^T z,
+ * w1 = z - V c1 (into d_w1, n entries), c2 = V^T w1, w2 = w1 - V c2 into d_w2,
+ * nsq = |w2|^2.  d_c1, d_c2 hold k doubles each. */
+PG_API int pg_cgs2_wide(const double* d_V, int64_t ld, int k, const double* d_z, int64_t n,
+                        double* d_c1, double* d_c2, double* d_nsq, double* d_w1, double* d_w2,
+                        pg_workspace* ws, void* stream);
 PG_API int pg_dot(const double* d_x, const double* d_y, int64_t n, double* d_out,
                   pg_workspace* ws, void* stream);
 PG_API int pg_scale_add(const double* d_base, double a, const double* d_v, int64_t n,

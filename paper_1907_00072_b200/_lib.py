@@ -23,6 +23,7 @@ PG_ERR_CUDA = -3
 PG_ERR_ALLOC = -4
 PG_SLICE = 32
 PG_KMAX = 64
+PG_MMAX = 256
 PG_PASS_FIRST = 1
 PG_PASS_WRITE_W = 2
 PG_ROOT_REAL = 0
@@ -58,6 +59,8 @@ _SIGNATURES = {
     "pg_normalize": ([_p, _p, _i64, _p, _p], C.c_int),
     "pg_gram": ([_p, _i64, _i32, _i64, _p, _p, _p], C.c_int),
     "pg_gemv": ([_p, _i64, _i32, _p, _i64, _p, _p], C.c_int),
+    "pg_gemv_acc": ([_p, _i64, _i32, _p, _i64, _p, _d, _p, _p], C.c_int),
+    "pg_cgs2_wide": ([_p, _i64, _i32, _p, _i64, _p, _p, _p, _p, _p, _p, _p], C.c_int),
     "pg_dot_blas": ([_p, _p, _i64, _i32, _p, _p], C.c_int),
     "pg_gram_blas_scratch": ([_i64, _i64, _i64, _i32, _pi64], C.c_int),
     "pg_gram_blas": ([_p, _i64, _i32, _i64, _i64, _i64, _p, _p, _p, _p], C.c_int),
@@ -152,7 +155,7 @@ def check(code: int, what: str = ""):
 LAUNCHING = frozenset({
     "pg_spmv", "pg_poly_pass", "pg_root_pass", "pg_residual", "pg_cgs2_phase1", "pg_cgs2_phase2",
     "pg_cgs2_phase3", "pg_normalize", "pg_gram", "pg_gemv", "pg_dot", "pg_scale_add",
-    "pg_gather", "pg_ilu_apply", "pg_dot_blas",
+    "pg_gather", "pg_ilu_apply", "pg_dot_blas", "pg_gemv_acc",
 })
 #: per-entry-point launch tally (bench.py reports it as gpu_launches)
 LAUNCH_COUNT: dict = {}

@@ -83,13 +83,13 @@ struct pg_dist {
   int32_t* d_send_idx = nullptr;
   double* d_send_buf = nullptr;
   int64_t send_total = 0;
-  // reduction scratch: [nranks][count], count <= 2*PG_KMAX + 8
+  // reduction scratch: [nranks][count], count <= 2*PG_MMAX + 8
   double* d_gather = nullptr;
 };
 
 namespace pg {
 
-constexpr int kRedMax = 2 * PG_KMAX + 8;
+constexpr int kRedMax = 2 * PG_MMAX + 8;
 
 __global__ void rank_sum_kernel(const double* __restrict__ parts, int nranks, int count,
                                 double* out) {

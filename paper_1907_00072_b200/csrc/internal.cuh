@@ -254,6 +254,12 @@ bool pdl_enabled();
 void dist_halo(pg_dist* d, double* x, cudaStream_t st);
 void dist_allreduce(pg_dist* d, double* buf, int count, cudaStream_t st);
 
+// CGS2 of z against a basis wider than PG_KMAX in column tiles (ortho.cu;
+// pg_cgs2_wide), with the reductions over dist's ranks when dist != null.
+void cgs2_wide(const double* V, int64_t ld, int k, const double* z, int64_t n, double* c1,
+               double* c2, double* nsq, double* w1, double* w2, pg_workspace* ws, pg_dist* dist,
+               cudaStream_t st);
+
 // Make `dev` current for a scope (restores the caller's device).
 struct DeviceScope {
   int prev = 0;

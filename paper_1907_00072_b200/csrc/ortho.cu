@@ -781,6 +781,63 @@ static int simple_grid(int64_t n, int threads, pg_workspace* ws) {
 using namespace pg;
 
 namespace pg {
+// out = base + sgn * (V[:, :k] c): sequential FMA over the columns per row,
+// like the GEMV (rows_kernel<false>); sgn = +-1 (exact).
+__global__ void __launch_bounds__(kRowThreads)
+    gemv_acc_kernel(const double* __restrict__ V, int64_t ld, int k, const double* __restrict__ c,
+                    int64_t n, const double* __restrict__ base, double sgn, double* out) {
+  pdl_entry();
+  __shared__ double cs[PG_KMAX];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = c[i];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+    const double* vr = V + r;
+    double t = 0.0;
+    int i = 0;
+    for (; i + 8 <= k; i += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(vr + (int64_t)(i + u) * ld);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t = __fma_rn(v[u], cs[i + u], t);
+    }
+    for (; i < k; ++i) t = __fma_rn(__ldcs(vr + (int64_t)i * ld), cs[i], t);
+    const double st = __dmul_rn(sgn, t);
+    out[r] = base ? __dadd_rn(base[r], st) : st;
+  }
+}
+
+// CGS2 against a basis wider than PG_KMAX, in column tiles: every phase reads
+// V once per tile (the reference's four passes, ortho.py:53-59); w1 is stored.
+void cgs2_wide(const double* V, int64_t ld, int k, const double* z, int64_t n, double* c1,
+               double* c2, double* nsq, double* w1, double* w2, pg_workspace* ws, pg_dist* dist,
+               cudaStream_t st) {
+  void* sv = reinterpret_cast<void*>(st);
+  auto tiles = [&](auto fn) {
+    for (int t0 = 0; t0 < k; t0 += PG_KMAX) fn(t0, k - t0 < PG_KMAX ? k - t0 : PG_KMAX);
+  };
+  auto chk = [](int rc) {
+    if (rc != PG_OK) {
+      char msg[512];
+      pg_last_error(msg, sizeof msg);
+      throw Error(rc, msg);
+    }
+  };
+  tiles([&](int t0, int kt) { chk(pg_cgs2_phase1(V + t0 * ld, ld, kt, z, n, c1 + t0, ws, sv)); });
+  dist_allreduce(dist, c1, k, st);
+  tiles([&](int t0, int kt) {
+    chk(pg_gemv_acc(V + t0 * ld, ld, kt, c1 + t0, n, t0 == 0 ? z : w1, -1.0, w1, sv));
+  });
+  tiles([&](int t0, int kt) { chk(pg_cgs2_phase1(V + t0 * ld, ld, kt, w1, n, c2 + t0, ws, sv)); });
+  dist_allreduce(dist, c2, k, st);
+  tiles([&](int t0, int kt) {
+    chk(pg_gemv_acc(V + t0 * ld, ld, kt, c2 + t0, n, t0 == 0 ? w1 : w2, -1.0, w2, sv));
+  });
+  chk(pg_dot(w2, w2, n, nsq, ws, sv));
+  dist_allreduce(dist, nsq, 1, st);
+}
+
 void normalize_publish(const double* x, const double* nsq, int64_t n, double* out,
                        const double* ring, int count, double* host, cudaStream_t st) {
   const int g = n > 0 ? simple_grid(n, 256, nullptr) : 1;
@@ -870,6 +927,31 @@ PG_API int pg_gemv(const double* d_V, int64_t ld, int k, const double* d_y, int6
     const int g = simple_grid(n, kRowThreads, nullptr);
     launch_k(rows_kernel<false>, g, kRowThreads, 0, as_stream(stream), d_V, ld, k, nullptr, n, d_y, nullptr, d_out, nullptr, nullptr, nullptr);
     check_launch();
+  });
+}
+
+PG_API int pg_gemv_acc(const double* d_V, int64_t ld, int k, const double* d_y, int64_t n,
+                       const double* d_base, double sgn, double* d_out, void* stream) {
+  return guard([&] {
+    check_tall(d_V, ld, k, n, 0);
+    PG_REQUIRE(d_out && (k == 0 || d_y), PG_ERR_PARAMETER, "null argument");
+    if (n == 0) return;
+    const int g = simple_grid(n, kRowThreads, nullptr);
+    launch_k(gemv_acc_kernel, g, kRowThreads, 0, as_stream(stream), d_V, ld, k, d_y, n, d_base,
+             sgn, d_out);
+    check_launch();
+  });
+}
+
+PG_API int pg_cgs2_wide(const double* d_V, int64_t ld, int k, const double* d_z, int64_t n,
+                        double* d_c1, double* d_c2, double* d_nsq, double* d_w1, double* d_w2,
+                        pg_workspace* ws, void* stream) {
+  return guard([&] {
+    PG_REQUIRE(k >= 1 && k <= PG_MMAX, PG_ERR_DIMENSION, "basis width out of range");
+    PG_REQUIRE(d_V && d_z && d_c1 && d_c2 && d_nsq && d_w1 && d_w2, PG_ERR_PARAMETER,
+               "null argument");
+    cgs2_wide(d_V, ld, k, d_z, n, d_c1, d_c2, d_nsq, d_w1, d_w2, ws, nullptr,
+              as_stream(stream));
   });
 }
 

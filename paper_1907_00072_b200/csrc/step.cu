@@ -264,7 +264,7 @@ void arnoldi_step_body(const pg_matrix* mat, const double* y, int d, double* d_V
     PG_REQUIRE(mat && d_V && d_z && d_ring && h_ring && ws && ev_done, PG_ERR_PARAMETER,
                "null argument");
     const int k = j + 1;
-    PG_REQUIRE(j >= 0 && k < PG_KMAX && ld >= mat->ncols, PG_ERR_PARAMETER,
+    PG_REQUIRE(j >= 0 && k < PG_MMAX && ld >= mat->ncols, PG_ERR_PARAMETER,
                "step index out of range");
     const int64_t n = mat->nrows;
     const double* vj = d_V + (int64_t)j * ld;
@@ -299,27 +299,34 @@ void arnoldi_step_body(const pg_matrix* mat, const double* y, int d, double* d_V
     } else {
       ok(pg_spmv(mat, vj, d_z, stream));
     }
-    // CGS2 against v_0..v_{k-1}; w2/|w2| into column k (ortho.py:53-70)
+    // CGS2 against v_0..v_{k-1}; w2/|w2| into column k (ortho.py:53-70).  The
+    // step's scalars are packed [c1 (k) | c2 (k) | nsq] at the ring's start.
     double* c1 = d_ring;
-    double* c2 = d_ring + PG_KMAX;
-    double* nsq = d_ring + 2 * PG_KMAX;
+    double* c2 = d_ring + k;
+    double* nsq = d_ring + 2 * k;
     double* col = d_V + (int64_t)k * ld;
-    // distributed: one batched reduction per phase (all-gather + rank-order sum)
-    ok(pg_cgs2_phase1(d_V, ld, k, d_z, n, c1, ws, stream));
-    dist_allreduce(dist, c1, k, cst);
-    ok(pg_cgs2_phase2(d_V, ld, k, d_z, n, c1, c2, ws, stream));
-    dist_allreduce(dist, c2, k, cst);
-    ok(pg_cgs2_phase3(d_V, ld, k, d_z, n, c1, c2, col, nsq, ws, stream));
-    dist_allreduce(dist, nsq, 1, cst);
+    if (k <= PG_KMAX) {
+      // distributed: one batched reduction per phase (all-gather + rank-order sum)
+      ok(pg_cgs2_phase1(d_V, ld, k, d_z, n, c1, ws, stream));
+      dist_allreduce(dist, c1, k, cst);
+      ok(pg_cgs2_phase2(d_V, ld, k, d_z, n, c1, c2, ws, stream));
+      dist_allreduce(dist, c2, k, cst);
+      ok(pg_cgs2_phase3(d_V, ld, k, d_z, n, c1, c2, col, nsq, ws, stream));
+      dist_allreduce(dist, nsq, 1, cst);
+    } else {
+      // wider than one tile: w1 into t (free once the wrapper SpMV has read it)
+      PG_REQUIRE(d_t, PG_ERR_PARAMETER, "a basis wider than PG_KMAX needs the t scratch");
+      cgs2_wide(d_V, ld, k, d_z, n, c1, c2, nsq, d_t, col, ws, dist, cst);
+    }
     // normalise into column k and publish the scalars straight into the
     // pinned host ring (no copy-engine transfer between steps), or copy them
     double* h_dev = mapped_host(h_ring);
     if (h_dev) {
-      normalize_publish(col, nsq, n, col, d_ring, 2 * PG_KMAX + 1, h_dev, as_stream(stream));
+      normalize_publish(col, nsq, n, col, d_ring, 2 * k + 1, h_dev, cst);
     } else {
       ok(pg_normalize(col, nsq, n, col, stream));
-      PG_CUDA(cudaMemcpyAsync(h_ring, d_ring, sizeof(double) * (2 * PG_KMAX + 1),
-                              cudaMemcpyDeviceToHost, as_stream(stream)));
+      PG_CUDA(cudaMemcpyAsync(h_ring, d_ring, sizeof(double) * (2 * k + 1),
+                              cudaMemcpyDeviceToHost, cst));
     }
     record(ev_done, stream);
 }

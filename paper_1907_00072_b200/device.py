@@ -31,7 +31,8 @@ from . import _lib
 from .errors import DeviceError, DimensionMismatchError, ParameterError
 
 F64 = torch.float64
-KMAX = _lib.PG_KMAX
+KMAX = _lib.PG_KMAX  # columns per tall-skinny kernel call
+MMAX = _lib.PG_MMAX  # widest basis (restart length + 1) of a solve
 ROW_ALIGN = 64  # leading-dimension alignment of basis blocks (rows)
 
 
@@ -158,11 +159,11 @@ class Shard:
         self.chain_fused = bool(fused.value)
         # small per-shard device scratch: [c1 | c2 | nsq | spare]
         self.scal = torch.zeros(2 * KMAX + 8, dtype=F64, device=device)
-        self.coef = torch.zeros(KMAX, dtype=F64, device=device)
-        # two-slot ring of CGS2 scalars (one Arnoldi step of look-ahead) and
-        # its pinned host mirror
-        self.ring = [torch.zeros(2 * KMAX + 8, dtype=F64, device=device) for _ in range(2)]
-        self.pinned = [torch.zeros(2 * KMAX + 1, dtype=F64).pin_memory() for _ in range(2)]
+        self.coef = torch.zeros(MMAX, dtype=F64, device=device)
+        # two-slot ring of CGS2 scalars (one Arnoldi step of look-ahead), each
+        # packed [c1 (k) | c2 (k) | nsq], and its pinned host mirror
+        self.ring = [torch.zeros(2 * MMAX + 8, dtype=F64, device=device) for _ in range(2)]
+        self.pinned = [torch.zeros(2 * MMAX + 1, dtype=F64).pin_memory() for _ in range(2)]
         self.send_idx: dict = {}
         self.send_buf: dict = {}
         self._lib = lib
@@ -1056,16 +1057,17 @@ class Engine:
     def cgs2_launch(self, Vs, k, zs, slot: int):
         """Asynchronous CGS2 (all three phases, their all-reduces and the
         normalisation of column k); the reduced scalars land in device ring
-        slot ``slot`` (0/1) and are copied to pinned host memory behind an
-        event.  Returns a handle for :meth:`cgs2_fetch`."""
+        slot ``slot`` (0/1), packed [c1 (k) | c2 (k) | nsq], and are copied to
+        pinned host memory behind an event.  Returns a handle for
+        :meth:`cgs2_fetch`."""
         bufs = [s.ring[slot] for s in self.shards]
-        c1 = [b[0:KMAX] for b in bufs]
-        c2 = [b[KMAX:2 * KMAX] for b in bufs]
-        nsq = [b[2 * KMAX:2 * KMAX + 1] for b in bufs]
+        c1 = [b[0:k] for b in bufs]
+        c2 = [b[k:2 * k] for b in bufs]
+        nsq = [b[2 * k:2 * k + 1] for b in bufs]
         self._cgs2_phases(Vs, k, zs, c1, c2, nsq)
         s0 = self.shards[0]
         host = s0.pinned[slot]
-        host.copy_(bufs[0][:2 * KMAX + 1], non_blocking=True)
+        host[:2 * k + 1].copy_(bufs[0][:2 * k + 1], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(s0.device))
         return ev, host, k
@@ -1079,9 +1081,11 @@ class Engine:
             c0, c1, s, d, vec = handle[3]
             self._time_chain(_Elapsed(c0.elapsed_time(c1)), None, s, d, vec)
         h = host.numpy()
-        return h[:k].copy(), h[KMAX:KMAX + k].copy(), float(h[2 * KMAX])
+        return h[:k].copy(), h[k:2 * k].copy(), float(h[2 * k])
 
     def _cgs2_phases(self, Vs, k, zs, c1, c2, nsq):
+        if k > KMAX:
+            return self._cgs2_wide(Vs, k, zs, c1, c2, nsq)
         if k > 0:
             for s, V, z, c in zip(self._each(), Vs, zs, c1):
                 _lib.call("pg_cgs2_phase1", ptr(V), s.ld, k, ptr(z), s.n, ptr(c), s.ws, s.stream)
@@ -1099,11 +1103,45 @@ class Engine:
         # scalars; on breakdown the column is simply never used (ortho.py:67-70)
         self.normalize_dev([V[k] for V in Vs], nsq, [V[k] for V in Vs])
 
+    def _cgs2_wide(self, Vs, k, zs, c1, c2, nsq):
+        """CGS2 against more than KMAX columns, in column tiles (the C
+        cgs2_wide with a reduction over the shards after each phase): c1 per
+        tile, w1 = z - V c1 stored, c2 per tile, w2 = w1 - V c2 into column k."""
+        tiles = [(t0, min(KMAX, k - t0)) for t0 in range(0, k, KMAX)]
+        w1s = self.cached_vecs("cgs2_w1")
+        for s, V, z, c in zip(self._each(), Vs, zs, c1):
+            for t0, kt in tiles:
+                _lib.call("pg_cgs2_phase1", ptr(V[t0]), s.ld, kt, ptr(z), s.n, ptr(c[t0:]), s.ws,
+                          s.stream)
+        self.comm.allreduce(c1)
+        for s, V, z, c, w1 in zip(self._each(), Vs, zs, c1, w1s):
+            for t0, kt in tiles:
+                _lib.call("pg_gemv_acc", ptr(V[t0]), s.ld, kt, ptr(c[t0:]), s.n,
+                          ptr(z if t0 == 0 else w1), -1.0, ptr(w1), s.stream)
+        for s, V, c, w1 in zip(self._each(), Vs, c2, w1s):
+            for t0, kt in tiles:
+                _lib.call("pg_cgs2_phase1", ptr(V[t0]), s.ld, kt, ptr(w1), s.n, ptr(c[t0:]), s.ws,
+                          s.stream)
+        self.comm.allreduce(c2)
+        for s, V, c, w1 in zip(self._each(), Vs, c2, w1s):
+            col = V[k]
+            for t0, kt in tiles:
+                _lib.call("pg_gemv_acc", ptr(V[t0]), s.ld, kt, ptr(c[t0:]), s.n,
+                          ptr(w1 if t0 == 0 else col), -1.0, ptr(col), s.stream)
+        for s, V, q in zip(self._each(), Vs, nsq):
+            _lib.call("pg_dot", ptr(V[k]), ptr(V[k]), s.n, ptr(q), s.ws, s.stream)
+        self.comm.allreduce(nsq)
+        self.normalize_dev([V[k] for V in Vs], nsq, [V[k] for V in Vs])
+
     def gemv(self, Vs, k, y_host, outs):
+        """out = V[:, :k] y (gmres.py:326); KMAX-column tiles past KMAX."""
         yt = torch.from_numpy(np.ascontiguousarray(y_host, dtype=np.float64))
         for s, V, o in zip(self._each(), Vs, outs):
             s.coef[:k].copy_(yt)
-            _lib.call("pg_gemv", ptr(V), s.ld, k, ptr(s.coef), s.n, ptr(o), s.stream)
+            _lib.call("pg_gemv", ptr(V), s.ld, min(k, KMAX), ptr(s.coef), s.n, ptr(o), s.stream)
+            for t0 in range(KMAX, k, KMAX):
+                _lib.call("pg_gemv_acc", ptr(V[t0]), s.ld, min(KMAX, k - t0), ptr(s.coef[t0:]),
+                          s.n, ptr(o), 1.0, ptr(o), s.stream)
 
     def gram(self, Ps, ncols) -> np.ndarray:
         """Global Gram matrix of the first ncols columns.  Each shard returns

@@ -23,7 +23,7 @@ import torch
 
 from . import _lib
 from .counters import CostCounters
-from .device import KMAX
+from .device import MMAX
 from .errors import (
     DimensionMismatchError,
     NumericalBreakdownError,
@@ -176,8 +176,8 @@ def _solve(op, b, x0, right_prec, config) -> GmresResult:
     if blen != (n,) and not (e.comm.distributed and blen == (e.local_n,)):
         raise DimensionMismatchError("right-hand side length does not match")
     m = config.restart_m
-    if m + 1 > KMAX:
-        raise ParameterError(f"restart_m must be at most {KMAX - 1} on the device path")
+    if m + 1 > MMAX:
+        raise ParameterError(f"restart_m must be at most {MMAX - 1} on the device path")
     tol = config.tol
 
     poly = right_prec if right_prec else None  # reference truthiness (gmres.py:261)

@@ -19,7 +19,7 @@ import torch
 
 from . import _lib
 from .counters import CostCounters
-from .device import KMAX, F64, _pad, ptr, require_cuda
+from .device import KMAX, MMAX, F64, _pad, ptr, require_cuda
 from .errors import DimensionMismatchError
 
 BREAKDOWN_RTOL = 1e-14
@@ -64,8 +64,8 @@ def icgs(basis, w, counters: CostCounters) -> OrthoResult:
     n, j = B.shape
     if tuple(W.shape) != (n,):
         raise DimensionMismatchError("w length does not match the basis")
-    if j > KMAX - 1:
-        raise DimensionMismatchError(f"basis wider than {KMAX - 1} columns")
+    if j > MMAX - 1:
+        raise DimensionMismatchError(f"basis wider than {MMAX - 1} columns")
     dev = W.device if (as_torch and W.is_cuda) else torch.device("cuda", torch.cuda.current_device())
     dev_ord = dev.index if dev.index is not None else torch.cuda.current_device()
     ld = _pad(n)
@@ -74,19 +74,24 @@ def icgs(basis, w, counters: CostCounters) -> OrthoResult:
         V[:j, :n].copy_(B.to(dev, F64).T)
     z = torch.zeros(ld, dtype=F64, device=dev)
     z[:n].copy_(W.to(dev, F64))
-    scal = torch.zeros(2 * KMAX + 1, dtype=F64, device=dev)
-    c1, c2, nsq = scal[:KMAX], scal[KMAX:2 * KMAX], scal[2 * KMAX:]
+    scal = torch.zeros(2 * j + 1, dtype=F64, device=dev)
+    c1, c2, nsq = scal[:j], scal[j:2 * j], scal[2 * j:]
     ws = workspace(dev_ord)
     st = torch.cuda.current_stream(dev).cuda_stream
     _lib.call("pg_set_device", dev_ord)
-    if j:
-        _lib.call("pg_cgs2_phase1", ptr(V), ld, j, ptr(z), n, ptr(c1), ws, st)
-        _lib.call("pg_cgs2_phase2", ptr(V), ld, j, ptr(z), n, ptr(c1), ptr(c2), ws, st)
-    _lib.call("pg_cgs2_phase3", ptr(V), ld, j, ptr(z), n, ptr(c1), ptr(c2), ptr(V[j]),
-              ptr(nsq), ws, st)
+    if j > KMAX:  # wider than one tile: the four-pass tiled form
+        w1 = torch.zeros(ld, dtype=F64, device=dev)
+        _lib.call("pg_cgs2_wide", ptr(V), ld, j, ptr(z), n, ptr(c1), ptr(c2), ptr(nsq), ptr(w1),
+                  ptr(V[j]), ws, st)
+    else:
+        if j:
+            _lib.call("pg_cgs2_phase1", ptr(V), ld, j, ptr(z), n, ptr(c1), ws, st)
+            _lib.call("pg_cgs2_phase2", ptr(V), ld, j, ptr(z), n, ptr(c1), ptr(c2), ws, st)
+        _lib.call("pg_cgs2_phase3", ptr(V), ld, j, ptr(z), n, ptr(c1), ptr(c2), ptr(V[j]),
+                  ptr(nsq), ws, st)
     host = scal.cpu().numpy()
-    coeffs = host[:j] + host[KMAX:KMAX + j]
-    new_norm = float(np.sqrt(host[2 * KMAX]))
+    coeffs = host[:j] + host[j:2 * j]
+    new_norm = float(np.sqrt(host[2 * j]))
     counters.dots += 3
     counters.scalar_dots += 2 * j + 1
     counters.vector_updates += 2 * j

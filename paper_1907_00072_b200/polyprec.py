@@ -114,7 +114,8 @@ def _check_decision(decision: str):
 
 def _device_power_gram(op, v0, top: int, counters: CostCounters, decision: str = "reference"):
     """Unit seed, then the ``top``+1 power columns on the device and their
-    full Gram matrix on the host.  Returns (Gram (top+1)^2, seed_norm)."""
+    Gram matrix on the host (the leading KMAX x KMAX block when top+1 > KMAX).
+    Returns (Gram, seed_norm)."""
     _check_decision(decision)
     e = _engine(op)
     if isinstance(v0, torch.Tensor):
@@ -124,8 +125,8 @@ def _device_power_gram(op, v0, top: int, counters: CostCounters, decision: str =
         v0 = np.asarray(v0, dtype=np.float64)
         if v0.shape != (op.dimension,) and not (e.comm.distributed and v0.shape == (e.local_n,)):
             raise DimensionMismatchError("seed vector length does not match operator")
-    if top + 1 > KMAX:
-        raise ParameterError(f"power sequence of {top + 1} columns exceeds the kernel limit {KMAX}")
+    if top + 1 > KMAX and decision != "reference":
+        raise ParameterError(f"exact decisions take at most {KMAX} power columns")
     vs = e.ingest(v0)
     # |v0|^2 stays in device slot 6 while the power sequence and the Gram are
     # queued: one host round trip (the Gram's) instead of two
@@ -138,7 +139,10 @@ def _device_power_gram(op, v0, top: int, counters: CostCounters, decision: str =
     e.normalize_dev(vs, e.slot(6), [blk[0] for blk in P])
     e.power_sequence(P, top + 1)
     e.count_ops(op.counters, top)
-    G = e.gram_blas(P, top + 1) if decision == "reference" else e.gram(P, top + 1)
+    # past KMAX columns only the leading KMAX x KMAX block is formed: the
+    # Cholesky pivots the decision needs all lie inside it (_factor)
+    kg = min(top + 1, KMAX)
+    G = e.gram_blas(P, kg) if decision == "reference" else e.gram(P, kg)
     seed_norm = float(np.sqrt(e.read_slot(6)))
     if seed_norm == 0.0:
         raise ParameterError("seed vector v0 must be nonzero")
@@ -152,13 +156,44 @@ def _normal_equations(Gfull: np.ndarray, deg: int, counters: CostCounters) -> Gr
     return GramSystem(Gfull[1:deg + 2, 1:deg + 2].copy(), Gfull[1:deg + 2, 0].copy())
 
 
-def _factor(system: GramSystem, decision: str):
+def _cholesky_ref(G: np.ndarray, rhs: np.ndarray, order: int) -> np.ndarray:
+    """dense_cholesky (polyprec.py:60-93) of the Gram block G with the pivot
+    floor of an order-``order`` system -- ``order`` = G's size, or larger when
+    G is the leading block of a system wider than the kernels form: pivot k of
+    the full system is pivot k of its leading block, only its floor
+    ``order*eps*G[k,k]`` grows with the order.  Raises CholeskyFailure."""
+    m = G.shape[0]
+    eps = np.finfo(np.float64).eps
+    L = np.zeros((m, m))
+    for k in range(m):
+        pivot = G[k, k] - L[k, :k] @ L[k, :k]
+        if pivot <= order * eps * G[k, k]:
+            raise CholeskyFailure(k + 1)
+        L[k, k] = np.sqrt(pivot)
+        if k + 1 < m:
+            L[k + 1:, k] = (G[k + 1:, k] - L[k + 1:, :k] @ L[k, :k]) / L[k, k]
+    if order > m:  # every available pivot passed: the rest is beyond the kernels
+        raise ParameterError(f"the Gram system of order {order} factors through its leading "
+                             f"{m} pivots; deciding it needs more than {KMAX} power columns")
+    z = np.zeros(m)
+    for k in range(m):
+        z[k] = (rhs[k] - L[k, :k] @ z[:k]) / L[k, k]
+    y = np.zeros(m)
+    for k in range(m - 1, -1, -1):
+        y[k] = (z[k] - L[k + 1:, k] @ y[k + 1:]) / L[k, k]
+    return y
+
+
+def _factor(system: GramSystem, decision: str, order: int | None = None):
     """(y, failed 1-based pivot or 0): the reference's Cholesky loop
-    (dense_cholesky, polyprec.py:60-93) or the native compensated one."""
+    (polyprec.py:60-93) or the native compensated one.  ``order`` > the
+    block's size: the leading block of a wider system (_cholesky_ref)."""
+    if order is None:
+        order = system.G.shape[0]
     if decision == "exact":
         return _lib.host_cholesky(system.G, system.rhs)
     try:
-        return dense_cholesky(system), 0
+        return _cholesky_ref(system.G, system.rhs, order), 0
     except CholeskyFailure as exc:
         return None, exc.pivot
 
@@ -173,7 +208,7 @@ def build_poly(op, v0, deg: int, counters: CostCounters,
     Gfull, seed_norm = _device_power_gram(op, v0, deg + 1, counters, decision)
     counters.scalar_dots += 1
     full = _normal_equations(Gfull, deg, counters)
-    y, pivot = _factor(full, decision)
+    y, pivot = _factor(full, decision, deg + 1)
     if pivot:
         raise CholeskyFailure(pivot)
     return PolyCoefficients(deg, y, seed_norm, seed_mode)
@@ -205,10 +240,15 @@ def _select_degree(full: GramSystem, cap: int, seed_norm: float, seed_mode: str,
         d, y = _lib.host_degree_select(full.G, full.rhs, cap)
     else:
         d, y = -1, None
-        for dd in range(1, cap + 1):
+        for dd in range(1, min(cap, full.G.shape[0] - 1) + 1):
             yy, piv = _factor(GramSystem(full.G[:dd + 1, :dd + 1], full.rhs[:dd + 1]), decision)
             if not piv and np.all(np.isfinite(yy)):
                 d, y = dd, yy
+        if cap + 1 > full.G.shape[0]:
+            # degrees past the formed block: a leading pivot failing at the
+            # floor of the next order fails at every larger one, so all of
+            # them fail (_cholesky_ref raises if none does: undecidable)
+            _factor(full, decision, full.G.shape[0] + 1)
     if d >= 1:
         return PolyCoefficients(d, y, seed_norm, seed_mode)
     y0, pivot = _factor(GramSystem(full.G[:1, :1], full.rhs[:1]), decision)
@@ -232,13 +272,10 @@ def build_poly_or_auto(op, v0, deg: int, counters: CostCounters,
     (oracle.degree_policy_shared)."""
     if deg < 1:
         return build_poly(op, v0, deg, counters, seed_mode, decision), None
-    if deg + 2 > KMAX:
-        raise ParameterError(f"degree {deg} needs {deg + 2} power columns; the tall-skinny "
-                             f"kernels take at most {KMAX}")
     Gfull, seed_norm = _device_power_gram(op, v0, deg + 1, counters, decision)
     counters.scalar_dots += 1
     full = _normal_equations(Gfull, deg, counters)
-    y, pivot = _factor(full, decision)
+    y, pivot = _factor(full, decision, deg + 1)
     if not pivot:
         return PolyCoefficients(deg, y, seed_norm, seed_mode), None
     return _select_degree(full, deg, seed_norm, seed_mode, decision), pivot

@@ -550,3 +550,65 @@ def test_recorded_step_graphs_replay_bitwise(golden, monkeypatch):
         assert np.array_equal(r[0], runs[0][0])
         assert r[1:] == runs[0][1:]
     op.close()
+
+
+# ---------------------------------------------------------------------------
+# bases wider than one tall-skinny kernel call (PG_KMAX = 64 columns)
+# ---------------------------------------------------------------------------
+def test_restart_100_unpreconditioned_matches_oracle(golden):
+    """GMRES(100) (the paper's restart length): Arnoldi steps
+    past 64 basis columns orthogonalize in 64-column tiles (pg_cgs2_wide)."""
+    A = _lap64(golden)
+    b = golden[0]["cfg1_b"]
+    res, sc, ref, t, poly, c = _solve_pair(A, b, None, 100, 1e-8, max_iters=400)
+    assert res.iterations > 64  # the wide path ran
+    _agree(res, sc, ref, t, 1e-8, c)
+    # the same through the kernel-by-kernel path and on 2 virtual shards
+    for shards in (1, 2):
+        c2 = pg.CostCounters()
+        op = pg.DeviceMatrixOperator(A, c2, shards=shards)
+        r2 = pg.solve(op, b, config=pg.GmresConfig(100, 1e-8, 400))
+        assert r2.converged and abs(r2.iterations - ref.iterations) <= 2
+        op.close()
+
+
+def test_restart_100_with_polynomial_and_icgs_wide(golden):
+    a, _ = golden
+    A = _lap64(golden)
+    res, sc, ref, t, poly, c = _solve_pair(A, a["cfg1_b"], 4, 100, 1e-12)
+    _agree(res, sc, ref, t, 1e-12, c)
+    g = np.random.default_rng(3)
+    for j in (65, 100, 130):
+        basis = np.linalg.qr(g.standard_normal((700, j)))[0]
+        w = g.uniform(-1, 1, 700)
+        cc = pg.CostCounters()
+        got = pg.icgs(basis, w, cc)
+        want = orc.cgs2(basis, w, orc.Tally())
+        np.testing.assert_allclose(got.coeffs, want[0], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(got.vector, want[2], rtol=0, atol=1e-12)
+        assert (cc.dots, cc.scalar_dots) == (3, 2 * j + 1)
+    with pytest.raises(pg.ParameterError):
+        pg.solve(pg.DeviceMatrixOperator(A), a["cfg1_b"], config=pg.GmresConfig(256, 1e-8))
+
+
+def test_degrees_past_the_kernel_width(golden):
+    """build_poly / auto_degree at degrees whose power sequence is wider than
+    PG_KMAX: the decision comes from the leading pivots at the full system's
+    floor (polyprec._cholesky_ref), as the reference's Cholesky would take it."""
+    _, meta = golden
+    A = _lap64(golden)
+    v0 = orc.sm64_uniform(1, 4096)
+    op = pg.DeviceMatrixOperator(A)
+    Gfull, _ = orc.gram_full_blas(orc.OracleMatrix.of(A), v0, 66)
+    for d in (63, 64):
+        want = orc.degree_decision_blas(Gfull[:d + 2, :d + 2], d)
+        before = op.counters.spmvs
+        with pytest.raises(pg.CholeskyFailure) as err:
+            pg.build_poly(op, v0, d, pg.CostCounters())
+        assert err.value.pivot == want[0]
+        assert op.counters.spmvs - before == d + 1  # the reference's power sequence length
+        assert pg.auto_degree(op, v0, d, pg.CostCounters()).degree == want[1]
+        p, piv = pg.build_poly_or_auto(op, v0, d, pg.CostCounters())
+        assert piv == want[0] and p.degree == want[1]
+    assert want[1] == meta["auto_lap64"]["degree"]
+    op.close()

@@ -205,14 +205,15 @@ def test_arnoldi_construction_matches_power_basis(golden, deg):
     op = pg.DeviceMatrixOperator(h, c)
     pa = pg.build_poly_arnoldi(op, v0, deg, c)
     assert pa.degree == deg and len(pa.roots) == deg + 1 and c.spmvs == deg + 1
-    pp = pg.build_poly(op, v0, deg, pg.CostCounters())
+    # the exact-arithmetic power-basis minimiser (the reference-order fp64
+    # Gram's rounding moves the degree-10 roots by more than the comparison)
+    pp = pg.build_poly(op, v0, deg, pg.CostCounters(), decision="exact")
     O = orc.OracleMatrix.of(h)
     v = v0 / np.linalg.norm(v0)
     ra, rp = _res_norm(O, pa.y, v), _res_norm(O, pp.y, v)
     # the harmonic-Ritz minimiser is never worse; the power basis loses a
-    # little to its conditioning at the top usable degree (deg 10: 2e-4 with
-    # the exact-arithmetic Gram, 1.2e-3 with the reference's fp64 one)
-    assert ra <= rp * (1 + 1e-6) and rp <= ra * (1 + 2e-3)
+    # little to its conditioning at the top usable degree (2e-4 at deg 10)
+    assert ra <= rp * (1 + 1e-6) and rp <= ra * (1 + 1e-3)
     rr = np.sort_complex(pg.residual_poly_roots(pp.y))
     assert np.allclose(np.sort_complex(pa.roots), rr, rtol=1e-4 if deg < 10 else 1e-2)
     if deg <= 8:
