@@ -107,7 +107,8 @@ PG_API int pg_matrix_destroy(pg_matrix* mat);
  *              dictionary with global gathers, 3 windowed pair TMA ring,
  *              4 pair dictionary, short uniform rows, 5 row-pattern
  *              dictionary (1 B per row), 6 windowed row patterns, 7 offset
- *              patterns (1 B per row + f64 values))} */
+ *              patterns (1 B per row + f64 values), 8 plane marching,
+ *              9 plane ring (TMA-staged plane windows))} */
 PG_API int pg_matrix_stats(const pg_matrix* mat, int64_t* stats);
 
 /* ---- reduction workspace (one per stream) --------------------------------

@@ -15,7 +15,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libpgmres.so")
 BUILD = os.path.join(ROOT, "build", "pgmres")
 
-SOURCES = ["abi.cu", "spmv.cu", "ortho.cu", "host.cu", "ilu.cu", "step.cu", "chain.cu", "blasorder.cu", "march.cu", "dist.cu"]
+SOURCES = ["abi.cu", "spmv.cu", "ortho.cu", "host.cu", "ilu.cu", "step.cu", "chain.cu", "blasorder.cu", "march.cu", "planes.cu", "dist.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -627,6 +627,7 @@ PG_API int pg_matrix_create(int device, int64_t nrows, int64_t ncols, const int6
       m->val = upload(val.data(), (size_t)h.padded, m->bytes);
       build_dictionaries(h, col.data(), val.data(), m);
       if (!m->pair8 && !m->col8 && !m->val8) build_offset_patterns(h, col.data(), m);
+      plane_prepare(m);
     } catch (...) {
       free_matrix(m);
       throw;
@@ -655,7 +656,8 @@ PG_API int pg_matrix_stats(const pg_matrix* m, int64_t* s) {
     // the kernel launch_sell picks for 16-byte aligned vectors (spmv.cu)
     int mk;
     int64_t mS, mg;
-    s[11] = march_shape(m, &mk, &mS, &mg) ? 8
+    s[11] = plane_shape(m) ? 9
+            : march_shape(m, &mk, &mS, &mg) ? 8
             : pattern_kernel(m) ? 5
             : (m->pair8 && m->wtab && m->rpat && winpat_enabled()) ? 6
             : opat_kernel(m) ? 7

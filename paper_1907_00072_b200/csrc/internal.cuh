@@ -54,6 +54,19 @@ inline void check_launch() { PG_CUDA(cudaGetLastError()); }
 // ------------------------------------------------------------ structures --
 }  // namespace pg
 
+namespace pg {
+// Plane-ring kernel launch plan (planes.cu plane_prepare), fixed at matrix
+// creation: tile width Q, tiles per plane, planes per chunk, in-plane halo H
+// (+ parity shift sh so window starts are even), ring layout, and the window
+// position of each middle-group value relative to the row's slot.
+struct PlaneArgs {
+  int64_t nrows, ncols, S, nz;
+  int Q, nqb, Zc, H, sh;
+  int stages, stage_bytes, off_a, off_b, off_p;
+  int woff[9];
+};
+}  // namespace pg
+
 struct pg_matrix {
   int device;
   int64_t nrows, ncols, nnz, padded_nnz, n_slices;
@@ -115,6 +128,9 @@ struct pg_matrix {
   int n_doff;
   int32_t doff[256];
   int64_t dband_lo, dband_hi;
+  // plane-ring kernel (planes.cu): plane_kind 0 = not a plane stencil / off
+  int plane_kind, plane_blocks;
+  pg::PlaneArgs plane;
   size_t bytes;
 };
 
@@ -315,6 +331,12 @@ struct ChainStep {
 // The plane-marching stencil kernel handles this matrix (march.cu): kind
 // (27, 7, 9, 5), plane stride S and row stride g of its master pattern.
 bool march_shape(const pg_matrix* m, int* kind, int64_t* S, int64_t* g);
+// The master pattern is a plane stencil (any size; march.cu).
+bool stencil_shape(const pg_matrix* m, int* kind, int64_t* S, int64_t* g);
+// pg_spmv & co. run the plane-ring kernel on this matrix (planes.cu).
+bool plane_shape(const pg_matrix* m);
+// Fix the plane-ring launch plan of a new matrix (planes.cu).
+void plane_prepare(pg_matrix* m);
 // pg_spmv & co. run the row-pattern kernel on this matrix (spmv.cu).
 bool pattern_kernel(const pg_matrix* m);
 // pg_spmv & co. run the offset-pattern kernel on this matrix (spmv.cu).

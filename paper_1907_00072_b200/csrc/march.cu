@@ -44,39 +44,6 @@ struct MarchArgs {
   int Z, nqb;
 };
 
-// per-kind shape: NO entries in each outer plane group, NM in the middle one;
-// FULL = all three groups use the same in-plane offsets (tensor stencils)
-template <int KIND>
-struct MarchShape;
-template <>
-struct MarchShape<27> {
-  static constexpr int NO = 9, NM = 9, CTR = 4;
-  static constexpr bool FULL = true;
-};
-template <>
-struct MarchShape<9> {
-  static constexpr int NO = 3, NM = 3, CTR = 1;
-  static constexpr bool FULL = true;
-};
-template <>
-struct MarchShape<7> {
-  static constexpr int NO = 1, NM = 5, CTR = 2;
-  static constexpr bool FULL = false;
-};
-template <>
-struct MarchShape<5> {
-  static constexpr int NO = 1, NM = 3, CTR = 1;
-  static constexpr bool FULL = false;
-};
-
-// i-th in-plane offset of the middle group (of every group when FULL)
-template <int KIND>
-__device__ __forceinline__ int64_t mid_off(int i, int64_t g) {
-  if (KIND == 27) return (int64_t)(i / 3 - 1) * g + (i % 3 - 1);
-  if (KIND == 7) return i == 0 ? -g : (i == 4 ? g : (int64_t)(i - 2));
-  return (int64_t)(i - 1);  // 9, 5
-}
-
 __device__ __forceinline__ double ld_x(const double* __restrict__ x, int64_t idx, int64_t ncols) {
   return (uint64_t)idx < (uint64_t)ncols ? __ldg(x + idx) : 0.0;
 }
@@ -338,12 +305,8 @@ static int march_env(const char* name, int dflt) {
 
 // Decide whether the matrix's master pattern is a plane-marching stencil;
 // fills kind, S, g.  The master offsets are in stored (ascending) order.
-bool march_shape(const pg_matrix* m, int* kind, int64_t* S, int64_t* g) {
-  static int on = -1;
-  // opt-in: measured slower than the windowed kernel on cfg4 (111 vs 76 us
-  // per pass) and the pattern kernel on cfg2 (9.8 vs 9.3 us), DESIGN.md §3
-  if (on < 0) on = march_env("PG_SPMV_MARCH", 0);
-  if (!on || !m->rpat || m->perm || m->pat_mlen <= 0) return false;
+bool stencil_shape(const pg_matrix* m, int* kind, int64_t* S, int64_t* g) {
+  if (!m->rpat || m->perm || m->pat_mlen <= 0) return false;
   const int L = m->pat_mlen;
   const int32_t* o = m->pat_mdoff;
   std::vector<int64_t> want;
@@ -368,17 +331,24 @@ bool march_shape(const pg_matrix* m, int* kind, int64_t* S, int64_t* g) {
   } else {
     return false;
   }
-  // enough in-plane indices to fill whole warps (PG_MARCH_MIN_S, default
-  // 512); tensor offsets strictly ordered
-  static int min_s = -1;
-  if (min_s < 0) min_s = march_env("PG_MARCH_MIN_S", 512);
-  if (s < min_s || s <= 2 || ((L == 27 || L == 7) && (gg <= 2 || s <= 2 * gg + 2))) return false;
+  // tensor offsets strictly ordered
+  if (s <= 2 || ((L == 27 || L == 7) && (gg <= 2 || s <= 2 * gg + 2))) return false;
   for (int i = 0; i < L; ++i)
     if (want[i] != o[i]) return false;
   *kind = L;
   *S = s;
   *g = gg;
   return true;
+}
+
+bool march_shape(const pg_matrix* m, int* kind, int64_t* S, int64_t* g) {
+  static int on = -1, min_s = -1;
+  // opt-in: measured slower than the windowed kernel on cfg4 (111 vs 76 us
+  // per pass) and the pattern kernel on cfg2 (9.8 vs 9.3 us), DESIGN.md §3
+  if (on < 0) on = march_env("PG_SPMV_MARCH", 0);
+  // enough in-plane indices to fill whole warps (PG_MARCH_MIN_S, default 512)
+  if (min_s < 0) min_s = march_env("PG_MARCH_MIN_S", 512);
+  return on && stencil_shape(m, kind, S, g) && *S >= min_s;
 }
 
 template <int MODE>

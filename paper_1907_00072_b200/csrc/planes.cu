@@ -1,0 +1,489 @@
+// Plane-ring SpMV for row-pattern plane stencils.
+//
+// The matrix is a constant-coefficient stencil in natural row order whose
+// master pattern (abi.cu build_patterns) splits into three plane groups
+// dz = -1, 0, +1 of a plane stride S (stencil_shape, march.cu): config 4's
+// 27-point operator, config 2's 7-point one, the 2-D 9/5-point ones (a
+// "plane" is then a grid line).  A block owns a tile of Q consecutive
+// in-plane indices and marches it through a chunk of planes.  One producer
+// lane streams, per plane p, the tile's x window (Q + 2H doubles, H the
+// in-plane halo), the pattern ids of the rows of plane p+1 and the epilogue
+// operands of the rows of plane p-1 into a shared-memory ring with
+// cp.async.bulk (TMA) completing on mbarriers.  The row threads read each
+// window value ONCE per plane (9 shared loads per 27-point row instead of
+// 27) and use it three times: plane p closes the sums of the rows of plane
+// p-1 (their dz = +1 group), continues those of plane p (dz = 0) and opens
+// those of plane p+1 (dz = -1).  Three running sums per in-plane index stay
+// in registers.
+//
+// Arithmetic is unchanged.  A row's stored entries are its dz = -1 group,
+// then dz = 0, then dz = +1, each in ascending in-plane order (the CSR
+// column order), and the row's sum receives them in exactly that sequence,
+// one separately rounded product and sum per entry, starting from 0.0: the
+// same operations in the same order as the row-sequential kernels and the
+// reference (sparse.py:151-168); the fused epilogue is the shared one
+// (polyprec.py:205-211).  Boundary rows (master subsequences) add only their
+// own entries; rows that are not master subsequences are summed from their
+// pattern table with global gathers when they close.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "pipeline.cuh"
+#include "sell.cuh"
+
+namespace pg {
+
+constexpr int kPlaneRowThreads = 288;  // 9 row warps
+constexpr int kPlaneThreads = kPlaneRowThreads + 32;  // + the producer warp
+constexpr int kPlaneRPT = 2;  // in-plane indices per row thread: t, t + 288
+constexpr int kPlaneMaxQ = kPlaneRowThreads * kPlaneRPT;
+constexpr int kPlaneMaxStages = 8;
+// timing experiments only (tools/build_variant.sh): 1 = no x-window copies,
+// 2 = no operand copies, 4 = row threads skip the arithmetic and stores,
+// 8 = no stores (a never-true test keeps the arithmetic), 16 = every warp
+// takes the interior path (wrong results at boundary rows)
+#ifndef PG_PLANE_EXP
+#define PG_PLANE_EXP 0
+#endif
+#ifndef PG_PLANE_MIN_BLOCKS
+#define PG_PLANE_MIN_BLOCKS 2
+#endif
+// dynamic shared memory per block (ring), leaving room for PG_PLANE_MIN_BLOCKS
+constexpr int kPlaneSmemBudget = 200 * 1024 / PG_PLANE_MIN_BLOCKS;
+
+
+// Window position of middle-group value i relative to the row's slot, with
+// the stencil's consecutive runs made explicit (one runtime base per run,
+// the rest immediate offsets)
+template <int KIND>
+__device__ __forceinline__ int win_off(int i, const PlaneArgs& pa) {
+  if (KIND == 27) return pa.woff[3 * (i / 3)] + i % 3;
+  if (KIND == 7) return i == 0 ? pa.woff[0] : (i == 4 ? pa.woff[4] : pa.woff[1] + (i - 1));
+  return pa.woff[0] + i;  // 9, 5: dx = -1, 0, 1
+}
+
+template <int MODE, int KIND>
+__global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
+    plane_ring_kernel(PlaneArgs pa, const uint8_t* __restrict__ rpat,
+                      const int32_t* __restrict__ pptr, const PairEnt* __restrict__ pent,
+                      int npat, const uint32_t* __restrict__ pmask, const PatMaster pm,
+                      const double* __restrict__ x, Epi e, double* partials,
+                      unsigned int* counter, double* nsq) {
+  using Sh = MarchShape<KIND>;
+  constexpr int NO = Sh::NO, NM = Sh::NM, LEN = 2 * NO + NM;
+  constexpr uint32_t kFull = (1u << LEN) - 1u;
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  extern __shared__ __align__(128) unsigned char smem_plane[];
+  __shared__ uint32_t s_mask[256];
+  __shared__ __align__(8) uint64_t full[kPlaneMaxStages];
+  __shared__ __align__(8) uint64_t empty[kPlaneMaxStages];
+  // the masks never change after matrix creation: staged before the wait
+  // (a pattern that is not a master subsequence: bit 31 + its id)
+  for (int i = threadIdx.x; i < npat; i += blockDim.x) {
+    const uint32_t mk = pmask[i];
+    s_mask[i] = (mk >> 31) ? (0x80000000u | (uint32_t)i) : mk;
+  }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  const int NS = pa.stages;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kPlaneRowThreads / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int qb = (int)(blockIdx.x % (unsigned)pa.nqb);
+  const int64_t za = (int64_t)(blockIdx.x / (unsigned)pa.nqb) * pa.Zc;
+  const int64_t zb = min(za + (int64_t)pa.Zc, pa.nz);
+  const int64_t S = pa.S;
+  const int64_t q0 = (int64_t)qb * pa.Q;
+  const int Qt = (int)min((int64_t)pa.Q, S - q0);
+  // stages: planes za - 1 .. zb
+  const int nstage = (int)(zb - za) + 2;
+  double local = 0.0;
+  const int warp = threadIdx.x >> 5;
+
+  if (warp == kPlaneRowThreads / 32) {
+    if ((threadIdx.x & 31) == 0) {
+      const double *A, *B;
+      epi_vectors<MODE>(e, x, A, B);
+      // window doubles per plane: Qt + 2H + sh rounded up to even
+      const int wl = (Qt + 2 * pa.H + pa.sh + 1) & ~1;
+      int st = 0, round = 0;
+      for (int k = 0; k < nstage; ++k) {
+        if (round > 0) mbar_wait(&empty[st], (uint32_t)((round - 1) & 1));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        unsigned char* buf = smem_plane + (size_t)st * pa.stage_bytes;
+        double* win = reinterpret_cast<double*>(buf);
+        const int64_t p = za - 1 + k;
+        // window of plane p: [p S + q0 - H - sh, p S + q0 + Qt + H + 1), both
+        // ends even (16-byte aligned bulk copies), clipped to [0, ncols): any
+        // part of it may lie in another plane or the ghost slots; entries a
+        // row does not store are never added.  Only a window clipped at an
+        // odd ncols has a tail element, copied plainly.
+        const int64_t ga = p * S + q0 - pa.H - pa.sh;
+        int64_t ca = max(ga, (int64_t)0);
+        const int64_t ce = min(ga + wl, pa.ncols);
+        const int64_t n = ce > ca ? ce - ca : 0;
+        if (n & 1) win[ca - ga + n - 1] = __ldg(x + ca + n - 1);
+        ca -= ga;  // now the window position of the first copied element
+        const bool start = p + 1 < zb;     // rows of plane p + 1 open
+        const bool close = p - 1 >= za;    // rows of plane p - 1 close
+        uint32_t bytes = 8u * (uint32_t)(n & ~(int64_t)1);
+        if (start) bytes += (uint32_t)Qt;
+        if (close && A) bytes += 8u * (uint32_t)Qt;
+        if (close && B) bytes += 8u * (uint32_t)Qt;
+        if (PG_PLANE_EXP & 1) bytes -= 8u * (uint32_t)(n & ~(int64_t)1);
+        if (PG_PLANE_EXP & 2) bytes -= ((close && A) + (close && B)) * 8u * (uint32_t)Qt;
+        mbar_expect_tx(&full[st], bytes);
+        if (n > 1 && !(PG_PLANE_EXP & 1)) bulk_g2s(win + ca, x + ga + ca, 8u * (uint32_t)(n & ~(int64_t)1), &full[st]);
+        if (start) bulk_g2s(buf + pa.off_p, rpat + (p + 1) * S + q0, (uint32_t)Qt, &full[st]);
+        if (close && A && !(PG_PLANE_EXP & 2))
+          bulk_g2s(buf + pa.off_a, A + (p - 1) * S + q0, 8u * (uint32_t)Qt, &full[st]);
+        if (close && B && !(PG_PLANE_EXP & 2))
+          bulk_g2s(buf + pa.off_b, B + (p - 1) * S + q0, 8u * (uint32_t)Qt, &full[st]);
+        if (++st == NS) {
+          st = 0;
+          ++round;
+        }
+      }
+    }
+  } else {
+    const int t = threadIdx.x;
+    const double *A, *B;
+    epi_vectors<MODE>(e, x, A, B);
+    // Per in-plane index h, the rows closing (f) and continuing (m) at the
+    // current plane: running sums and pattern masks (a pattern that is not a
+    // master subsequence carries bit 31 and its id in the low bits).
+    double acc_f[kPlaneRPT], acc_m[kPlaneRPT];
+    uint32_t mk_f[kPlaneRPT], mk_m[kPlaneRPT];
+    // local in-plane indices of this thread (an inactive index reads slot 0:
+    // in range, never used)
+    int jj[kPlaneRPT];
+    bool act[kPlaneRPT];
+#pragma unroll
+    for (int h = 0; h < kPlaneRPT; ++h) {
+      const int j = t + h * kPlaneRowThreads;
+      act[h] = j < Qt;
+      jj[h] = act[h] ? j : 0;
+      acc_f[h] = acc_m[h] = 0.0;
+      mk_f[h] = mk_m[h] = kFull;
+    }
+    constexpr uint32_t kMid = (1u << NM) - 1u;
+    // the row mask of a "box" row with in-plane entries qm: all three plane
+    // groups present
+    auto box = [](uint32_t qm) -> uint32_t {
+      return Sh::FULL ? (qm | (qm << NO) | (qm << (NO + NM)))
+                      : (1u | (qm << NO) | (1u << (NO + NM)));
+    };
+    int st = 0;
+    uint32_t phase = 0;
+    const unsigned char* buf = smem_plane;
+    auto next_slot = [&]() {
+      __syncwarp();
+      if ((t & 31) == 0) mbar_arrive(&empty[st]);
+      buf += pa.stage_bytes;
+      if (++st == NS) {
+        st = 0;
+        phase ^= 1u;
+        buf = smem_plane;
+      }
+    };
+    // masks of the rows opening at plane p (their pattern ids are staged)
+    auto open_masks = [&](uint32_t (&mk_s)[kPlaneRPT], bool start) {
+#pragma unroll
+      for (int h = 0; h < kPlaneRPT; ++h)
+        mk_s[h] = (start && act[h]) ? s_mask[buf[pa.off_p + jj[h]]] : kFull;
+    };
+    auto rotate = [&](const double (&acc_s)[kPlaneRPT], const uint32_t (&mk_s)[kPlaneRPT]) {
+#pragma unroll
+      for (int h = 0; h < kPlaneRPT; ++h) {
+        acc_f[h] = acc_m[h];
+        mk_f[h] = mk_m[h];
+        acc_m[h] = acc_s[h];
+        mk_m[h] = mk_s[h];
+      }
+    };
+    auto finish = [&](int h, int64_t row, double acc) {
+      Pre pre{0.0, 0.0};
+      if (A) pre.a = reinterpret_cast<const double*>(buf + pa.off_a)[jj[h]];
+      if (B) pre.b = reinterpret_cast<const double*>(buf + pa.off_b)[jj[h]];
+      if (!(PG_PLANE_EXP & 8) || acc == 1.2345e300) {
+        const double r = epilogue<MODE>(e, pre, row, acc);
+        if (MODE == kResid) local = __fma_rn(r, r, local);
+      }
+    };
+    // Any stage: per-lane masked adds; rows that are not master
+    // subsequences are summed from their pattern table when they close.
+    auto general = [&](int p, bool close, bool mid, bool start,
+                       const uint32_t (&mk_s)[kPlaneRPT]) {
+      const double* win = reinterpret_cast<const double*>(buf);
+      double acc_s[kPlaneRPT];
+#pragma unroll
+      for (int h = 0; h < kPlaneRPT; ++h) {
+        const int j = jj[h];
+        double P[NM];
+#pragma unroll
+        for (int i = 0; i < NM; ++i) P[i] = win[j + win_off<KIND>(i, pa)];
+        // outer-group value i (dz = -1 or +1): the same in-plane offsets as
+        // the middle group (tensor stencils) or the center (cross stencils)
+        auto outer = [&](int i) { return Sh::FULL ? P[i] : P[Sh::CTR]; };
+        acc_s[h] = 0.0;
+        if (close && act[h]) {  // rows of plane p - 1: dz = +1 group, then the epilogue
+          const int64_t row = (int64_t)(p - 1) * S + q0 + j;
+          double acc = acc_f[h];
+          const uint32_t mk = mk_f[h];
+          if (mk >> 31) {
+            const int pid = (int)(mk & 255u);
+            acc = row_sum_pattern<false>(__ldg(pptr + pid), __ldg(pptr + pid + 1), row, x, pent);
+          } else {
+#pragma unroll
+            for (int i = 0; i < NO; ++i)
+              if (mk & (1u << (NO + NM + i)))
+                acc = __dadd_rn(acc, __dmul_rn(pm.v[NO + NM + i], outer(i)));
+          }
+          finish(h, row, acc);
+        }
+        if (mid && act[h]) {  // rows of plane p: dz = 0 group
+          double acc = acc_m[h];
+#pragma unroll
+          for (int i = 0; i < NM; ++i)
+            if (mk_m[h] & (1u << (NO + i))) acc = __dadd_rn(acc, __dmul_rn(pm.v[NO + i], P[i]));
+          acc_m[h] = acc;
+        }
+        if (start && act[h]) {  // rows of plane p + 1: dz = -1 group
+          double acc = 0.0;
+#pragma unroll
+          for (int i = 0; i < NO; ++i)
+            if (mk_s[h] & (1u << i)) acc = __dadd_rn(acc, __dmul_rn(pm.v[i], outer(i)));
+          acc_s[h] = acc;
+        }
+      }
+      rotate(acc_s, mk_s);
+    };
+    // Steady stage (rows close, continue and open): the unrolled path when,
+    // for every row of the warp, the closing, continuing and opening rows at
+    // its in-plane index are the same "box" row -- all three plane groups
+    // present, each holding the in-plane entries qm (interior rows: all of
+    // them).  Window values outside qm are zeroed: a product with +-0.0 added
+    // to a running sum leaves it unchanged (the sum starts at +0.0 and a
+    // round-to-nearest sum is never -0.0), so each row still receives
+    // exactly its own entries, in order.  Other warps take the general path.
+    auto steady = [&](int p) {
+      uint32_t mk_s[kPlaneRPT], qm[kPlaneRPT];
+      open_masks(mk_s, true);
+      bool ok = true, partial = false;
+#pragma unroll
+      for (int h = 0; h < kPlaneRPT; ++h) {
+        qm[h] = (mk_m[h] >> NO) & kMid;
+        const uint32_t b = box(qm[h]);
+        ok = ok && mk_f[h] == b && mk_m[h] == b && mk_s[h] == b;
+        partial = partial || qm[h] != kMid;
+      }
+      if (PG_PLANE_EXP & 4) return;
+      if (!((PG_PLANE_EXP & 16) || __all_sync(0xffffffffu, ok))) {
+        general(p, true, true, true, mk_s);
+        return;
+      }
+      const double* win = reinterpret_cast<const double*>(buf);
+      double P[kPlaneRPT][NM];
+#pragma unroll
+      for (int h = 0; h < kPlaneRPT; ++h)
+#pragma unroll
+        for (int i = 0; i < NM; ++i) P[h][i] = win[jj[h] + win_off<KIND>(i, pa)];
+      if (__any_sync(0xffffffffu, partial)) {
+#pragma unroll
+        for (int h = 0; h < kPlaneRPT; ++h)
+#pragma unroll
+          for (int i = 0; i < NM; ++i)
+            if (!((qm[h] >> i) & 1u)) P[h][i] = 0.0;
+      }
+      // six independent chains (close / continue / open x 2 indices), each
+      // in its row's stored order
+      double acc_s[kPlaneRPT];
+#pragma unroll
+      for (int h = 0; h < kPlaneRPT; ++h) acc_s[h] = 0.0;
+#pragma unroll
+      for (int i = 0; i < NM; ++i) {
+#pragma unroll
+        for (int h = 0; h < kPlaneRPT; ++h) {
+          if (i < NO) {
+            const double o = Sh::FULL ? P[h][i] : P[h][Sh::CTR];
+            acc_f[h] = __dadd_rn(acc_f[h], __dmul_rn(pm.v[NO + NM + i], o));
+            acc_s[h] = __dadd_rn(acc_s[h], __dmul_rn(pm.v[i], o));
+          }
+          acc_m[h] = __dadd_rn(acc_m[h], __dmul_rn(pm.v[NO + i], P[h][i]));
+        }
+      }
+      const int64_t rb = (int64_t)(p - 1) * S + q0;
+#pragma unroll
+      for (int h = 0; h < kPlaneRPT; ++h)
+        if (act[h]) finish(h, rb + jj[h], acc_f[h]);
+      rotate(acc_s, mk_s);
+    };
+    // planes za - 1, za: warm-up; za + 1 .. zb - 2: steady; zb - 1, zb: drain
+    const int pa0 = (int)za, pb0 = (int)zb;
+    for (int p = pa0 - 1; p <= pb0; ++p) {
+      mbar_wait(&full[st], phase);
+      if (p >= pa0 + 1 && p <= pb0 - 2) {
+        steady(p);
+      } else {
+        const bool start = p + 1 < pb0;
+        uint32_t mk_s[kPlaneRPT];
+        open_masks(mk_s, start);
+        general(p, p - 1 >= pa0, p >= pa0 && p < pb0, start, mk_s);
+      }
+      next_slot();
+    }
+  }
+  if (MODE == kResid) {
+    const double s = block_sum(local);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    last_block_reduce(partials, counter, 1, nsq);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static int plane_env(const char* name, int dflt) {
+  const char* s = std::getenv(name);
+  return s ? std::atoi(s) : dflt;
+}
+
+// in-plane offset of middle-group value i
+static int64_t mid_off_host(int kind, int i, int64_t g) {
+  if (kind == 27) return (int64_t)(i / 3 - 1) * g + (i % 3 - 1);
+  if (kind == 7) return i == 0 ? -g : (i == 4 ? g : (int64_t)(i - 2));
+  return (int64_t)(i - 1);
+}
+
+// Tile width Q and planes per chunk Zc: the pair that minimises
+// waves x (Q + H/2) x (Zc + 2 warm-up planes) for the resident blocks (all
+// blocks of a wave march the same planes together, so the tiles' halo reads
+// of a plane hit L2), with at most kMaxBlocks blocks (the residual's partial
+// slots).  PG_PLANE_Q / PG_PLANE_Z / PG_PLANE_STAGES override.
+void plane_prepare(pg_matrix* m) {
+  m->plane_kind = 0;
+  // 1 (default): 27-point stencils; 2: every plane stencil; 0: off
+  const int on = plane_env("PG_SPMV_PLANES", 1);
+  if (!on) return;
+  int kind;
+  int64_t S, g;
+  if (!stencil_shape(m, &kind, &S, &g)) return;
+  if (on == 1 && kind != 27) return;
+  // 16-byte aligned pattern-id / operand slices and whole planes
+  if (S % 16 != 0 || m->nrows % S != 0 || m->n_pat > 256) return;
+  // zeroed window values stand for absent entries (v * 0.0 = +-0.0): finite
+  // master values only
+  for (int i = 0; i < m->pat_mlen; ++i)
+    if (!std::isfinite(m->pat_mv[i])) return;
+  const int NM = kind == 27 ? 9 : kind == 7 ? 5 : 3;
+  const int64_t H = (kind == 27) ? g + 1 : (kind == 7 ? g : 1);
+  const int64_t nz = m->nrows / S;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
+  const int64_t cap = (int64_t)sms * PG_PLANE_MIN_BLOCKS;
+  const int qenv = plane_env("PG_PLANE_Q", 0), zenv = plane_env("PG_PLANE_Z", 0);
+  double best = 1e300;
+  int bq = 0;
+  int64_t bz = 0;
+  for (int Q = 64; Q <= kPlaneMaxQ; Q += 32) {
+    if (qenv > 0 && Q != qenv) continue;
+    const int64_t sb = 8 * (Q + 2 * H + 2) + 17 * (int64_t)Q + 256;
+    if (2 * sb > kPlaneSmemBudget) continue;
+    const int64_t nqb = (S + Q - 1) / Q;
+    int64_t last = -1;
+    for (int64_t nch = 1; nch <= nz; ++nch) {
+      const int64_t Zc = zenv > 0 ? std::min<int64_t>(zenv, nz) : (nz + nch - 1) / nch;
+      if (Zc == last) continue;
+      last = Zc;
+      const int64_t items = nqb * ((nz + Zc - 1) / Zc);
+      if (items > kMaxBlocks) continue;
+      const int64_t waves = (items + cap - 1) / cap;
+      const double cost = (double)waves * (Q + 0.5 * H) * (double)(Zc + 2);
+      if (cost < best) {
+        best = cost;
+        bq = Q;
+        bz = Zc;
+      }
+    }
+  }
+  if (!bq) return;
+  PlaneArgs& pa = m->plane;
+  std::memset(&pa, 0, sizeof pa);
+  pa.nrows = m->nrows;
+  pa.ncols = m->ncols;
+  pa.S = S;
+  pa.nz = nz;
+  pa.Q = bq;
+  pa.nqb = (int)((S + bq - 1) / bq);
+  pa.Zc = (int)bz;
+  pa.H = (int)H;
+  pa.sh = (int)(H & 1);
+  const int wdoubles = bq + 2 * (int)H + 2;
+  pa.off_a = ((8 * wdoubles + 127) / 128) * 128;
+  pa.off_b = pa.off_a + 8 * bq;
+  pa.off_p = pa.off_b + 8 * bq;
+  pa.stage_bytes = ((pa.off_p + bq + 127) / 128) * 128;
+  int stages = kPlaneSmemBudget / pa.stage_bytes;
+  const int senv = plane_env("PG_PLANE_STAGES", 0);
+  if (senv > 0 && senv * pa.stage_bytes <= kPlaneSmemBudget) stages = senv;
+  if (stages > kPlaneMaxStages) stages = kPlaneMaxStages;
+  if (stages < 2) return;
+  pa.stages = stages;
+  for (int i = 0; i < NM; ++i) pa.woff[i] = (int)(mid_off_host(kind, i, g) + H + pa.sh);
+  m->plane_blocks = (int)((int64_t)pa.nqb * ((nz + bz - 1) / bz));
+  m->plane_kind = kind;
+}
+
+bool plane_shape(const pg_matrix* m) { return m->plane_kind != 0; }
+
+template <int MODE>
+bool plane_launch(const pg_matrix* m, const double* x, Epi e, pg_workspace* ws, double* nsq,
+                  cudaStream_t st) {
+  if (!m->plane_kind) return false;
+  // every bulk-copied vector 16-byte aligned
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+  if (!(al16(x) && al16(e.acc_in) && al16(e.base) && al16(e.b) && al16(m->rpat))) return false;
+  if (MODE == kResid && !ws) return false;
+  PatMaster pm;
+  std::memset(&pm, 0, sizeof pm);
+  pm.len = m->pat_mlen;
+  for (int i = 0; i < pm.len; ++i) pm.v[i] = m->pat_mv[i];
+  const size_t smem = (size_t)m->plane.stages * m->plane.stage_bytes;
+  auto kern = m->plane_kind == 27 ? plane_ring_kernel<MODE, 27>
+            : m->plane_kind == 7  ? plane_ring_kernel<MODE, 7>
+            : m->plane_kind == 9  ? plane_ring_kernel<MODE, 9>
+                            : plane_ring_kernel<MODE, 5>;
+  static bool attr[4][4][64] = {};
+  const int ki = m->plane_kind == 27 ? 0 : m->plane_kind == 7 ? 1 : m->plane_kind == 9 ? 2 : 3;
+  const int dev = m->device;
+  if (!attr[MODE][ki][dev]) {
+    PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kPlaneSmemBudget));
+    attr[MODE][ki][dev] = true;
+  }
+  launch_k(kern, m->plane_blocks, kPlaneThreads, smem, st, m->plane, (const uint8_t*)m->rpat,
+           (const int32_t*)m->pat_ptr, (const PairEnt*)m->pat_ent, m->n_pat,
+           (const uint32_t*)m->pat_mask, pm, x, e, ws ? ws->partials : nullptr,
+           ws ? ws->counter : nullptr, nsq);
+  check_launch();
+  return true;
+}
+
+template bool plane_launch<kSpmv>(const pg_matrix*, const double*, Epi, pg_workspace*, double*,
+                                  cudaStream_t);
+template bool plane_launch<kPoly>(const pg_matrix*, const double*, Epi, pg_workspace*, double*,
+                                  cudaStream_t);
+template bool plane_launch<kResid>(const pg_matrix*, const double*, Epi, pg_workspace*, double*,
+                                   cudaStream_t);
+template bool plane_launch<kRoot>(const pg_matrix*, const double*, Epi, pg_workspace*, double*,
+                                  cudaStream_t);
+
+}  // namespace pg

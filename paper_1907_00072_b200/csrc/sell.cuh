@@ -84,6 +84,23 @@ __device__ __forceinline__ Pre epi_load(const Epi& e, const double* __restrict__
   return p;
 }
 
+// The epilogue operands a row reads (epi_load), as whole vectors so that the
+// producer can stage the block's slice of them: A -> Pre::a, B -> Pre::b.
+template <int MODE>
+__device__ __forceinline__ void epi_vectors(const Epi& e, const double* x, const double*& A,
+                                            const double*& B) {
+  A = B = nullptr;
+  if (MODE == kPoly) {
+    A = (e.flags & PG_PASS_FIRST) ? x : e.acc_in;
+    B = e.base;
+  } else if (MODE == kResid) {
+    A = e.b;
+  } else if (MODE == kRoot) {
+    A = ((e.flags & 3) == PG_ROOT_PAIR_B) ? e.base : x;
+    B = e.acc_in;
+  }
+}
+
 // Row epilogue; returns the residual entry (kResid) for the norm.
 template <int MODE>
 __device__ __forceinline__ double epilogue(const Epi& e, const Pre& p, int64_t row, double ax) {
@@ -332,10 +349,49 @@ __device__ __forceinline__ double row_sum_omaster(uint32_t mask, const PatMaster
   return acc;
 }
 
+// Plane stencils (march.cu, planes.cu): a row-pattern master whose offsets
+// are three plane groups dz = -1, 0, +1 of a plane stride S.
+// per-kind shape: NO entries in each outer plane group, NM in the middle one;
+// FULL = all three groups use the same in-plane offsets (tensor stencils)
+template <int KIND>
+struct MarchShape;
+template <>
+struct MarchShape<27> {
+  static constexpr int NO = 9, NM = 9, CTR = 4;
+  static constexpr bool FULL = true;
+};
+template <>
+struct MarchShape<9> {
+  static constexpr int NO = 3, NM = 3, CTR = 1;
+  static constexpr bool FULL = true;
+};
+template <>
+struct MarchShape<7> {
+  static constexpr int NO = 1, NM = 5, CTR = 2;
+  static constexpr bool FULL = false;
+};
+template <>
+struct MarchShape<5> {
+  static constexpr int NO = 1, NM = 3, CTR = 1;
+  static constexpr bool FULL = false;
+};
+
+// i-th in-plane offset of the middle group (of every group when FULL)
+template <int KIND>
+__device__ __forceinline__ int64_t mid_off(int i, int64_t g) {
+  if (KIND == 27) return (int64_t)(i / 3 - 1) * g + (i % 3 - 1);
+  if (KIND == 7) return i == 0 ? -g : (i == 4 ? g : (int64_t)(i - 2));
+  return (int64_t)(i - 1);  // 9, 5
+}
+
 // Plane-marching SpMV (march.cu): issues the pass and returns true when the
 // matrix is a row-pattern stencil it handles (march_shape), else false.
 template <int MODE>
 bool march_launch(const pg_matrix* m, const double* x, Epi e, pg_workspace* ws, double* nsq,
+                  cudaStream_t st);
+// Plane-ring SpMV (planes.cu): same contract as march_launch.
+template <int MODE>
+bool plane_launch(const pg_matrix* m, const double* x, Epi e, pg_workspace* ws, double* nsq,
                   cudaStream_t st);
 
 }  // namespace pg

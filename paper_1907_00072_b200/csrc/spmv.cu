@@ -464,23 +464,6 @@ struct WinArgs {
   int32_t lo[kWinMaxGroups], start[kWinMaxGroups], len[kWinMaxGroups];
 };
 
-// The epilogue operands a row reads (epi_load), as whole vectors so that the
-// producer can stage the block's slice of them: A -> Pre::a, B -> Pre::b.
-template <int MODE>
-__device__ __forceinline__ void epi_vectors(const Epi& e, const double* x, const double*& A,
-                                            const double*& B) {
-  A = B = nullptr;
-  if (MODE == kPoly) {
-    A = (e.flags & PG_PASS_FIRST) ? x : e.acc_in;
-    B = e.base;
-  } else if (MODE == kResid) {
-    A = e.b;
-  } else if (MODE == kRoot) {
-    A = ((e.flags & 3) == PG_ROOT_PAIR_B) ? e.base : x;
-    B = e.acc_in;
-  }
-}
-
 // Row sum over the pair stream: per entry one byte -> one 16-byte table
 // entry {value, window byte offset} -> one window load, mul, add.  Full
 // 4-entry chunks run without predicates; only the row's last partial chunk
@@ -873,7 +856,9 @@ static void launch_sell(const pg_matrix* m, const double* x, Epi e, pg_workspace
   }
   const int dev = m->device;
   PG_REQUIRE(dev >= 0 && dev < 64, PG_ERR_PARAMETER, "device ordinal out of range");
-  // stencil row patterns: the plane-marching kernel (march.cu)
+  // plane stencils: the plane-ring kernel (planes.cu), else the opt-in
+  // plane-marching kernel (march.cu)
+  if (plane_launch<MODE>(m, x, e, ws, nsq, st)) return;
   if (march_launch<MODE>(m, x, e, ws, nsq, st)) return;
   double* part = ws ? ws->partials : nullptr;
   unsigned* cnt = ws ? ws->counter : nullptr;

@@ -216,7 +216,7 @@ class Shard:
         + 1 B per row for the offset-pattern format; else the
         stored entry bytes + a 4-byte row length), the compulsory gather of x
         (8 B per row) and ``vec_bytes`` per row of epilogue vectors."""
-        if self.stats["kernel"] in (5, 6, 8):  # row patterns (gather, windowed, marching)
+        if self.stats["kernel"] in (5, 6, 8, 9):  # row patterns (gather, windowed, marching, plane ring)
             return (1 + 8 + vec_bytes) * self.n
         if self.stats["kernel"] == 7:  # offset patterns: f64 values + 1 B per row
             return 8 * self.nnz + (1 + 8 + vec_bytes) * self.n

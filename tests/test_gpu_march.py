@@ -77,7 +77,7 @@ def _check(h, shards=1):
 def _run_isolated(env, code):
     """Run `code` in a fresh interpreter (the kernel choice is read once per
     process) with `env` added; assert it succeeds."""
-    full = dict(os.environ, PG_SPMV_MARCH="1", PYTHONPATH=ROOT)
+    full = dict(os.environ, PG_SPMV_MARCH="1", PG_SPMV_PLANES="0", PYTHONPATH=ROOT)
     full.update(env)
     res = subprocess.run([sys.executable, "-c", code], env=full, capture_output=True, text=True,
                          cwd=ROOT, timeout=600)

@@ -6,11 +6,12 @@ name=$1; shift
 root=$(cd "$(dirname "$0")/.." && pwd)
 out=$root/variants_tmp/$name
 mkdir -p "$out"
-flags="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden,-ffp-contract=off -I $root/include"
-for f in abi spmv ortho host ilu step chain blasorder march; do
+nccl=$(python -c "from paper_1907_00072_b200._build import _nccl_include; print(_nccl_include())")
+flags="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden,-ffp-contract=off -I $root/include -I $nccl"
+for f in $(python -c "from paper_1907_00072_b200._build import SOURCES; print(' '.join(x[:-3] for x in SOURCES))"); do
   nvcc $flags "$@" -c "$root/paper_1907_00072_b200/csrc/$f.cu" -o "$out/$f.o" &
 done
 wait
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out/libpgmres.so" "$out"/*.o
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out/libpgmres.so" "$out"/*.o -ldl
 rm -f "$out"/*.o
 echo "$out/libpgmres.so"

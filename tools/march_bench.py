@@ -16,7 +16,7 @@ from paper_1907_00072_b200 import workloads as wl  # noqa: E402
 from paper_1907_00072_b200.device import Engine  # noqa: E402
 from spmv_bench import time_pass  # noqa: E402
 
-for key, kw in (("cfg4", {}), ("cfg2", {})):
+for key, kw in [(c, {}) for c in os.environ.get("CASES", "cfg4,cfg2").split(",")]:
     conf = wl.CONFIGS[int(key[-1])]
     A = wl.make_matrix(conf, **kw)
     e = Engine.build(A)
