@@ -170,6 +170,7 @@ static void free_matrix(pg_matrix* m) {
   cudaFree(m->pat_mask);
   cudaFree(m->opat);
   cudaFree(m->opat_mask);
+  cudaFree(m->plane_qm);
   cudaSetDevice(cur);
   delete m;
 }

@@ -131,6 +131,10 @@ struct pg_matrix {
   // plane-ring kernel (planes.cu): plane_kind 0 = not a plane stencil / off
   int plane_kind, plane_blocks;
   pg::PlaneArgs plane;
+  // plane_qm[q]: the in-plane entry mask of every interior-plane row at
+  // in-plane index q (host-verified: the same box pattern on planes
+  // 1 .. nz-2), or null when the rows do not have that structure
+  uint16_t* plane_qm;
   size_t bytes;
 };
 

@@ -30,15 +30,24 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "pipeline.cuh"
 #include "sell.cuh"
 
 namespace pg {
 
-constexpr int kPlaneRowThreads = 288;  // 9 row warps
+#ifndef PG_PLANE_ROW_THREADS
+#define PG_PLANE_ROW_THREADS 288
+#endif
+#ifndef PG_PLANE_RPT
+#define PG_PLANE_RPT 2
+#endif
+constexpr int kPlaneRowThreads = PG_PLANE_ROW_THREADS;  // row warps x 32
 constexpr int kPlaneThreads = kPlaneRowThreads + 32;  // + the producer warp
-constexpr int kPlaneRPT = 2;  // in-plane indices per row thread: t, t + 288
+// in-plane indices per row thread: t, t + kPlaneRowThreads, ...
+constexpr int kPlaneRPT = PG_PLANE_RPT;
+static_assert(kPlaneRPT % 2 == 0, "the steady path works on pairs of in-plane indices");
 constexpr int kPlaneMaxQ = kPlaneRowThreads * kPlaneRPT;
 constexpr int kPlaneMaxStages = 8;
 // timing experiments only (tools/build_variant.sh): 1 = no x-window copies,
@@ -65,13 +74,29 @@ __device__ __forceinline__ int win_off(int i, const PlaneArgs& pa) {
   return pa.woff[0] + i;  // 9, 5: dx = -1, 0, 1
 }
 
-template <int MODE, int KIND>
+// The row epilogue; EF >= 0 (kPoly only): the pass flags (PG_PASS_FIRST,
+// PG_PASS_WRITE_W) and base presence (4) as compile-time constants -- the
+// same operations in the same order as sell.cuh epilogue<kPoly>.
+template <int MODE, int EF>
+__device__ __forceinline__ double plane_epilogue(const Epi& e, const Pre& p, int64_t row,
+                                                 double ax) {
+  if (MODE != kPoly || EF < 0) return epilogue<MODE>(e, p, row, ax);
+  double t = (EF & PG_PASS_FIRST) ? __dmul_rn(e.y0, p.a) : p.a;
+  t = __dadd_rn(t, __dmul_rn(e.yk, ax));
+  if (EF & PG_PASS_WRITE_W) e.w_out[row] = ax;
+  if (EF & 4) t = __dadd_rn(p.b, t);
+  e.acc_out[row] = t;
+  return 0.0;
+}
+
+template <int MODE, int KIND, int EF>
 __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     plane_ring_kernel(PlaneArgs pa, const uint8_t* __restrict__ rpat,
                       const int32_t* __restrict__ pptr, const PairEnt* __restrict__ pent,
                       int npat, const uint32_t* __restrict__ pmask, const PatMaster pm,
                       const double* __restrict__ x, Epi e, double* partials,
-                      unsigned int* counter, double* nsq) {
+                      unsigned int* counter, double* nsq,
+                      const uint16_t* __restrict__ plane_qm) {
   using Sh = MarchShape<KIND>;
   constexpr int NO = Sh::NO, NM = Sh::NM, LEN = 2 * NO + NM;
   constexpr uint32_t kFull = (1u << LEN) - 1u;
@@ -134,15 +159,18 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
         ca -= ga;  // now the window position of the first copied element
         const bool start = p + 1 < zb;     // rows of plane p + 1 open
         const bool close = p - 1 >= za;    // rows of plane p - 1 close
+        // interior "box" stages read no pattern ids (plane_qm, see the row threads)
+        const bool boxed = plane_qm && p >= za + 1 && p + 2 <= zb && p >= 2 && p + 3 <= pa.nz;
+        const bool ids = start && !boxed;
         uint32_t bytes = 8u * (uint32_t)(n & ~(int64_t)1);
-        if (start) bytes += (uint32_t)Qt;
+        if (ids) bytes += (uint32_t)Qt;
         if (close && A) bytes += 8u * (uint32_t)Qt;
         if (close && B) bytes += 8u * (uint32_t)Qt;
         if (PG_PLANE_EXP & 1) bytes -= 8u * (uint32_t)(n & ~(int64_t)1);
         if (PG_PLANE_EXP & 2) bytes -= ((close && A) + (close && B)) * 8u * (uint32_t)Qt;
         mbar_expect_tx(&full[st], bytes);
         if (n > 1 && !(PG_PLANE_EXP & 1)) bulk_g2s(win + ca, x + ga + ca, 8u * (uint32_t)(n & ~(int64_t)1), &full[st]);
-        if (start) bulk_g2s(buf + pa.off_p, rpat + (p + 1) * S + q0, (uint32_t)Qt, &full[st]);
+        if (ids) bulk_g2s(buf + pa.off_p, rpat + (p + 1) * S + q0, (uint32_t)Qt, &full[st]);
         if (close && A && !(PG_PLANE_EXP & 2))
           bulk_g2s(buf + pa.off_a, A + (p - 1) * S + q0, 8u * (uint32_t)Qt, &full[st]);
         if (close && B && !(PG_PLANE_EXP & 2))
@@ -162,6 +190,9 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     // master subsequence carries bit 31 and its id in the low bits).
     double acc_f[kPlaneRPT], acc_m[kPlaneRPT];
     uint32_t mk_f[kPlaneRPT], mk_m[kPlaneRPT];
+    // "box" in-plane masks of those rows (see steady): the row's in-plane
+    // entries when all three plane groups hold exactly them, else kNoBox
+    uint32_t bq_f[kPlaneRPT], bq_m[kPlaneRPT];
     // local in-plane indices of this thread (an inactive index reads slot 0:
     // in range, never used)
     int jj[kPlaneRPT];
@@ -174,12 +205,16 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
       acc_f[h] = acc_m[h] = 0.0;
       mk_f[h] = mk_m[h] = kFull;
     }
-    constexpr uint32_t kMid = (1u << NM) - 1u;
-    // the row mask of a "box" row with in-plane entries qm: all three plane
-    // groups present
-    auto box = [](uint32_t qm) -> uint32_t {
-      return Sh::FULL ? (qm | (qm << NO) | (qm << (NO + NM)))
-                      : (1u | (qm << NO) | (1u << (NO + NM)));
+    constexpr uint32_t kMid = (1u << NM) - 1u, kNoBox = 0xffffffffu;
+#pragma unroll
+    for (int h = 0; h < kPlaneRPT; ++h) bq_f[h] = bq_m[h] = kMid;
+    // the in-plane mask of a "box" row (all three plane groups present, each
+    // holding the same in-plane entries), else kNoBox
+    auto boxq = [](uint32_t mk) -> uint32_t {
+      const uint32_t qm = (mk >> NO) & kMid;
+      const uint32_t b = Sh::FULL ? (qm | (qm << NO) | (qm << (NO + NM)))
+                                  : (1u | (qm << NO) | (1u << (NO + NM)));
+      return mk == b ? qm : kNoBox;
     };
     int st = 0;
     uint32_t phase = 0;
@@ -200,21 +235,25 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
       for (int h = 0; h < kPlaneRPT; ++h)
         mk_s[h] = (start && act[h]) ? s_mask[buf[pa.off_p + jj[h]]] : kFull;
     };
-    auto rotate = [&](const double (&acc_s)[kPlaneRPT], const uint32_t (&mk_s)[kPlaneRPT]) {
+    auto rotate = [&](const double (&acc_s)[kPlaneRPT], const uint32_t (&mk_s)[kPlaneRPT],
+                      const uint32_t (&bq_s)[kPlaneRPT]) {
 #pragma unroll
       for (int h = 0; h < kPlaneRPT; ++h) {
         acc_f[h] = acc_m[h];
         mk_f[h] = mk_m[h];
+        bq_f[h] = bq_m[h];
         acc_m[h] = acc_s[h];
         mk_m[h] = mk_s[h];
+        bq_m[h] = bq_s[h];
       }
     };
     auto finish = [&](int h, int64_t row, double acc) {
       Pre pre{0.0, 0.0};
-      if (A) pre.a = reinterpret_cast<const double*>(buf + pa.off_a)[jj[h]];
-      if (B) pre.b = reinterpret_cast<const double*>(buf + pa.off_b)[jj[h]];
+      if (EF >= 0 ? true : A != nullptr) pre.a = reinterpret_cast<const double*>(buf + pa.off_a)[jj[h]];
+      if (EF >= 0 ? (EF & 4) != 0 : B != nullptr)
+        pre.b = reinterpret_cast<const double*>(buf + pa.off_b)[jj[h]];
       if (!(PG_PLANE_EXP & 8) || acc == 1.2345e300) {
-        const double r = epilogue<MODE>(e, pre, row, acc);
+        const double r = plane_epilogue<MODE, EF>(e, pre, row, acc);
         if (MODE == kResid) local = __fma_rn(r, r, local);
       }
     };
@@ -264,7 +303,10 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
           acc_s[h] = acc;
         }
       }
-      rotate(acc_s, mk_s);
+      uint32_t bq_s[kPlaneRPT];
+#pragma unroll
+      for (int h = 0; h < kPlaneRPT; ++h) bq_s[h] = boxq(mk_s[h]);
+      rotate(acc_s, mk_s, bq_s);
     };
     // Steady stage (rows close, continue and open): the unrolled path when,
     // for every row of the warp, the closing, continuing and opening rows at
@@ -274,64 +316,98 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     // to a running sum leaves it unchanged (the sum starts at +0.0 and a
     // round-to-nearest sum is never -0.0), so each row still receives
     // exactly its own entries, in order.  Other warps take the general path.
+    // the unrolled interior body: every row of the warp at this stage is a
+    // box row with in-plane entries bq_m (closing, continuing and opening
+    // rows alike); zero: some lane's rows miss in-plane entries
+    auto body = [&](int p, const uint32_t (&mk_s)[kPlaneRPT], const uint32_t (&bq_s)[kPlaneRPT],
+                    bool zero) {
+      const double* win = reinterpret_cast<const double*>(buf);
+      const int64_t rb = (int64_t)(p - 1) * S + q0;
+      double acc_s[kPlaneRPT];
+      // pairs of in-plane indices: six independent chains each (close /
+      // continue / open x 2), every chain in its row's stored order
+#pragma unroll
+      for (int h0 = 0; h0 < kPlaneRPT; h0 += 2) {
+        double P[2][NM];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int i = 0; i < NM; ++i) P[u][i] = win[jj[h0 + u] + win_off<KIND>(i, pa)];
+        if (zero) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int i = 0; i < NM; ++i)
+              if (!((bq_m[h0 + u] >> i) & 1u)) P[u][i] = 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) acc_s[h0 + u] = 0.0;
+#pragma unroll
+        for (int i = 0; i < NM; ++i) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int h = h0 + u;
+            if (i < NO) {
+              const double o = Sh::FULL ? P[u][i] : P[u][Sh::CTR];
+              acc_f[h] = __dadd_rn(acc_f[h], __dmul_rn(pm.v[NO + NM + i], o));
+              acc_s[h] = __dadd_rn(acc_s[h], __dmul_rn(pm.v[i], o));
+            }
+            acc_m[h] = __dadd_rn(acc_m[h], __dmul_rn(pm.v[NO + i], P[u][i]));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (act[h0 + u]) finish(h0 + u, rb + jj[h0 + u], acc_f[h0 + u]);
+      }
+      rotate(acc_s, mk_s, bq_s);
+    };
+    // Steady stage (rows close, continue and open): the unrolled body when,
+    // for every row of the warp, the closing, continuing and opening rows at
+    // its in-plane index are the same "box" row -- all three plane groups
+    // present, each holding the in-plane entries qm (interior rows: all of
+    // them).  Window values outside qm are zeroed: a product with +-0.0 added
+    // to a running sum leaves it unchanged (the sum starts at +0.0 and a
+    // round-to-nearest sum is never -0.0), so each row still receives
+    // exactly its own entries, in order.  Other warps take the general path.
     auto steady = [&](int p) {
-      uint32_t mk_s[kPlaneRPT], qm[kPlaneRPT];
+      uint32_t mk_s[kPlaneRPT], bq_s[kPlaneRPT];
       open_masks(mk_s, true);
       bool ok = true, partial = false;
 #pragma unroll
       for (int h = 0; h < kPlaneRPT; ++h) {
-        qm[h] = (mk_m[h] >> NO) & kMid;
-        const uint32_t b = box(qm[h]);
-        ok = ok && mk_f[h] == b && mk_m[h] == b && mk_s[h] == b;
-        partial = partial || qm[h] != kMid;
+        bq_s[h] = boxq(mk_s[h]);
+        ok = ok && bq_f[h] == bq_m[h] && bq_m[h] == bq_s[h] && bq_s[h] != kNoBox;
+        partial = partial || bq_m[h] != kMid;
       }
       if (PG_PLANE_EXP & 4) return;
       if (!((PG_PLANE_EXP & 16) || __all_sync(0xffffffffu, ok))) {
         general(p, true, true, true, mk_s);
         return;
       }
-      const double* win = reinterpret_cast<const double*>(buf);
-      double P[kPlaneRPT][NM];
-#pragma unroll
-      for (int h = 0; h < kPlaneRPT; ++h)
-#pragma unroll
-        for (int i = 0; i < NM; ++i) P[h][i] = win[jj[h] + win_off<KIND>(i, pa)];
-      if (__any_sync(0xffffffffu, partial)) {
-#pragma unroll
-        for (int h = 0; h < kPlaneRPT; ++h)
-#pragma unroll
-          for (int i = 0; i < NM; ++i)
-            if (!((qm[h] >> i) & 1u)) P[h][i] = 0.0;
-      }
-      // six independent chains (close / continue / open x 2 indices), each
-      // in its row's stored order
-      double acc_s[kPlaneRPT];
-#pragma unroll
-      for (int h = 0; h < kPlaneRPT; ++h) acc_s[h] = 0.0;
-#pragma unroll
-      for (int i = 0; i < NM; ++i) {
-#pragma unroll
-        for (int h = 0; h < kPlaneRPT; ++h) {
-          if (i < NO) {
-            const double o = Sh::FULL ? P[h][i] : P[h][Sh::CTR];
-            acc_f[h] = __dadd_rn(acc_f[h], __dmul_rn(pm.v[NO + NM + i], o));
-            acc_s[h] = __dadd_rn(acc_s[h], __dmul_rn(pm.v[i], o));
-          }
-          acc_m[h] = __dadd_rn(acc_m[h], __dmul_rn(pm.v[NO + i], P[h][i]));
-        }
-      }
-      const int64_t rb = (int64_t)(p - 1) * S + q0;
-#pragma unroll
-      for (int h = 0; h < kPlaneRPT; ++h)
-        if (act[h]) finish(h, rb + jj[h], acc_f[h]);
-      rotate(acc_s, mk_s);
+      body(p, mk_s, bq_s, __any_sync(0xffffffffu, partial));
     };
+    // Interior planes of a host-verified matrix (plane_qm): the rows at
+    // in-plane index q are box rows with entries plane_qm[q] on every
+    // interior plane, so no pattern ids are read.
+    uint32_t qb_t[kPlaneRPT], mb_t[kPlaneRPT];
+    bool zero_t = false;
+#pragma unroll
+    for (int h = 0; h < kPlaneRPT; ++h) {
+      qb_t[h] = (plane_qm && act[h]) ? (uint32_t)__ldg(plane_qm + q0 + jj[h]) : kMid;
+      mb_t[h] = Sh::FULL ? (qb_t[h] | (qb_t[h] << NO) | (qb_t[h] << (NO + NM)))
+                         : (1u | (qb_t[h] << NO) | (1u << (NO + NM)));
+      zero_t = zero_t || qb_t[h] != kMid;
+    }
+    zero_t = __any_sync(0xffffffffu, zero_t);
     // planes za - 1, za: warm-up; za + 1 .. zb - 2: steady; zb - 1, zb: drain
     const int pa0 = (int)za, pb0 = (int)zb;
     for (int p = pa0 - 1; p <= pb0; ++p) {
       mbar_wait(&full[st], phase);
       if (p >= pa0 + 1 && p <= pb0 - 2) {
-        steady(p);
+        if (plane_qm && p >= 2 && p + 3 <= (int)pa.nz && !(PG_PLANE_EXP & 4))
+          body(p, mb_t, qb_t, zero_t);
+        else
+          steady(p);
       } else {
         const bool start = p + 1 < pb0;
         uint32_t mk_s[kPlaneRPT];
@@ -440,6 +516,34 @@ void plane_prepare(pg_matrix* m) {
   for (int i = 0; i < NM; ++i) pa.woff[i] = (int)(mid_off_host(kind, i, g) + H + pa.sh);
   m->plane_blocks = (int)((int64_t)pa.nqb * ((nz + bz - 1) / bz));
   m->plane_kind = kind;
+  // Interior planes 1 .. nz-2: if every in-plane index q has one pattern on
+  // all of them and that pattern is a "box" row (all three plane groups
+  // holding the same in-plane entries qm), the kernel's interior stages use
+  // qm[q] without reading pattern ids (PG_PLANE_BOX=0: always read them).
+  if (nz >= 3 && plane_env("PG_PLANE_BOX", 1)) {
+    std::vector<uint8_t> id((size_t)m->nrows);
+    std::vector<uint32_t> mk((size_t)m->n_pat);
+    PG_CUDA(cudaMemcpy(id.data(), m->rpat, id.size(), cudaMemcpyDeviceToHost));
+    PG_CUDA(cudaMemcpy(mk.data(), m->pat_mask, 4 * mk.size(), cudaMemcpyDeviceToHost));
+    const int NO = kind == 27 ? 9 : (kind == 9 ? 3 : 1);
+    const uint32_t mid = (1u << NM) - 1u;
+    std::vector<uint16_t> qm((size_t)S);
+    bool ok = true;
+    for (int64_t q = 0; q < S && ok; ++q) {
+      const uint8_t pid = id[(size_t)(S + q)];
+      for (int64_t z = 2; z + 1 < nz && ok; ++z) ok = id[(size_t)(z * S + q)] == pid;
+      const uint32_t mkq = mk[pid], m9 = (mkq >> NO) & mid;
+      const uint32_t box = (kind == 27 || kind == 9) ? (m9 | (m9 << NO) | (m9 << (NO + NM)))
+                                                   : (1u | (m9 << NO) | (1u << (NO + NM)));
+      ok = ok && mkq == box;
+      qm[(size_t)q] = (uint16_t)m9;
+    }
+    if (ok) {
+      PG_CUDA(cudaMalloc(&m->plane_qm, 2 * qm.size()));
+      PG_CUDA(cudaMemcpy(m->plane_qm, qm.data(), 2 * qm.size(), cudaMemcpyHostToDevice));
+      m->bytes += 2 * qm.size();
+    }
+  }
 }
 
 bool plane_shape(const pg_matrix* m) { return m->plane_kind != 0; }
@@ -457,12 +561,25 @@ bool plane_launch(const pg_matrix* m, const double* x, Epi e, pg_workspace* ws, 
   pm.len = m->pat_mlen;
   for (int i = 0; i < pm.len; ++i) pm.v[i] = m->pat_mv[i];
   const size_t smem = (size_t)m->plane.stages * m->plane.stage_bytes;
-  auto kern = m->plane_kind == 27 ? plane_ring_kernel<MODE, 27>
-            : m->plane_kind == 7  ? plane_ring_kernel<MODE, 7>
-            : m->plane_kind == 9  ? plane_ring_kernel<MODE, 9>
-                            : plane_ring_kernel<MODE, 5>;
-  static bool attr[4][4][64] = {};
-  const int ki = m->plane_kind == 27 ? 0 : m->plane_kind == 7 ? 1 : m->plane_kind == 9 ? 2 : 3;
+  // kPoly on 27-point stencils: the pass flags and base presence as
+  // compile-time constants (EF); else runtime flags (EF = -1)
+  const int ef = (e.flags & 3) | (e.base ? 4 : 0);
+  auto kern = plane_ring_kernel<MODE, 27, -1>;
+  int ki = 0;
+  if (MODE == kPoly && m->plane_kind == 27) {
+    kern = ef == 0 ? plane_ring_kernel<MODE, 27, 0> : ef == 1 ? plane_ring_kernel<MODE, 27, 1>
+         : ef == 2 ? plane_ring_kernel<MODE, 27, 2> : ef == 3 ? plane_ring_kernel<MODE, 27, 3>
+         : ef == 4 ? plane_ring_kernel<MODE, 27, 4> : ef == 5 ? plane_ring_kernel<MODE, 27, 5>
+         : ef == 6 ? plane_ring_kernel<MODE, 27, 6> : plane_ring_kernel<MODE, 27, 7>;
+    ki = 4 + ef;
+  } else {
+    kern = m->plane_kind == 27 ? plane_ring_kernel<MODE, 27, -1>
+         : m->plane_kind == 7  ? plane_ring_kernel<MODE, 7, -1>
+         : m->plane_kind == 9  ? plane_ring_kernel<MODE, 9, -1>
+                               : plane_ring_kernel<MODE, 5, -1>;
+    ki = m->plane_kind == 27 ? 0 : m->plane_kind == 7 ? 1 : m->plane_kind == 9 ? 2 : 3;
+  }
+  static bool attr[4][12][64] = {};
   const int dev = m->device;
   if (!attr[MODE][ki][dev]) {
     PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -472,7 +589,7 @@ bool plane_launch(const pg_matrix* m, const double* x, Epi e, pg_workspace* ws, 
   launch_k(kern, m->plane_blocks, kPlaneThreads, smem, st, m->plane, (const uint8_t*)m->rpat,
            (const int32_t*)m->pat_ptr, (const PairEnt*)m->pat_ent, m->n_pat,
            (const uint32_t*)m->pat_mask, pm, x, e, ws ? ws->partials : nullptr,
-           ws ? ws->counter : nullptr, nsq);
+           ws ? ws->counter : nullptr, nsq, (const uint16_t*)m->plane_qm);
   check_launch();
   return true;
 }

@@ -81,6 +81,8 @@ print("ok")
     {"PG_PLANE_Q": "96", "PG_PLANE_Z": "3", "PG_PLANE_STAGES": "2"},  # ring wraps every block
     {"PG_PLANE_Q": "576", "PG_PLANE_Z": "5"},     # the widest tile (second row set)
     {"PG_PLANE_STAGES": "3"},
+    {"PG_PLANE_BOX": "0"},                        # per-row pattern ids on every plane
+    {"PG_PLANE_BOX": "0", "PG_PLANE_Q": "64", "PG_PLANE_Z": "4"},
 ])
 def test_plane_kernel_selected_and_bitwise(env):
     env = dict(env, PG_SPMV_PLANES="2")

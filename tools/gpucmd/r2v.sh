@@ -1,0 +1,8 @@
+mkdir -p gpurun_out/r2v
+timeout 900 python -m pytest tests/test_gpu_planes.py -x -q > gpurun_out/r2v/pytest_planes.log 2>&1; echo "planes rc=$?"; tail -3 gpurun_out/r2v/pytest_planes.log | cut -c1-400
+cd tools
+export CASES=cfg4
+timeout 200 python march_bench.py 2>&1 | tail -1
+PG_PLANE_Q=896 timeout 150 python march_bench.py 2>&1 | tail -1
+for v in rpt2; do echo "== $v"; PG_LIB_PATH=../variants_tmp/$v/libpgmres.so timeout 150 python march_bench.py 2>&1 | tail -1; done
+for s in 2 3 4; do PG_PLANE_STAGES=$s PG_LIB_PATH=../variants_tmp/rpt2/libpgmres.so timeout 150 python march_bench.py 2>&1 | tail -1; done
