@@ -434,7 +434,7 @@ KERNEL_NAMES = {0: "sell_kernel<kPoly,0,0>", 1: "sell_kernel<kPoly,1,1>",
                 2: "sell_pair_kernel<kPoly>", 3: "sell_win_kernel<kPoly>",
                 4: "sell_pair_short_kernel<kPoly>", 5: "sell_pat_kernel<kPoly>",
                 6: "sell_win_kernel<kPoly, patterns>", 7: "sell_opat_kernel<kPoly>",
-                8: "sell_march_kernel<kPoly>"}
+                8: "sell_march_kernel<kPoly>", 9: "plane_ring_kernel<kPoly, 27>"}
 MATRIX_FORMATS = {
     0: "SELL-C-sigma (int32 column + f64 value, 12 B/entry)",
     1: "dictionary SELL (1 B offset + 1 B value index)",
@@ -445,6 +445,9 @@ MATRIX_FORMATS = {
     6: "row-pattern dictionary (1 B per row), x windows + pattern ids staged by a TMA ring",
     7: "offset-pattern SELL (1 B per row names the column offsets; f64 values, 8 B/entry)",
     8: "row-pattern dictionary (1 B per row), plane-marching: x planes kept in registers",
+    9: "row-pattern plane stencil: x plane windows, pattern ids (boundary planes only) and "
+       "epilogue operands staged by a TMA ring; each x value loaded once per plane, used by "
+       "three rows",
 }
 
 

@@ -53,7 +53,8 @@ constexpr int kPlaneMaxStages = 8;
 // timing experiments only (tools/build_variant.sh): 1 = no x-window copies,
 // 2 = no operand copies, 4 = row threads skip the arithmetic and stores,
 // 8 = no stores (a never-true test keeps the arithmetic), 16 = every warp
-// takes the interior path (wrong results at boundary rows)
+// takes the interior path (wrong results at boundary rows), 32 = no zeroing
+// of absent in-plane entries on interior planes (wrong at boundary rows)
 #ifndef PG_PLANE_EXP
 #define PG_PLANE_EXP 0
 #endif
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
                          : (1u | (qb_t[h] << NO) | (1u << (NO + NM)));
       zero_t = zero_t || qb_t[h] != kMid;
     }
-    zero_t = __any_sync(0xffffffffu, zero_t);
+    zero_t = __any_sync(0xffffffffu, zero_t) && !(PG_PLANE_EXP & 32);
     // planes za - 1, za: warm-up; za + 1 .. zb - 2: steady; zb - 1, zb: drain
     const int pa0 = (int)za, pb0 = (int)zb;
     for (int p = pa0 - 1; p <= pb0; ++p) {

@@ -212,11 +212,14 @@ class Shard:
 
     def pass_bytes(self, vec_bytes: int) -> int:
         """Algorithmic bytes of one SpMV pass over the stored format: the
-        matrix stream (1 B per row for the row-pattern format, 8 B per entry
+        matrix stream (1 B per row for the row-pattern format -- none for the
+        plane-ring kernel, whose interior planes read no pattern ids -- 8 B per entry
         + 1 B per row for the offset-pattern format; else the
         stored entry bytes + a 4-byte row length), the compulsory gather of x
         (8 B per row) and ``vec_bytes`` per row of epilogue vectors."""
-        if self.stats["kernel"] in (5, 6, 8, 9):  # row patterns (gather, windowed, marching, plane ring)
+        if self.stats["kernel"] == 9:  # plane ring: interior planes read no pattern ids
+            return (8 + vec_bytes) * self.n
+        if self.stats["kernel"] in (5, 6, 8):  # row patterns (gather, windowed, marching)
             return (1 + 8 + vec_bytes) * self.n
         if self.stats["kernel"] == 7:  # offset patterns: f64 values + 1 B per row
             return 8 * self.nnz + (1 + 8 + vec_bytes) * self.n

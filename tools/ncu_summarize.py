@@ -86,7 +86,8 @@ def full(rep, out, traffic_json=None, workload=None):
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     if traffic_json:
-        poly = [r["_dram_bytes"] for r in recs if "sell" in r["kernel"] and "_dram_bytes" in r]
+        poly = [r["_dram_bytes"] for r in recs
+                if ("sell" in r["kernel"] or "plane_ring" in r["kernel"]) and "_dram_bytes" in r]
         data = {}
         try:
             data = json.load(open(traffic_json))
