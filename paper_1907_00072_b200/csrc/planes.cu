@@ -30,6 +30,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "pipeline.cuh"
@@ -55,6 +56,11 @@ constexpr int kPlaneMaxStages = 8;
 // 8 = no stores (a never-true test keeps the arithmetic), 16 = every warp
 // takes the interior path (wrong results at boundary rows), 32 = no zeroing
 // of absent in-plane entries on interior planes (wrong at boundary rows)
+// unroll of the interior-plane loop (3 = the rows' role rotation period)
+#ifndef PG_PLANE_UNROLL
+#define PG_PLANE_UNROLL 1
+#endif
+constexpr int kPlaneUnroll = PG_PLANE_UNROLL;
 #ifndef PG_PLANE_EXP
 #define PG_PLANE_EXP 0
 #endif
@@ -321,7 +327,8 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     // box row with in-plane entries bq_m (closing, continuing and opening
     // rows alike); zero: some lane's rows miss in-plane entries
     auto body = [&](int p, const uint32_t (&mk_s)[kPlaneRPT], const uint32_t (&bq_s)[kPlaneRPT],
-                    bool zero) {
+                    auto zero_c) {
+      constexpr bool zero = decltype(zero_c)::value;
       const double* win = reinterpret_cast<const double*>(buf);
       const int64_t rb = (int64_t)(p - 1) * S + q0;
       double acc_s[kPlaneRPT];
@@ -334,7 +341,7 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
         for (int u = 0; u < 2; ++u)
 #pragma unroll
           for (int i = 0; i < NM; ++i) P[u][i] = win[jj[h0 + u] + win_off<KIND>(i, pa)];
-        if (zero) {
+        if constexpr (zero) {
 #pragma unroll
           for (int u = 0; u < 2; ++u)
 #pragma unroll
@@ -385,7 +392,10 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
         general(p, true, true, true, mk_s);
         return;
       }
-      body(p, mk_s, bq_s, __any_sync(0xffffffffu, partial));
+      if (__any_sync(0xffffffffu, partial))
+        body(p, mk_s, bq_s, std::true_type{});
+      else
+        body(p, mk_s, bq_s, std::false_type{});
     };
     // Interior planes of a host-verified matrix (plane_qm): the rows at
     // in-plane index q are box rows with entries plane_qm[q] on every
@@ -400,21 +410,50 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
       zero_t = zero_t || qb_t[h] != kMid;
     }
     zero_t = __any_sync(0xffffffffu, zero_t) && !(PG_PLANE_EXP & 32);
-    // planes za - 1, za: warm-up; za + 1 .. zb - 2: steady; zb - 1, zb: drain
+    // planes za - 1, za: warm-up; za + 1 .. zb - 2: steady; zb - 1, zb: drain.
+    // The steady planes whose three rows are all on interior planes of a
+    // host-verified matrix, [bl, bh], run as a counted loop of the unrolled
+    // body (no pattern ids, no per-stage dispatch).
     const int pa0 = (int)za, pb0 = (int)zb;
-    for (int p = pa0 - 1; p <= pb0; ++p) {
-      mbar_wait(&full[st], phase);
+    auto stage = [&](int p) {
       if (p >= pa0 + 1 && p <= pb0 - 2) {
-        if (plane_qm && p >= 2 && p + 3 <= (int)pa.nz && !(PG_PLANE_EXP & 4))
-          body(p, mb_t, qb_t, zero_t);
-        else
-          steady(p);
+        steady(p);
       } else {
         const bool start = p + 1 < pb0;
         uint32_t mk_s[kPlaneRPT];
         open_masks(mk_s, start);
         general(p, p - 1 >= pa0, p >= pa0 && p < pb0, start, mk_s);
       }
+    };
+    int bl = max(pa0 + 1, 2), bh = min(pb0 - 2, (int)pa.nz - 3);
+    if (!plane_qm || (PG_PLANE_EXP & 4) || bh < bl) {
+      bl = pb0 + 1;
+      bh = pb0;
+    }
+    int p = pa0 - 1;
+    for (; p < bl; ++p) {
+      mbar_wait(&full[st], phase);
+      stage(p);
+      next_slot();
+    }
+    if (zero_t) {
+#pragma unroll kPlaneUnroll
+      for (; p <= bh; ++p) {
+        mbar_wait(&full[st], phase);
+        body(p, mb_t, qb_t, std::true_type{});
+        next_slot();
+      }
+    } else {
+#pragma unroll kPlaneUnroll
+      for (; p <= bh; ++p) {
+        mbar_wait(&full[st], phase);
+        body(p, mb_t, qb_t, std::false_type{});
+        next_slot();
+      }
+    }
+    for (; p <= pb0; ++p) {
+      mbar_wait(&full[st], phase);
+      stage(p);
       next_slot();
     }
   }
