@@ -96,6 +96,22 @@ __device__ __forceinline__ double plane_epilogue(const Epi& e, const Pre& p, int
   return 0.0;
 }
 
+// The same positions as runs: NR runs of consecutive window values, value i
+// at run run_of(i), position run_pos(i); run r starts at pa.woff[run_base(r)]
+template <int KIND>
+struct WinRuns {
+  static constexpr int NR = (KIND == 27 || KIND == 7) ? 3 : 1;
+  __device__ static constexpr int run_of(int i) {
+    return KIND == 27 ? i / 3 : KIND == 7 ? (i == 0 ? 0 : i == 4 ? 2 : 1) : 0;
+  }
+  __device__ static constexpr int run_pos(int i) {
+    return KIND == 27 ? i % 3 : KIND == 7 ? (i == 0 || i == 4 ? 0 : i - 1) : i;
+  }
+  __device__ static constexpr int run_base(int r) {
+    return KIND == 27 ? 3 * r : KIND == 7 ? (r == 0 ? 0 : r == 1 ? 1 : 4) : 0;
+  }
+};
+
 template <int MODE, int KIND, int EF>
 __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     plane_ring_kernel(PlaneArgs pa, const uint8_t* __restrict__ rpat,
@@ -326,11 +342,19 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     // the unrolled interior body: every row of the warp at this stage is a
     // box row with in-plane entries bq_m (closing, continuing and opening
     // rows alike); zero: some lane's rows miss in-plane entries
-    auto body = [&](int p, const uint32_t (&mk_s)[kPlaneRPT], const uint32_t (&bq_s)[kPlaneRPT],
-                    auto zero_c) {
+    // byte offsets of this thread's window runs inside a ring stage
+    using Runs = WinRuns<KIND>;
+    uint32_t wrun[kPlaneRPT][Runs::NR];
+#pragma unroll
+    for (int h = 0; h < kPlaneRPT; ++h)
+#pragma unroll
+      for (int r = 0; r < Runs::NR; ++r) wrun[h][r] = 8u * (uint32_t)(jj[h] + pa.woff[Runs::run_base(r)]);
+    // ri: the (32-bit) row of in-plane index 0 of the tile on the closing
+    // plane p - 1; ROT: also rotate the rows' masks (the interior-plane loop
+    // keeps them fixed and sets them once after the loop)
+    auto body = [&](int ri, const uint32_t (&mk_s)[kPlaneRPT], const uint32_t (&bq_s)[kPlaneRPT],
+                    auto zero_c, auto rot_c) {
       constexpr bool zero = decltype(zero_c)::value;
-      const double* win = reinterpret_cast<const double*>(buf);
-      const int64_t rb = (int64_t)(p - 1) * S + q0;
       double acc_s[kPlaneRPT];
       // pairs of in-plane indices: six independent chains each (close /
       // continue / open x 2), every chain in its row's stored order
@@ -340,13 +364,15 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int i = 0; i < NM; ++i) P[u][i] = win[jj[h0 + u] + win_off<KIND>(i, pa)];
+          for (int i = 0; i < NM; ++i)
+            P[u][i] = reinterpret_cast<const double*>(buf + wrun[h0 + u][Runs::run_of(i)])
+                [Runs::run_pos(i)];
         if constexpr (zero) {
 #pragma unroll
           for (int u = 0; u < 2; ++u)
 #pragma unroll
             for (int i = 0; i < NM; ++i)
-              if (!((bq_m[h0 + u] >> i) & 1u)) P[u][i] = 0.0;
+              if (!((bq_s[h0 + u] >> i) & 1u)) P[u][i] = 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) acc_s[h0 + u] = 0.0;
@@ -365,9 +391,17 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u)
-          if (act[h0 + u]) finish(h0 + u, rb + jj[h0 + u], acc_f[h0 + u]);
+          if (act[h0 + u]) finish(h0 + u, (int64_t)(ri + jj[h0 + u]), acc_f[h0 + u]);
       }
-      rotate(acc_s, mk_s, bq_s);
+      if constexpr (decltype(rot_c)::value) {
+        rotate(acc_s, mk_s, bq_s);
+      } else {
+#pragma unroll
+        for (int h = 0; h < kPlaneRPT; ++h) {
+          acc_f[h] = acc_m[h];
+          acc_m[h] = acc_s[h];
+        }
+      }
     };
     // Steady stage (rows close, continue and open): the unrolled body when,
     // for every row of the warp, the closing, continuing and opening rows at
@@ -392,10 +426,11 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
         general(p, true, true, true, mk_s);
         return;
       }
+      const int ri = (p - 1) * (int)S + (int)q0;
       if (__any_sync(0xffffffffu, partial))
-        body(p, mk_s, bq_s, std::true_type{});
+        body(ri, mk_s, bq_s, std::true_type{}, std::true_type{});
       else
-        body(p, mk_s, bq_s, std::false_type{});
+        body(ri, mk_s, bq_s, std::false_type{}, std::true_type{});
     };
     // Interior planes of a host-verified matrix (plane_qm): the rows at
     // in-plane index q are box rows with entries plane_qm[q] on every
@@ -436,19 +471,32 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
       stage(p);
       next_slot();
     }
-    if (zero_t) {
+    if (p <= bh) {
+      int ri = (p - 1) * (int)S + (int)q0;
+      if (zero_t) {
 #pragma unroll kPlaneUnroll
-      for (; p <= bh; ++p) {
-        mbar_wait(&full[st], phase);
-        body(p, mb_t, qb_t, std::true_type{});
-        next_slot();
+        for (; p <= bh; ++p, ri += (int)S) {
+          mbar_wait(&full[st], phase);
+          body(ri, mb_t, qb_t, std::true_type{}, std::false_type{});
+          next_slot();
+        }
+      } else {
+#pragma unroll kPlaneUnroll
+        for (; p <= bh; ++p, ri += (int)S) {
+          mbar_wait(&full[st], phase);
+          body(ri, mb_t, qb_t, std::false_type{}, std::false_type{});
+          next_slot();
+        }
       }
-    } else {
-#pragma unroll kPlaneUnroll
-      for (; p <= bh; ++p) {
-        mbar_wait(&full[st], phase);
-        body(p, mb_t, qb_t, std::false_type{});
-        next_slot();
+      // the interior loop left the masks in place: the rows now closing and
+      // continuing were opened inside it (at least one plane each)
+      const int nb = bh - bl + 1;
+#pragma unroll
+      for (int h = 0; h < kPlaneRPT; ++h) {
+        mk_f[h] = nb >= 2 ? mb_t[h] : mk_m[h];
+        bq_f[h] = nb >= 2 ? qb_t[h] : bq_m[h];
+        mk_m[h] = mb_t[h];
+        bq_m[h] = qb_t[h];
       }
     }
     for (; p <= pb0; ++p) {
@@ -495,6 +543,8 @@ void plane_prepare(pg_matrix* m) {
   if (on == 1 && kind != 27) return;
   // 16-byte aligned pattern-id / operand slices and whole planes
   if (S % 16 != 0 || m->nrows % S != 0 || m->n_pat > 256) return;
+  // 32-bit row indices inside the kernel
+  if (m->nrows + 4 * S >= ((int64_t)1 << 31)) return;
   // zeroed window values stand for absent entries (v * 0.0 = +-0.0): finite
   // master values only
   for (int i = 0; i < m->pat_mlen; ++i)
