@@ -40,8 +40,9 @@ int grid_for(int device, const void* kernel, int block, size_t smem, int64_t wor
   PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem));
   if (per_sm < 1) per_sm = 1;
+  // whole waves only: at most kMaxBlocks (the reductions' partial slots)
+  if (per_sm > kMaxBlocks / sms) per_sm = kMaxBlocks / sms > 0 ? kMaxBlocks / sms : 1;
   int64_t g = (int64_t)sms * per_sm;
-  if (g > kMaxBlocks) g = kMaxBlocks;
   if (work_blocks < g) g = work_blocks;
   if (g < 1) g = 1;
   return (int)g;

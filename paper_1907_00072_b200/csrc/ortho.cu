@@ -271,6 +271,10 @@ __global__ void __launch_bounds__(kTileThreads)
 }
 
 constexpr int kRowThreads = 256;
+// phase 3 row loop with the next column group's loads in flight (A/B: 0)
+#ifndef PG_ROWS_PIPE
+#define PG_ROWS_PIPE 0
+#endif
 
 template <bool PHASE3>
 __global__ void __launch_bounds__(kRowThreads)
@@ -291,6 +295,33 @@ __global__ void __launch_bounds__(kRowThreads)
     if (PHASE3) {
       double t1 = 0.0, t2 = 0.0;
       int i = 0;
+#if PG_ROWS_PIPE
+      // software-pipelined: the next 8 columns' loads are issued before this
+      // group's FMAs (same sequential order per row)
+      if (k >= 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(vr + (int64_t)u * ld);
+        for (; i + 16 <= k; i += 8) {
+          double vn[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) vn[u] = __ldcs(vr + (int64_t)(i + 8 + u) * ld);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            t1 = __fma_rn(v[u], cs1[i + u], t1);
+            t2 = __fma_rn(v[u], cs2[i + u], t2);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = vn[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          t1 = __fma_rn(v[u], cs1[i + u], t1);
+          t2 = __fma_rn(v[u], cs2[i + u], t2);
+        }
+        i += 8;
+      }
+#else
       for (; i + 8 <= k; i += 8) {
         double v[8];
 #pragma unroll
@@ -301,6 +332,7 @@ __global__ void __launch_bounds__(kRowThreads)
           t2 = __fma_rn(v[u], cs2[i + u], t2);
         }
       }
+#endif
       for (; i < k; ++i) {
         const double v = __ldcs(vr + (int64_t)i * ld);
         t1 = __fma_rn(v, cs1[i], t1);
@@ -767,12 +799,33 @@ static void launch_tile(const double* V, int64_t ld, int k, const double* z, int
   check_launch();
 }
 
-static int simple_grid(int64_t n, int threads, pg_workspace* ws) {
-  int sms = ws ? ws->num_sms : 148;
-  int64_t need = (n + threads - 1) / threads;
-  int64_t cap = (int64_t)sms * (2048 / threads);
-  if (cap > kMaxBlocks) cap = kMaxBlocks;
-  int64_t g = need < cap ? need : cap;
+// Grid of a grid-stride streaming kernel: whole waves of the blocks an SM
+// keeps resident (occupancy of this kernel), at most kMaxBlocks (the
+// reductions' partial slots) -- a partial second wave ran phase 3 of CGS2 at
+// 1.38 waves (1024 blocks, 740 resident) -- or fewer when n is small.
+static int simple_grid(int64_t n, int threads, const void* kernel) {
+  static int sms = 0;
+  if (!sms) PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device()));
+  static const void* kern[16] = {};
+  static int occ[16] = {};
+  int per_sm = 0;
+  for (int i = 0; i < 16; ++i) {
+    if (kern[i] == kernel) {
+      per_sm = occ[i];
+      break;
+    }
+    if (!kern[i]) {
+      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0));
+      kern[i] = kernel;
+      occ[i] = per_sm;
+      break;
+    }
+  }
+  if (per_sm < 1) per_sm = 1;
+  const int cap_sm = kMaxBlocks / sms > 0 ? kMaxBlocks / sms : 1;
+  int64_t g = (int64_t)sms * (per_sm < cap_sm ? per_sm : cap_sm);
+  const int64_t need = (n + threads - 1) / threads;
+  if (need < g) g = need;
   return (int)(g < 1 ? 1 : g);
 }
 
@@ -840,7 +893,7 @@ void cgs2_wide(const double* V, int64_t ld, int k, const double* z, int64_t n, d
 
 void normalize_publish(const double* x, const double* nsq, int64_t n, double* out,
                        const double* ring, int count, double* host, cudaStream_t st) {
-  const int g = n > 0 ? simple_grid(n, 256, nullptr) : 1;
+  const int g = n > 0 ? simple_grid(n, 256, (const void*)normalize_publish_kernel) : 1;
   launch_k(normalize_publish_kernel, g, 256, 0, st, x, nsq, n, out, ring, count, host);
   check_launch();
 }
@@ -886,7 +939,7 @@ PG_API int pg_cgs2_phase3(const double* d_V, int64_t ld, int k, const double* d_
       return;
     }
     if (use_tile_cgs2(k)) {
-      const int g = simple_grid(n, kRowThreads, ws);
+      const int g = simple_grid(n, kRowThreads, (const void*)rows_kernel<true>);
       launch_k(rows_kernel<true>, g, kRowThreads, 0, st, d_V, ld, k, d_z, n, d_c1, d_c2, d_w2,
                                                     ws->partials, ws->counter, d_nsq);
     } else {
@@ -903,7 +956,7 @@ PG_API int pg_normalize(const double* d_x, const double* d_nsq, int64_t n, doubl
   return guard([&] {
     PG_REQUIRE(d_x && d_nsq && d_out, PG_ERR_PARAMETER, "null argument");
     if (n == 0) return;
-    const int g = simple_grid(n, 256, nullptr);
+    const int g = simple_grid(n, 256, (const void*)normalize_kernel);
     launch_k(normalize_kernel, g, 256, 0, as_stream(stream), d_x, d_nsq, n, d_out);
     check_launch();
   });
@@ -924,7 +977,7 @@ PG_API int pg_gemv(const double* d_V, int64_t ld, int k, const double* d_y, int6
     check_tall(d_V, ld, k, n, 0);
     PG_REQUIRE(d_out && (k == 0 || d_y), PG_ERR_PARAMETER, "null argument");
     if (n == 0) return;
-    const int g = simple_grid(n, kRowThreads, nullptr);
+    const int g = simple_grid(n, kRowThreads, (const void*)rows_kernel<false>);
     launch_k(rows_kernel<false>, g, kRowThreads, 0, as_stream(stream), d_V, ld, k, nullptr, n, d_y, nullptr, d_out, nullptr, nullptr, nullptr);
     check_launch();
   });
@@ -936,7 +989,7 @@ PG_API int pg_gemv_acc(const double* d_V, int64_t ld, int k, const double* d_y, 
     check_tall(d_V, ld, k, n, 0);
     PG_REQUIRE(d_out && (k == 0 || d_y), PG_ERR_PARAMETER, "null argument");
     if (n == 0) return;
-    const int g = simple_grid(n, kRowThreads, nullptr);
+    const int g = simple_grid(n, kRowThreads, (const void*)gemv_acc_kernel);
     launch_k(gemv_acc_kernel, g, kRowThreads, 0, as_stream(stream), d_V, ld, k, d_y, n, d_base,
              sgn, d_out);
     check_launch();
@@ -965,7 +1018,7 @@ PG_API int pg_dot(const double* d_x, const double* d_y, int64_t n, double* d_out
       PG_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double), st));
       return;
     }
-    const int g = simple_grid(n, 256, ws);
+    const int g = simple_grid(n, 256, (const void*)dot_kernel);
     launch_k(dot_kernel, g, 256, 0, st, d_x, d_y, n, ws->partials, ws->counter, d_out);
     check_launch();
   });
@@ -976,7 +1029,7 @@ PG_API int pg_scale_add(const double* d_base, double a, const double* d_v, int64
   return guard([&] {
     PG_REQUIRE(d_v && d_out, PG_ERR_PARAMETER, "null argument");
     if (n == 0) return;
-    const int g = simple_grid(n, 256, nullptr);
+    const int g = simple_grid(n, 256, (const void*)scale_add_kernel);
     launch_k(scale_add_kernel, g, 256, 0, as_stream(stream), d_base, a, d_v, n, d_out);
     check_launch();
   });
@@ -987,7 +1040,7 @@ PG_API int pg_gather(const double* d_x, const int32_t* d_idx, int64_t m, double*
   return guard([&] {
     if (m == 0) return;
     PG_REQUIRE(d_x && d_idx && d_out, PG_ERR_PARAMETER, "null argument");
-    const int g = simple_grid(m, 256, nullptr);
+    const int g = simple_grid(m, 256, (const void*)gather_kernel);
     launch_k(gather_kernel, g, 256, 0, as_stream(stream), d_x, d_idx, m, d_out);
     check_launch();
   });
