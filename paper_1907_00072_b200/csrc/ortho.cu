@@ -15,6 +15,9 @@
 // 16-byte cp.async copies, double buffered, so the next tile's HBM reads are
 // in flight while the current tile is reduced.
 
+#include <cuda.h>
+
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.cuh"
@@ -268,6 +271,117 @@ __global__ void __launch_bounds__(kTileThreads)
     }
     last_block_reduce(partials, counter, k, out);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Phases 1 and 2 with the tiles loaded by the tensor-memory accelerator: V as
+// a 2-D tensor map (rows x columns, column stride ld), one
+// cp.async.bulk.tensor.2d per 8 columns of a TR-row tile plus one 1-D tensor
+// copy of z's segment, issued by one thread and completing on the slot's
+// mbarrier; rows past n (and columns past k in the last 8-column box) arrive
+// zero-filled.  The per-lane 16-byte cp.async staging of tile_kernel costs
+// ~11 copy instructions per thread per tile; here the other threads only
+// compute.  Same arithmetic and order as tile_kernel (kDots, kUpdDots).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kTmaBoxCols = 8;
+
+template <int MODE, int STAGES, int TR>
+__global__ void __launch_bounds__(kTileThreads)
+    tma_tile_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmZ,
+                    int k, int64_t n, const double* __restrict__ c1, double* partials,
+                    unsigned int* counter, double* out) {
+  static_assert(MODE == kDots || MODE == kUpdDots, "dots phases only");
+  pdl_entry();
+  extern __shared__ __align__(128) double smem[];
+  __shared__ double c1s[PG_KMAX];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  const int nbox = (k + kTmaBoxCols - 1) / kTmaBoxCols;
+  const int zcol = nbox * kTmaBoxCols;  // z's column slot
+  const int buf_elems = (zcol + 1) * TR;
+  double* w1s = smem + STAGES * buf_elems;  // kUpdDots only
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t tile_bytes = 8u * (uint32_t)((zcol + 1) * TR);
+  if (MODE == kUpdDots)
+    for (int i = threadIdx.x; i < k; i += kTileThreads) c1s[i] = c1[i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t ntiles = (n + TR - 1) / TR;
+  auto issue = [&](int64_t t, int slot) {
+    double* buf = smem + (size_t)slot * buf_elems;
+    mbar_expect_tx(&full[slot], tile_bytes);
+    const int r0 = (int)(t * TR);
+    for (int b = 0; b < nbox; ++b)
+      tma_load_2d(buf + (size_t)b * kTmaBoxCols * TR, &tmV, r0, b * kTmaBoxCols, &full[slot]);
+    tma_load_2d(buf + (size_t)zcol * TR, &tmZ, r0, 0, &full[slot]);
+  };
+  int64_t tile = blockIdx.x;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      const int64_t t = tile + (int64_t)s * gridDim.x;
+      if (t < ntiles) issue(t, s);
+    }
+  }
+  double acc[kColsPerWarp];
+#pragma unroll
+  for (int m = 0; m < kColsPerWarp; ++m) acc[m] = 0.0;
+  int it = 0;
+  for (; tile < ntiles; tile += gridDim.x, ++it) {
+    // every thread is done with tile it-1: refill its slot
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int64_t t = tile + (int64_t)(STAGES - 1) * gridDim.x;
+      if (t < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(t, (it + STAGES - 1) % STAGES);
+      }
+    }
+    const int slot = it % STAGES;
+    mbar_wait(&full[slot], (uint32_t)((it / STAGES) & 1));
+    const double* S = smem + (size_t)slot * buf_elems;
+    const double* vec = S + (size_t)zcol * TR;
+    if (MODE == kUpdDots) {
+      if (threadIdx.x < TR) {
+        const int r = threadIdx.x;
+        const double t = row_proj(k, c1s, [&](int i) { return S[i * TR + r]; });
+        w1s[r] = __dsub_rn(vec[r], t);
+      }
+      __syncthreads();
+      vec = w1s;
+    }
+#pragma unroll
+    for (int m = 0; m < kColsPerWarp; ++m) {
+      const int i = warp + m * kWarps;
+      if (i < k) {
+        const double* col = S + i * TR;
+#pragma unroll
+        for (int q = 0; q < TR / 32; ++q)
+          acc[m] = __fma_rn(col[lane + 32 * q], vec[lane + 32 * q], acc[m]);
+      }
+    }
+    if (MODE == kUpdDots) __syncthreads();  // w1s is rewritten by the next tile
+  }
+#pragma unroll
+  for (int m = 0; m < kColsPerWarp; ++m) {
+    double v = acc[m];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int i = warp + m * kWarps;
+    if (lane == 0 && i < k) partials[(size_t)blockIdx.x * k + i] = v;
+  }
+  last_block_reduce(partials, counter, k, out);
 }
 
 constexpr int kRowThreads = 256;
@@ -799,6 +913,133 @@ static void launch_tile(const double* V, int64_t ld, int k, const double* z, int
   check_launch();
 }
 
+// ------------------------------------------------------- TMA tile launch --
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    const cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (e == cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    else if (std::getenv("PG_TMA_DEBUG"))
+      std::fprintf(stderr, "pgmres: cuTensorMapEncodeTiled entry point: err %d query %d\n", (int)e, (int)q);
+  }
+  return fn;
+}
+
+// Phases 1-2 through tma_tile_kernel (PG_CGS2_TMA=0: the cp.async tile
+// kernel).  Same tile height and ring depth policy as launch_tile.
+template <int MODE>
+static bool launch_tma(const double* V, int64_t ld, int k, const double* z, int64_t n,
+                       const double* c1, double* out, pg_workspace* ws, cudaStream_t st) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("PG_CGS2_TMA");
+    on = e ? std::atoi(e) : 1;
+  }
+  if (!on || n <= 0 || n > 0x7fffffffLL || k < 1) return false;
+  if (ld % 2 != 0 || ((uintptr_t)V & 15) != 0 || ((uintptr_t)z & 15) != 0) return false;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  // tile height and ring depth with TMA staging (tools/cgs2_bench.py sweep on
+  // B200, profiles/r02/cgs2_tma_sweep.md): phase 1 takes 256-row tiles
+  // everywhere (n = 8M, k = 45: 414 vs 442 us); phase 2 256-row tiles up to
+  // k = 20 and, at n <= 2M, beyond k = 32, else 128-row tiles with a ring
+  // sized for 3 CTAs per SM (n = 8M, k = 45: 427 vs 439 us)
+  const bool small = n <= (int64_t)2000000;
+  int tr = 256, ctas = 0;
+  if (MODE == kUpdDots && !(k <= 20 || (small && k > 32))) {
+    tr = 128;
+    ctas = 3;
+  }
+  static int force_tr = -1;
+  if (force_tr < 0) {
+    const char* e = std::getenv("PG_TILE_ROWS");
+    force_tr = e ? std::atoi(e) : 0;
+  }
+  if (force_tr == 128 || force_tr == 256) tr = force_tr;
+  int stages;
+  if (ctas > 0 && !std::getenv(MODE == kDots ? "PG_TILE_CTAS_P1" : "PG_TILE_CTAS_P2")) {
+    stages = 2;
+    for (int s = 4; s > 2; --s)
+      if (tile_smem(MODE, k, s, tr) <= kTileSmemMax / ctas) {
+        stages = s;
+        break;
+      }
+  } else {
+    stages = tile_stages(MODE, k, n, tr);
+  }
+  const int nbox = (k + kTmaBoxCols - 1) / kTmaBoxCols;
+  const size_t smem = sizeof(double) * ((size_t)stages * (nbox * kTmaBoxCols + 1) * tr +
+                                        (MODE == kUpdDots ? (size_t)tr : 0));
+  if (smem > kTileSmemMax) return false;
+  CUtensorMap tmV, tmZ;
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)k};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)tr, (cuuint32_t)kTmaBoxCols};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(&tmV, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)V, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      if (std::getenv("PG_TMA_DEBUG")) std::fprintf(stderr, "pgmres: V tensor map rejected\n");
+      return false;
+    }
+  }
+  {
+    // z as an n x 1 matrix (a rank-1 map was rejected by the driver here)
+    const cuuint64_t dims[2] = {(cuuint64_t)n, 1};
+    const cuuint64_t strides[1] = {(cuuint64_t)((n + 1) & ~(int64_t)1) * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)tr, 1};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(&tmZ, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)z, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      if (std::getenv("PG_TMA_DEBUG")) std::fprintf(stderr, "pgmres: z tensor map rejected\n");
+      return false;
+    }
+  }
+  const int dev = ws->device;
+  const void* kern =
+      tr == 256 ? (stages == 4   ? (const void*)tma_tile_kernel<MODE, 4, 256>
+                   : stages == 3 ? (const void*)tma_tile_kernel<MODE, 3, 256>
+                                 : (const void*)tma_tile_kernel<MODE, 2, 256>)
+                : (stages == 4   ? (const void*)tma_tile_kernel<MODE, 4, 128>
+                   : stages == 3 ? (const void*)tma_tile_kernel<MODE, 3, 128>
+                                 : (const void*)tma_tile_kernel<MODE, 2, 128>);
+  static bool attr[2][2][5][64] = {};
+  if (!attr[MODE - 1][tr == 256][stages][dev]) {
+    PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kTileSmemMax));
+    attr[MODE - 1][tr == 256][stages][dev] = true;
+  }
+  const int64_t ntiles = (n + tr - 1) / tr;
+  const int g = grid_for(dev, kern, kTileThreads, smem, ntiles);
+#define PG_TMA_LAUNCH(S, R)                                                                 \
+  launch_k(tma_tile_kernel<MODE, S, R>, g, kTileThreads, smem, st, tmV, tmZ, k, n, c1,      \
+           ws->partials, ws->counter, out)
+  if (tr == 256) {
+    if (stages == 4) PG_TMA_LAUNCH(4, 256);
+    else if (stages == 3) PG_TMA_LAUNCH(3, 256);
+    else PG_TMA_LAUNCH(2, 256);
+  } else {
+    if (stages == 4) PG_TMA_LAUNCH(4, 128);
+    else if (stages == 3) PG_TMA_LAUNCH(3, 128);
+    else PG_TMA_LAUNCH(2, 128);
+  }
+#undef PG_TMA_LAUNCH
+  check_launch();
+  return true;
+}
+
 // Grid of a grid-stride streaming kernel: whole waves of the blocks an SM
 // keeps resident (occupancy of this kernel), at most kMaxBlocks (the
 // reductions' partial slots) -- a partial second wave ran phase 3 of CGS2 at
@@ -908,7 +1149,7 @@ PG_API int pg_cgs2_phase1(const double* d_V, int64_t ld, int k, const double* d_
     PG_REQUIRE(d_z && d_c1, PG_ERR_PARAMETER, "null argument");
     if (!use_tile_cgs2(k, 1))
       launch_chunk_dots<1>(d_V, ld, k, d_z, n, nullptr, d_c1, ws, as_stream(stream));
-    else
+    else if (!launch_tma<kDots>(d_V, ld, k, d_z, n, nullptr, d_c1, ws, as_stream(stream)))
       launch_tile<kDots>(d_V, ld, k, d_z, n, nullptr, d_c1, ws, as_stream(stream));
   });
 }
@@ -920,7 +1161,7 @@ PG_API int pg_cgs2_phase2(const double* d_V, int64_t ld, int k, const double* d_
     PG_REQUIRE(d_z && d_c1 && d_c2, PG_ERR_PARAMETER, "null argument");
     if (!use_tile_cgs2(k, 2))
       launch_chunk_dots<2>(d_V, ld, k, d_z, n, d_c1, d_c2, ws, as_stream(stream));
-    else
+    else if (!launch_tma<kUpdDots>(d_V, ld, k, d_z, n, d_c1, d_c2, ws, as_stream(stream)))
       launch_tile<kUpdDots>(d_V, ld, k, d_z, n, d_c1, d_c2, ws, as_stream(stream));
   });
 }
