@@ -22,6 +22,7 @@ kernel.  PyTorch provides device memory, streams and the collectives.
 from __future__ import annotations
 
 import os
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -456,6 +457,82 @@ class _StepGraph:
             self.h = None
 
 
+
+class HostStage:
+    """Two pinned staging buffers per device for numpy (pageable) vectors --
+    the reference's call signature.  A large vector moves in chunks: the host
+    copy of chunk i+1 into one pinned buffer overlaps the DMA of chunk i from
+    the other (torch's pageable copy staged the whole vector synchronously,
+    ~40 ms of the cfg4 e2e for b, v0 and x).  Chunks are ordered on the
+    caller's stream; a buffer is refilled only after its previous DMA's event."""
+
+    CHUNK = 1 << 20  # doubles (8 MB)
+    MIN = 1 << 19    # smaller vectors take the plain copy
+
+    _per_device: dict = {}
+
+    def __init__(self):
+        self.buf = [torch.empty(self.CHUNK, dtype=F64).pin_memory() for _ in range(2)]
+        self.ev = [None, None]
+        self.lock = threading.Lock()
+
+    @classmethod
+    def get(cls, device) -> "HostStage":
+        key = torch.device(device).index
+        st = cls._per_device.get(key)
+        if st is None:
+            st = cls._per_device[key] = HostStage()
+        return st
+
+    def _wait(self, i):
+        if self.ev[i] is not None:
+            self.ev[i].synchronize()
+            self.ev[i] = None
+
+    def h2d(self, src: np.ndarray, dst: torch.Tensor):
+        """dst[:len(src)] <- src (numpy, contiguous f64)."""
+        with self.lock, torch.cuda.device(dst.device):
+            self._h2d(src, dst)
+
+    def d2h(self, src: torch.Tensor, out: np.ndarray):
+        """out <- src[:len(out)] (device)."""
+        with self.lock, torch.cuda.device(src.device):
+            self._d2h(src, out)
+
+    def _h2d(self, src, dst):
+        n = src.shape[0]
+        stream = torch.cuda.current_stream(dst.device)
+        for c, a in enumerate(range(0, n, self.CHUNK)):
+            i = c & 1
+            m = min(self.CHUNK, n - a)
+            self._wait(i)
+            self.buf[i][:m].copy_(torch.from_numpy(src[a:a + m]))
+            dst[a:a + m].copy_(self.buf[i][:m], non_blocking=True)
+            self.ev[i] = torch.cuda.Event()
+            self.ev[i].record(stream)
+        for i in range(2):
+            self._wait(i)
+
+    def _d2h(self, src, out):
+        n = out.shape[0]
+        stream = torch.cuda.current_stream(src.device)
+        pend = []
+        for c, a in enumerate(range(0, n, self.CHUNK)):
+            i = c & 1
+            m = min(self.CHUNK, n - a)
+            if len(pend) == 2:  # drain the chunk that used this buffer
+                ja, jm, ji = pend.pop(0)
+                self._wait(ji)
+                out[ja:ja + jm] = self.buf[ji][:jm].numpy()
+            self.buf[i][:m].copy_(src[a:a + m], non_blocking=True)
+            self.ev[i] = torch.cuda.Event()
+            self.ev[i].record(stream)
+            pend.append((a, m, i))
+        for ja, jm, ji in pend:
+            self._wait(ji)
+            out[ja:ja + jm] = self.buf[ji][:jm].numpy()
+
+
 class Engine:
     def __init__(self, shards, comm, n_global: int):
         self.shards = shards
@@ -728,7 +805,11 @@ class Engine:
         else:
             raise DimensionMismatchError("vector length does not match operator")
         for s, t, part in zip(self.shards, out, parts):
-            src = torch.from_numpy(np.ascontiguousarray(part))
+            part = np.ascontiguousarray(part)
+            if not pinned and part.shape[0] >= HostStage.MIN and t.is_cuda:
+                HostStage.get(t.device).h2d(part, t)
+                continue
+            src = torch.from_numpy(part)
             if pinned:
                 src = src.pin_memory()
             t[:s.n].copy_(src, non_blocking=pinned)
@@ -755,7 +836,16 @@ class Engine:
         return out
 
     def to_host(self, xs) -> np.ndarray:
-        return np.concatenate([t[:s.n].cpu().numpy() for s, t in zip(self.shards, xs)])
+        out = np.empty(self.local_n if self.comm.distributed else
+                       sum(s.n for s in self.shards), dtype=np.float64)
+        a = 0
+        for s, t in zip(self.shards, xs):
+            if s.n >= HostStage.MIN and t.is_cuda:
+                HostStage.get(t.device).d2h(t[:s.n], out[a:a + s.n])
+            else:
+                out[a:a + s.n] = t[:s.n].cpu().numpy()
+            a += s.n
+        return out
 
     def to_torch(self, xs) -> torch.Tensor:
         if len(xs) == 1:
