@@ -54,6 +54,10 @@ typedef struct pg_dist pg_dist;
 
 /* ---- library / errors -------------------------------------------------- */
 PG_API int pg_version(void); /* ABI version, currently 1 */
+/* 1 when this build carries the device-side invariant checks (PG_CHECKS:
+ * ring-slot tags and shared-memory bounds of the asynchronous kernels,
+ * libpgmres_checked.so), else 0 */
+PG_API int pg_build_checks(void);
 PG_API int pg_last_error(char* buf, size_t len);
 PG_API int pg_device_count(int* count);
 /* Make `device` current for the calling thread (kernels launch on it). */

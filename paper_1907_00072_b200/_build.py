@@ -13,6 +13,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libpgmres.so")
+# the same sources with the device-side invariant checks (PG_CHECKS=1)
+LIB_CHECKED = os.path.join(HERE, "libpgmres_checked.so")
 BUILD = os.path.join(ROOT, "build", "pgmres")
 
 SOURCES = ["abi.cu", "spmv.cu", "ortho.cu", "host.cu", "ilu.cu", "step.cu", "chain.cu", "blasorder.cu", "march.cu", "planes.cu", "dist.cu"]
@@ -53,18 +55,23 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_library(force: bool = False, verbose: bool = False) -> str:
+def build_library(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """nvcc the sources into libpgmres.so (checked: libpgmres_checked.so with
+    -DPG_CHECKS=1, objects under build/pgmres_checked)."""
     headers = [os.path.join(INCLUDE, "pgmres.h"), os.path.join(CSRC, "internal.cuh"),
                os.path.join(CSRC, "pipeline.cuh"), os.path.join(CSRC, "sell.cuh")]
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    if not force and not _stale(LIB, srcs + headers + [__file__]):
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+    lib = LIB_CHECKED if checked else LIB
+    if not force and not _stale(lib, srcs + headers + [__file__]):
+        return lib
+    build_dir = BUILD + ("_checked" if checked else "")
+    os.makedirs(build_dir, exist_ok=True)
     nvcc = _nvcc()
+    extra = ["-DPG_CHECKS=1"] if checked else []
 
     def compile_one(src):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-I", _nccl_include(), "-c", src, "-o", obj]
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", _nccl_include(), "-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
@@ -74,16 +81,16 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
         objs = list(ex.map(compile_one, srcs))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{res.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     if verbose:
         for o in objs:
             print(open(o + ".ptxas.txt").read())
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -39,6 +39,7 @@ _pi64 = C.POINTER(C.c_int64)
 
 _SIGNATURES = {
     "pg_version": ([], C.c_int),
+    "pg_build_checks": ([], C.c_int),
     "pg_last_error": ([C.c_char_p, C.c_size_t], C.c_int),
     "pg_device_count": ([C.POINTER(C.c_int)], C.c_int),
     "pg_set_device": ([_i32], C.c_int),

@@ -520,6 +520,7 @@ using namespace pg;
 extern "C" {
 
 PG_API int pg_version(void) { return 1; }
+PG_API int pg_build_checks(void) { return PG_CHECKS; }
 
 PG_API int pg_last_error(char* buf, size_t len) {
   if (!buf || !len) return PG_ERR_PARAMETER;

@@ -4,10 +4,29 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 
 #include "pgmres.h"
+
+// Device-side invariant checks of the asynchronous kernels (ring-slot tags:
+// the slot a consumer reads holds the tile / plane / row block it expects;
+// shared-memory index bounds).  Compiled only into the checked library
+// (PG_CHECKS=1: libpgmres_checked.so, tests/test_gpu_checked.py); a violated
+// invariant prints the condition and traps, so the launch fails.  This stands
+// in for compute-sanitizer, which is closed on the GPU pool this runs on.
+#ifndef PG_CHECKS
+#define PG_CHECKS 0
+#endif
+#define PG_DCHECK(cond)                                                                  \
+  do {                                                                                   \
+    if (PG_CHECKS && !(cond)) {                                                          \
+      printf("PG_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__,        \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                               \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
 
 namespace pg {
 

@@ -163,10 +163,12 @@ __global__ void __launch_bounds__(kTileThreads)
   }
 
   // STAGES-deep cp.async ring: STAGES-1 tiles in flight while one is reduced
+  __shared__ int64_t ctag[STAGES];  // PG_CHECKS: the tile a slot holds
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     const int64_t t = tile + (int64_t)s * gridDim.x;
     if (t < ntiles) stage_tile<TR>(smem + s * buf_elems, V, ld, k, has_z ? z : nullptr, n, t);
+    if (PG_CHECKS && threadIdx.x == 0) ctag[s] = t;
     cp_async_commit();
   }
   int it = 0;
@@ -180,8 +182,10 @@ __global__ void __launch_bounds__(kTileThreads)
       if (t < ntiles)
         stage_tile<TR>(smem + ((it + STAGES - 1) % STAGES) * buf_elems, V, ld, k,
                    has_z ? z : nullptr, n, t);
+      if (PG_CHECKS && threadIdx.x == 0) ctag[(it + STAGES - 1) % STAGES] = t;
       cp_async_commit();
     }
+    PG_DCHECK(ctag[it % STAGES] == tile);
     const double* S = smem + (it % STAGES) * buf_elems;
 
     if (MODE == kDots || MODE == kUpdDots) {
@@ -304,6 +308,7 @@ __global__ void __launch_bounds__(kTileThreads)
   extern __shared__ __align__(128) double smem[];
   __shared__ double c1s[PG_KMAX];
   __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ int64_t ttag[STAGES];  // PG_CHECKS: the tile a slot holds
   const int nbox = (k + kTmaBoxCols - 1) / kTmaBoxCols;
   const int zcol = nbox * kTmaBoxCols;  // z's column slot
   const int buf_elems = (zcol + 1) * TR;
@@ -320,6 +325,7 @@ __global__ void __launch_bounds__(kTileThreads)
   const int64_t ntiles = (n + TR - 1) / TR;
   auto issue = [&](int64_t t, int slot) {
     double* buf = smem + (size_t)slot * buf_elems;
+    if (PG_CHECKS) ttag[slot] = t;
     mbar_expect_tx(&full[slot], tile_bytes);
     const int r0 = (int)(t * TR);
     for (int b = 0; b < nbox; ++b)
@@ -350,6 +356,7 @@ __global__ void __launch_bounds__(kTileThreads)
     }
     const int slot = it % STAGES;
     mbar_wait(&full[slot], (uint32_t)((it / STAGES) & 1));
+    PG_DCHECK(ttag[slot] == tile);
     const double* S = smem + (size_t)slot * buf_elems;
     const double* vec = S + (size_t)zcol * TR;
     if (MODE == kUpdDots) {

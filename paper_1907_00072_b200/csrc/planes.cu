@@ -107,6 +107,9 @@ struct WinRuns {
   __device__ static constexpr int run_pos(int i) {
     return KIND == 27 ? i % 3 : KIND == 7 ? (i == 0 || i == 4 ? 0 : i - 1) : i;
   }
+  __device__ static constexpr int run_len(int r) {
+    return KIND == 27 ? 3 : KIND == 7 ? (r == 1 ? 3 : 1) : 3;
+  }
   __device__ static constexpr int run_base(int r) {
     return KIND == 27 ? 3 * r : KIND == 7 ? (r == 0 ? 0 : r == 1 ? 1 : 4) : 0;
   }
@@ -128,6 +131,7 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
   __shared__ uint32_t s_mask[256];
   __shared__ __align__(8) uint64_t full[kPlaneMaxStages];
   __shared__ __align__(8) uint64_t empty[kPlaneMaxStages];
+  __shared__ int tag[kPlaneMaxStages];  // PG_CHECKS: the plane a slot holds
   // the masks never change after matrix creation: staged before the wait
   // (a pattern that is not a master subsequence: bit 31 + its id)
   for (int i = threadIdx.x; i < npat; i += blockDim.x) {
@@ -180,6 +184,8 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
         const int64_t n = ce > ca ? ce - ca : 0;
         if (n & 1) win[ca - ga + n - 1] = __ldg(x + ca + n - 1);
         ca -= ga;  // now the window position of the first copied element
+        PG_DCHECK(n == 0 || (ca >= 0 && ca + n <= (int64_t)pa.Q + 2 * pa.H + 2));
+        if (PG_CHECKS) tag[st] = (int)p;
         const bool start = p + 1 < zb;     // rows of plane p + 1 open
         const bool close = p - 1 >= za;    // rows of plane p - 1 close
         // interior "box" stages read no pattern ids (plane_qm, see the row threads)
@@ -348,7 +354,12 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
 #pragma unroll
     for (int h = 0; h < kPlaneRPT; ++h)
 #pragma unroll
-      for (int r = 0; r < Runs::NR; ++r) wrun[h][r] = 8u * (uint32_t)(jj[h] + pa.woff[Runs::run_base(r)]);
+      for (int r = 0; r < Runs::NR; ++r) {
+        wrun[h][r] = 8u * (uint32_t)(jj[h] + pa.woff[Runs::run_base(r)]);
+        PG_DCHECK(jj[h] + pa.woff[Runs::run_base(r)] >= 0 &&
+                  wrun[h][r] + 8u * Runs::run_len(r) <=
+                      8u * (uint32_t)(pa.Q + 2 * pa.H + 2));
+      }
     // ri: the (32-bit) row of in-plane index 0 of the tile on the closing
     // plane p - 1; ROT: also rotate the rows' masks (the interior-plane loop
     // keeps them fixed and sets them once after the loop)
@@ -468,6 +479,7 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     int p = pa0 - 1;
     for (; p < bl; ++p) {
       mbar_wait(&full[st], phase);
+      PG_DCHECK(tag[st] == p);
       stage(p);
       next_slot();
     }
@@ -477,6 +489,7 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
 #pragma unroll kPlaneUnroll
         for (; p <= bh; ++p, ri += (int)S) {
           mbar_wait(&full[st], phase);
+          PG_DCHECK(tag[st] == p);
           body(ri, mb_t, qb_t, std::true_type{}, std::false_type{});
           next_slot();
         }
@@ -484,6 +497,7 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
 #pragma unroll kPlaneUnroll
         for (; p <= bh; ++p, ri += (int)S) {
           mbar_wait(&full[st], phase);
+          PG_DCHECK(tag[st] == p);
           body(ri, mb_t, qb_t, std::false_type{}, std::false_type{});
           next_slot();
         }
@@ -501,6 +515,7 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     }
     for (; p <= pb0; ++p) {
       mbar_wait(&full[st], phase);
+      PG_DCHECK(tag[st] == p);
       stage(p);
       next_slot();
     }

@@ -608,6 +608,7 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
   __shared__ PairEnt s_ptab[PAT ? 1 : 256];
   __shared__ __align__(8) uint64_t full[kWinMaxStages];
   __shared__ __align__(8) uint64_t empty[kWinMaxStages];
+  __shared__ int64_t wtag[kWinMaxStages];  // PG_CHECKS: the row block a slot holds
   const int S = wa.stages;
   // the tables never change after matrix creation: staged before the wait
   const int32_t* s_pptr = nullptr;
@@ -651,6 +652,7 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
         bounds(rb + gridDim.x, q0, q1);
         if (round > 0) mbar_wait(&empty[st], (uint32_t)((round - 1) & 1));
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        if (PG_CHECKS) wtag[st] = rb;
         win_issue<MODE, PAT>(a, wa, e, pair8, x, rb, p0, p1,
                              smem_win + (size_t)st * wa.stage_bytes, &full[st]);
         p0 = q0;
@@ -689,6 +691,7 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
           if (!kWinStageEpi<PAT> && row < a.nrows) pre[h] = epi_load<MODE>(e, x, row);
         }
         mbar_wait(&full[st], phase);
+        PG_DCHECK(wtag[st] == rb);
 #pragma unroll
         for (int h = 0; h < kWinRPT; ++h) {
           const int th = t + h * kWinRowThreads;  // row slot inside the stage
@@ -742,6 +745,7 @@ __global__ void __launch_bounds__(kWinThreads, PG_WIN_MIN_BLOCKS)
         }
       }
       mbar_wait(&full[st], phase);
+      PG_DCHECK(wtag[st] == rb);
       if (kWinStageEpi<PAT>) {
         if (lane < sl) swl = reinterpret_cast<const int32_t*>(buf + wa.off_sw)[lane];
         if (live) {
