@@ -126,64 +126,133 @@ __global__ void __launch_bounds__(kGbThreads)
     }
   }
   const bool open = be > g0 + n;  // continues in the next shard
-  double* dst = open ? chain_out : partial + (size_t)blockIdx.x * npairs;
+  // completed blocks: partial[p * nblk + block] (pair-major, so that
+  // gram_blas_sum reads each pair's blocks contiguously)
 #pragma unroll
   for (int m = 0; m < kGbPPT; ++m) {
     const int p = threadIdx.x + m * kGbThreads;
-    if (p < npairs) dst[p] = acc[m];
+    if (p < npairs) {
+      if (open)
+        chain_out[p] = acc[m];
+      else
+        partial[(size_t)p * gridDim.x + blockIdx.x] = acc[m];
+    }
   }
 }
 
 // C = sum_in; C = C + partial[b] over the shard's completed blocks in order.
+// One warp per pair: the lanes load 32 consecutive blocks' partials at a time
+// (coalesced, several segments in flight) and every lane runs the same
+// sequential sum over them through shuffles -- the reference's order, with
+// the data movement spread over many warps (one thread per pair looping over
+// 20833 blocks took 2.7 ms at n = 8M).  ndone <= nstride columns per pair.
+constexpr int kSumAhead = 4;
 __global__ void __launch_bounds__(kGbThreads)
-    gram_blas_sum(int npairs, int64_t ndone, const double* __restrict__ partial,
+    gram_blas_sum(int npairs, int64_t ndone, int64_t nstride, const double* __restrict__ partial,
                   const double* __restrict__ sum_in, double* __restrict__ sum_out,
                   double* __restrict__ chain_out, bool zero_chain) {
   pdl_entry();
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += gridDim.x * blockDim.x) {
-    double c = sum_in ? sum_in[p] : 0.0;
-    for (int64_t b = 0; b < ndone; ++b) c = __dadd_rn(c, __ldcg(partial + b * npairs + p));
+  const int lane = threadIdx.x & 31;
+  const int p = blockIdx.x * (kGbThreads / 32) + (threadIdx.x >> 5);
+  if (p >= npairs) return;
+  const double* src = partial + (size_t)p * nstride;
+  double c = sum_in ? sum_in[p] : 0.0;
+  const int64_t nseg = (ndone + 31) / 32;
+  double v[kSumAhead];
+#pragma unroll
+  for (int u = 0; u < kSumAhead; ++u) {
+    const int64_t b = (int64_t)u * 32 + lane;
+    v[u] = b < ndone ? __ldcg(src + b) : 0.0;
+  }
+  for (int64_t s0 = 0; s0 < nseg; s0 += kSumAhead) {
+#pragma unroll
+    for (int u = 0; u < kSumAhead; ++u) {
+      const int64_t s = s0 + u;
+      if (s < nseg) {
+        const double cur = v[u];
+        const int64_t bn = (s + kSumAhead) * 32 + lane;  // refill this slot kSumAhead ahead
+        v[u] = bn < ndone ? __ldcg(src + bn) : 0.0;
+        const int cnt = (int)((ndone - s * 32) < 32 ? (ndone - s * 32) : 32);
+        for (int j = 0; j < cnt; ++j) c = __dadd_rn(c, __shfl_sync(0xffffffffu, cur, j));
+      }
+    }
+  }
+  if (lane == 0) {
     sum_out[p] = c;
     if (zero_chain) chain_out[p] = 0.0;
   }
 }
 
-// OpenBLAS x86-64 ddot order (see the file header).  One warp per chunk.
-__global__ void __launch_bounds__(1024)
+// OpenBLAS x86-64 ddot order (see the file header).  One CTA per chunk:
+// warp 0's 32 lanes run the chunk's 32 FMA chains (lane l: elements l, l+32,
+// ... in order) from shared memory while the other warps stage the next
+// kDotTile elements of x and y (double-buffered), so the chains do not wait
+// on one global load batch at a time (one CTA of 16 warps loading for
+// itself took 2.1 ms at n = 8M).  The chunk's dot goes to scratch[t];
+// dot_blas_sum adds the chunks in order.
+constexpr int kDotThreads = 512;
+constexpr int kDotTile = 2048;   // elements of x and of y per ring stage
+constexpr int kDotStages = 4;    // 128 KB of dynamic shared memory
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__global__ void __launch_bounds__(kDotThreads)
     dot_blas_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
-                    int nthreads, double* out) {
+                    int nthreads, double* scratch) {
   pdl_entry();
-  __shared__ double lane_acc[32][33];
-  __shared__ double chunk_dot[32];
-  const int lane = threadIdx.x & 31, t = threadIdx.x >> 5;
-  if (t < nthreads) {
-    int64_t off = 0, w = 0;
-    for (int u = 0; u <= t; ++u) {
-      off += w;
-      w = (n - off + (nthreads - u) - 1) / (nthreads - u);
-    }
-    const double* xs = x + off;
-    const double* ys = y + off;
-    const int64_t n1 = w & ~(int64_t)15, n32 = w & ~(int64_t)31;
-    double a = 0.0;
-    int64_t i = lane;
-    for (; i + 7 * 32 < n32; i += 8 * 32) {
-      double xv[8], yv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        xv[u] = __ldcs(xs + i + 32 * u);
-        yv[u] = __ldcs(ys + i + 32 * u);
+  extern __shared__ double ring[];  // [kDotStages][2][kDotTile]
+  __shared__ double lane_acc[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x;
+  int64_t off = 0, w = 0;
+  for (int u = 0; u <= t; ++u) {
+    off += w;
+    w = (n - off + (nthreads - u) - 1) / (nthreads - u);
+  }
+  const double* xs = x + off;
+  const double* ys = y + off;
+  const int64_t n1 = w & ~(int64_t)15, n32 = w & ~(int64_t)31;
+  const int64_t ntile = (n32 + kDotTile - 1) / kDotTile;
+  // warps 1.. keep kDotStages-1 tiles in flight (8-byte cp.async: the
+  // chunk start is not 16-byte aligned in general)
+  auto stage = [&](int64_t tile) {
+    if (tile < ntile) {
+      double* X = ring + (tile % kDotStages) * 2 * kDotTile;
+      const int64_t a = tile * kDotTile;
+      const int m = (int)((n32 - a) < kDotTile ? (n32 - a) : kDotTile);
+      for (int e = threadIdx.x - 32; e < m; e += kDotThreads - 32) {
+        cp_async8(X + e, xs + a + e);
+        cp_async8(X + kDotTile + e, ys + a + e);
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) a = __fma_rn(xv[u], yv[u], a);
     }
-    for (; i < n32; i += 32) a = __fma_rn(xs[i], ys[i], a);
-    lane_acc[t][lane] = a;
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if (warp > 0)
+    for (int s = 0; s < kDotStages - 1; ++s) stage(s);
+  double acc = 0.0;
+  for (int64_t i = 0; i < ntile; ++i) {
+    if (warp > 0) asm volatile("cp.async.wait_group %0;\n" ::"n"(kDotStages - 2) : "memory");
+    __syncthreads();  // tile i landed; warp 0 is done with tile i-1
+    if (warp == 0) {
+      const int m = (int)((n32 - i * kDotTile) < kDotTile ? (n32 - i * kDotTile) : kDotTile);
+      const double* X = ring + (i % kDotStages) * 2 * kDotTile;
+      const double* Y = X + kDotTile;
+      for (int e = lane; e < m; e += 32) acc = __fma_rn(X[e], Y[e], acc);
+    } else {
+      stage(i + kDotStages - 1);
+    }
+  }
+  if (warp > 0) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  if (warp == 0) {
+    lane_acc[lane] = acc;
     __syncwarp();
     if (lane == 0) {
       double dot = 0.0;
       if (n1 > 0) {
-        const double* L = lane_acc[t];
+        const double* L = lane_acc;
         double q[4][4];
 #pragma unroll
         for (int g = 0; g < 4; ++g)
@@ -203,14 +272,18 @@ __global__ void __launch_bounds__(1024)
         dot = __dadd_rn(__dadd_rn(s[0], s[2]), __dadd_rn(s[1], s[3]));
       }
       for (int64_t r = n1; r < w; ++r) dot = __fma_rn(ys[r], xs[r], dot);
-      chunk_dot[t] = dot;
+      scratch[t] = dot;
     }
   }
-  __syncthreads();
+}
+
+// The chunks' dots added in chunk order (one chunk: its dot as is).
+__global__ void dot_blas_sum(const double* __restrict__ scratch, int nthreads, double* out) {
+  pdl_entry();
   if (threadIdx.x == 0) {
     double d = 0.0;
-    for (int u = 0; u < nthreads; ++u) d = __dadd_rn(d, chunk_dot[u]);
-    *out = nthreads == 1 ? chunk_dot[0] : d;
+    for (int u = 0; u < nthreads; ++u) d = __dadd_rn(d, scratch[u]);
+    *out = nthreads == 1 ? scratch[0] : d;
   }
 }
 
@@ -271,8 +344,9 @@ PG_API int pg_gram_blas(const double* d_P, int64_t ld, int ncols, int64_t n, int
              n, g0, N, b_lo, chain_in, chain_out, d_scratch);
     check_launch();
     const int64_t ndone = open ? nblk - 1 : nblk;
-    launch_k(gram_blas_sum, dim3((npairs + kGbThreads - 1) / kGbThreads), dim3(kGbThreads), 0,
-             st, npairs, ndone, (const double*)d_scratch, sum_in, sum_out, chain_out, !open);
+    const int wpb = kGbThreads / 32;
+    launch_k(gram_blas_sum, dim3((npairs + wpb - 1) / wpb), dim3(kGbThreads), 0, st, npairs,
+             ndone, nblk, (const double*)d_scratch, sum_in, sum_out, chain_out, !open);
     check_launch();
   });
 }
@@ -288,7 +362,26 @@ PG_API int pg_dot_blas(const double* d_x, const double* d_y, int64_t n, int nthr
       return;
     }
     const int T = n <= 10000 ? 1 : nthreads;
-    launch_k(dot_blas_kernel, dim3(1), dim3(32 * T), 0, st, d_x, d_y, n, T, d_out);
+    // 32 chunk dots per device, allocated once (before any graph capture:
+    // pg_dot_blas is a construction-time call)
+    static double* scratch[64] = {};
+    int dev = 0;
+    PG_CUDA(cudaGetDevice(&dev));
+    PG_REQUIRE(dev >= 0 && dev < 64, PG_ERR_PARAMETER, "device ordinal out of range");
+    if (!scratch[dev]) {
+      PG_REQUIRE(!g_capturing, PG_ERR_PARAMETER, "pg_dot_blas first called inside a capture");
+      PG_CUDA(cudaMalloc(&scratch[dev], 32 * sizeof(double)));
+    }
+    static bool dot_attr[64] = {};
+    if (!dot_attr[dev]) {
+      PG_CUDA(cudaFuncSetAttribute(dot_blas_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(double) * kDotStages * 2 * kDotTile)));
+      dot_attr[dev] = true;
+    }
+    launch_k(dot_blas_kernel, dim3(T), dim3(kDotThreads), sizeof(double) * kDotStages * 2 * kDotTile,
+             st, d_x, d_y, n, T, scratch[dev]);
+    check_launch();
+    launch_k(dot_blas_sum, dim3(1), dim3(32), 0, st, (const double*)scratch[dev], T, d_out);
     check_launch();
   });
 }
