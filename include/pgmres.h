@@ -114,6 +114,15 @@ PG_API int pg_matrix_destroy(pg_matrix* mat);
  *              patterns (1 B per row + f64 values), 8 plane marching,
  *              9 plane ring (TMA-staged plane windows))} */
 PG_API int pg_matrix_stats(const pg_matrix* mat, int64_t* stats);
+/* Launch plan of the plane-ring kernel (stats kernel 9), fixed at creation:
+ * plan[9] = {stencil kind (27, 7, 9, 5; 0 = not a plane stencil), tile width
+ *            Q, planes per chunk, ring stages, blocks, in-plane halo H,
+ *            box level (0: pattern ids read on every plane, 1: none on
+ *            interior planes, 2: none at all -- end planes verified too),
+ *            stage bytes, shared outer-group products (1: the dz = -1 and
+ *            dz = +1 coefficients are equal at every in-plane offset but the
+ *            center, each such product is computed once for both rows)}. */
+PG_API int pg_plane_plan(const pg_matrix* mat, int64_t* plan);
 
 /* ---- reduction workspace (one per stream) --------------------------------
  * Block partials + a completion counter for the deterministic fixed-order

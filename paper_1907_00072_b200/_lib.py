@@ -48,6 +48,7 @@ _SIGNATURES = {
     "pg_matrix_create": ([_i32, _i64, _i64, _p, _p, _p, _i32, C.POINTER(_p)], C.c_int),
     "pg_matrix_destroy": ([_p], C.c_int),
     "pg_matrix_stats": ([_p, _pi64], C.c_int),
+    "pg_plane_plan": ([_p, _pi64], C.c_int),
     "pg_workspace_create": ([_i32, C.POINTER(_p)], C.c_int),
     "pg_workspace_destroy": ([_p], C.c_int),
     "pg_spmv": ([_p, _p, _p, _p], C.c_int),

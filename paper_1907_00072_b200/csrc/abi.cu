@@ -670,6 +670,22 @@ PG_API int pg_matrix_stats(const pg_matrix* m, int64_t* s) {
   });
 }
 
+PG_API int pg_plane_plan(const pg_matrix* m, int64_t* s) {
+  return guard([&] {
+    PG_REQUIRE(m && s, PG_ERR_PARAMETER, "null argument");
+    const bool on = m->plane_kind != 0;
+    s[0] = m->plane_kind;
+    s[1] = on ? m->plane.Q : 0;
+    s[2] = on ? m->plane.Zc : 0;
+    s[3] = on ? m->plane.stages : 0;
+    s[4] = on ? m->plane_blocks : 0;
+    s[5] = on ? m->plane.H : 0;
+    s[6] = !on || !m->plane_qm ? 0 : (m->plane.allbox ? 2 : 1);
+    s[7] = on ? m->plane.stage_bytes : 0;
+    s[8] = on ? m->plane_sym : 0;
+  });
+}
+
 PG_API int pg_workspace_create(int device, pg_workspace** out) {
   return guard([&] {
     PG_REQUIRE(out, PG_ERR_PARAMETER, "out is null");

@@ -83,6 +83,7 @@ struct PlaneArgs {
   int Q, nqb, Zc, H, sh;
   int stages, stage_bytes, off_a, off_b, off_p;
   int woff[9];
+  int allbox;  // end planes verified too: no stage reads pattern ids (planes.cu)
 };
 }  // namespace pg
 
@@ -149,6 +150,8 @@ struct pg_matrix {
   int64_t dband_lo, dband_hi;
   // plane-ring kernel (planes.cu): plane_kind 0 = not a plane stencil / off
   int plane_kind, plane_blocks;
+  int plane_sym;  // 1: outer plane groups share their coefficients but the center's
+
   pg::PlaneArgs plane;
   // plane_qm[q]: the in-plane entry mask of every interior-plane row at
   // in-plane index q (host-verified: the same box pattern on planes

@@ -115,7 +115,12 @@ struct WinRuns {
   }
 };
 
-template <int MODE, int KIND, int EF>
+// SYM (tensor stencils): outer-group coefficients equal bit for bit, dz = -1
+// vs dz = +1 at the same in-plane offset, for every offset (2) or every one
+// but the center (1: the plane-normal convection term sits on the center
+// pair only).  The two rows that use a window value with those coefficients
+// then receive the same rounded product, computed once.
+template <int MODE, int KIND, int EF, int SYM = 0>
 __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     plane_ring_kernel(PlaneArgs pa, const uint8_t* __restrict__ rpat,
                       const int32_t* __restrict__ pptr, const PairEnt* __restrict__ pent,
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
         const bool close = p - 1 >= za;    // rows of plane p - 1 close
         // interior "box" stages read no pattern ids (plane_qm, see the row threads)
         const bool boxed = plane_qm && p >= za + 1 && p + 2 <= zb && p >= 2 && p + 3 <= pa.nz;
-        const bool ids = start && !boxed;
+        const bool ids = start && !boxed && !pa.allbox;
         uint32_t bytes = 8u * (uint32_t)(n & ~(int64_t)1);
         if (ids) bytes += (uint32_t)Qt;
         if (close && A) bytes += 8u * (uint32_t)Qt;
@@ -394,8 +399,11 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
             const int h = h0 + u;
             if (i < NO) {
               const double o = Sh::FULL ? P[u][i] : P[u][Sh::CTR];
-              acc_f[h] = __dadd_rn(acc_f[h], __dmul_rn(pm.v[NO + NM + i], o));
-              acc_s[h] = __dadd_rn(acc_s[h], __dmul_rn(pm.v[i], o));
+              const double pf = __dmul_rn(pm.v[NO + NM + i], o);
+              const bool same = Sh::FULL && (SYM == 2 || (SYM == 1 && i != Sh::CTR));
+              const double ps = same ? pf : __dmul_rn(pm.v[i], o);
+              acc_f[h] = __dadd_rn(acc_f[h], pf);
+              acc_s[h] = __dadd_rn(acc_s[h], ps);
             }
             acc_m[h] = __dadd_rn(acc_m[h], __dmul_rn(pm.v[NO + i], P[u][i]));
           }
@@ -461,8 +469,58 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     // host-verified matrix, [bl, bh], run as a counted loop of the unrolled
     // body (no pattern ids, no per-stage dispatch).
     const int pa0 = (int)za, pb0 = (int)zb;
+    // Host-verified matrices whose end planes are box rows too (pa.allbox:
+    // plane 0 rows hold no dz = -1 group, plane nz-1 rows no dz = +1 group,
+    // every other group the in-plane entries plane_qm[q]): the warm-up and
+    // drain stages of a chunk run the unrolled body with the absent groups
+    // switched off, so no stage reads pattern ids or takes the general path.
+    auto edge = [&](int p) {
+      const bool C = p - 1 >= pa0;               // rows of plane p - 1 close
+      const bool CA = C && p < (int)pa.nz;       // ... and have a dz = +1 group
+      const bool M = p >= pa0 && p < pb0;        // rows of plane p continue
+      const bool SA = p + 1 < pb0 && p >= 0;     // rows of plane p + 1 open with a dz = -1 group
+      const int ri = (p - 1) * (int)S + (int)q0;
+      double acc_s[kPlaneRPT];
+#pragma unroll
+      for (int h0 = 0; h0 < kPlaneRPT; h0 += 2) {
+        double P[2][NM];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int i = 0; i < NM; ++i) {
+            P[u][i] = reinterpret_cast<const double*>(buf + wrun[h0 + u][Runs::run_of(i)])
+                [Runs::run_pos(i)];
+            if (!((qb_t[h0 + u] >> i) & 1u)) P[u][i] = 0.0;
+          }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) acc_s[h0 + u] = 0.0;
+#pragma unroll
+        for (int i = 0; i < NM; ++i) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int h = h0 + u;
+            if (i < NO) {
+              const double o = Sh::FULL ? P[u][i] : P[u][Sh::CTR];
+              if (CA) acc_f[h] = __dadd_rn(acc_f[h], __dmul_rn(pm.v[NO + NM + i], o));
+              if (SA) acc_s[h] = __dadd_rn(acc_s[h], __dmul_rn(pm.v[i], o));
+            }
+            if (M) acc_m[h] = __dadd_rn(acc_m[h], __dmul_rn(pm.v[NO + i], P[u][i]));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (C && act[h0 + u]) finish(h0 + u, (int64_t)(ri + jj[h0 + u]), acc_f[h0 + u]);
+      }
+#pragma unroll
+      for (int h = 0; h < kPlaneRPT; ++h) {
+        acc_f[h] = acc_m[h];
+        acc_m[h] = acc_s[h];
+      }
+    };
     auto stage = [&](int p) {
-      if (p >= pa0 + 1 && p <= pb0 - 2) {
+      if (pa.allbox) {
+        edge(p);
+      } else if (p >= pa0 + 1 && p <= pb0 - 2) {
         steady(p);
       } else {
         const bool start = p + 1 < pb0;
@@ -472,6 +530,10 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
       }
     };
     int bl = max(pa0 + 1, 2), bh = min(pb0 - 2, (int)pa.nz - 3);
+    if (pa.allbox) {  // every steady stage of the chunk, global end planes included
+      bl = pa0 + 1;
+      bh = pb0 - 2;
+    }
     if (!plane_qm || (PG_PLANE_EXP & 4) || bh < bl) {
       bl = pb0 + 1;
       bh = pb0;
@@ -621,6 +683,18 @@ void plane_prepare(pg_matrix* m) {
   for (int i = 0; i < NM; ++i) pa.woff[i] = (int)(mid_off_host(kind, i, g) + H + pa.sh);
   m->plane_blocks = (int)((int64_t)pa.nqb * ((nz + bz - 1) / bz));
   m->plane_kind = kind;
+  // outer plane groups with bitwise equal coefficients (kernel SYM variants;
+  // PG_PLANE_SYM=0: off)
+  m->plane_sym = 0;
+  if (kind == 27 && m->pat_mlen == 27 && plane_env("PG_PLANE_SYM", 1)) {
+    bool rest = true, ctr = true;
+    for (int i = 0; i < 9; ++i) {
+      const bool eq = std::memcmp(&m->pat_mv[i], &m->pat_mv[18 + i], sizeof(double)) == 0;
+      if (i == 4) ctr = eq; else rest = rest && eq;
+    }
+    m->plane_sym = rest ? 1 : 0;  // (ctr && rest: still variant 1, one product more)
+    (void)ctr;
+  }
   // Interior planes 1 .. nz-2: if every in-plane index q has one pattern on
   // all of them and that pattern is a "box" row (all three plane groups
   // holding the same in-plane entries qm), the kernel's interior stages use
@@ -644,6 +718,18 @@ void plane_prepare(pg_matrix* m) {
       qm[(size_t)q] = (uint16_t)m9;
     }
     if (ok) {
+      // end planes: plane 0 rows without the dz = -1 group, plane nz-1 rows
+      // without the dz = +1 group, the other groups as on interior planes
+      // (PG_PLANE_BOX=1: interior planes only)
+      bool ends = plane_env("PG_PLANE_BOX", 2) >= 2;
+      const bool full = kind == 27 || kind == 9;
+      for (int64_t q = 0; q < S && ends; ++q) {
+        const uint32_t m9 = qm[(size_t)q];
+        const uint32_t lo = full ? m9 : 1u, hi = (full ? m9 : 1u) << (NO + NM);
+        ends = mk[id[(size_t)q]] == ((m9 << NO) | hi) &&
+               mk[id[(size_t)((nz - 1) * S + q)]] == (lo | (m9 << NO));
+      }
+      pa.allbox = ends ? 1 : 0;
       PG_CUDA(cudaMalloc(&m->plane_qm, 2 * qm.size()));
       PG_CUDA(cudaMemcpy(m->plane_qm, qm.data(), 2 * qm.size(), cudaMemcpyHostToDevice));
       m->bytes += 2 * qm.size();
@@ -667,16 +753,28 @@ bool plane_launch(const pg_matrix* m, const double* x, Epi e, pg_workspace* ws, 
   for (int i = 0; i < pm.len; ++i) pm.v[i] = m->pat_mv[i];
   const size_t smem = (size_t)m->plane.stages * m->plane.stage_bytes;
   // kPoly on 27-point stencils: the pass flags and base presence as
-  // compile-time constants (EF); else runtime flags (EF = -1)
+  // compile-time constants (EF); else runtime flags (EF = -1).  27-point
+  // stencils whose outer plane groups share their coefficients (SYM, all
+  // offsets but the center): the shared-product variants.
   const int ef = (e.flags & 3) | (e.base ? 4 : 0);
   auto kern = plane_ring_kernel<MODE, 27, -1>;
   int ki = 0;
+  const bool sym = m->plane_kind == 27 && m->plane_sym == 1;
   if (MODE == kPoly && m->plane_kind == 27) {
-    kern = ef == 0 ? plane_ring_kernel<MODE, 27, 0> : ef == 1 ? plane_ring_kernel<MODE, 27, 1>
-         : ef == 2 ? plane_ring_kernel<MODE, 27, 2> : ef == 3 ? plane_ring_kernel<MODE, 27, 3>
-         : ef == 4 ? plane_ring_kernel<MODE, 27, 4> : ef == 5 ? plane_ring_kernel<MODE, 27, 5>
-         : ef == 6 ? plane_ring_kernel<MODE, 27, 6> : plane_ring_kernel<MODE, 27, 7>;
-    ki = 4 + ef;
+    if (sym)
+      kern = ef == 0 ? plane_ring_kernel<MODE, 27, 0, 1> : ef == 1 ? plane_ring_kernel<MODE, 27, 1, 1>
+           : ef == 2 ? plane_ring_kernel<MODE, 27, 2, 1> : ef == 3 ? plane_ring_kernel<MODE, 27, 3, 1>
+           : ef == 4 ? plane_ring_kernel<MODE, 27, 4, 1> : ef == 5 ? plane_ring_kernel<MODE, 27, 5, 1>
+           : ef == 6 ? plane_ring_kernel<MODE, 27, 6, 1> : plane_ring_kernel<MODE, 27, 7, 1>;
+    else
+      kern = ef == 0 ? plane_ring_kernel<MODE, 27, 0> : ef == 1 ? plane_ring_kernel<MODE, 27, 1>
+           : ef == 2 ? plane_ring_kernel<MODE, 27, 2> : ef == 3 ? plane_ring_kernel<MODE, 27, 3>
+           : ef == 4 ? plane_ring_kernel<MODE, 27, 4> : ef == 5 ? plane_ring_kernel<MODE, 27, 5>
+           : ef == 6 ? plane_ring_kernel<MODE, 27, 6> : plane_ring_kernel<MODE, 27, 7>;
+    ki = 4 + ef + (sym ? 8 : 0);
+  } else if (sym) {
+    kern = plane_ring_kernel<MODE, 27, -1, 1>;
+    ki = 20;
   } else {
     kern = m->plane_kind == 27 ? plane_ring_kernel<MODE, 27, -1>
          : m->plane_kind == 7  ? plane_ring_kernel<MODE, 7, -1>
@@ -684,7 +782,7 @@ bool plane_launch(const pg_matrix* m, const double* x, Epi e, pg_workspace* ws, 
                                : plane_ring_kernel<MODE, 5, -1>;
     ki = m->plane_kind == 27 ? 0 : m->plane_kind == 7 ? 1 : m->plane_kind == 9 ? 2 : 3;
   }
-  static bool attr[4][12][64] = {};
+  static bool attr[4][21][64] = {};
   const int dev = m->device;
   if (!attr[MODE][ki][dev]) {
     PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -35,6 +35,29 @@ def _matrix(kind, g):
         return wl.convdiff3d_7pt(g)
     if kind == "lap5":
         return wl.laplacian2d(g)
+    if kind == "rand27":
+        # a constant-coefficient 27-point operator with 27 distinct values (no
+        # coefficient shared between the outer plane groups)
+        from paper_1907_00072_b200.workloads import CsrHost
+        w = np.random.default_rng(27).uniform(-1.0, 1.0, (3, 3, 3))
+        w[1, 1, 1] = 9.0
+        z, y, x = np.meshgrid(np.arange(g), np.arange(g), np.arange(g), indexing="ij")
+        rows, cols, vals = [], [], []
+        for dz in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    ok = ((z + dz >= 0) & (z + dz < g) & (y + dy >= 0) & (y + dy < g)
+                          & (x + dx >= 0) & (x + dx < g))
+                    r = ((z * g + y) * g + x)[ok]
+                    rows.append(r)
+                    cols.append(r + (dz * g + dy) * g + dx)
+                    vals.append(np.full(r.size, w[dz + 1, dy + 1, dx + 1]))
+        rows, cols, vals = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+        order = np.lexsort((cols, rows))
+        n = g ** 3
+        rp = np.zeros(n + 1, dtype=np.int64)
+        np.add.at(rp, rows + 1, 1)
+        return CsrHost(n, n, np.cumsum(rp), cols[order].astype(np.int64), vals[order])
     # a constant-coefficient 2-D 9-point operator (row patterns, not offset patterns)
     from paper_1907_00072_b200.workloads import CsrHost
     n = g * g

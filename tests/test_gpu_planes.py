@@ -21,7 +21,8 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 # (kind, g): the plane stride S (g^2 for 3-D, g for 2-D) must be a multiple of 16
-CASES = [("aniso27", 12), ("aniso27", 20), ("aniso27", 28), ("conv7", 20), ("conv7", 28),
+CASES = [("aniso27", 12), ("aniso27", 20), ("aniso27", 28), ("rand27", 12), ("rand27", 20),
+         ("conv7", 20), ("conv7", 28),
          ("lap5", 48), ("conv9", 32), ("conv9", 64)]
 
 
@@ -67,6 +68,16 @@ for kind, g in {CASES!r}:
     k = op.engine.shards[0].stats["kernel"]
     op.close()
     assert k == 9, (kind, g, k)
+    import os
+    want_box = int(os.environ.get("PG_PLANE_BOX", "2"))
+    op = pg.DeviceMatrixOperator(h)
+    plan = op.engine.shards[0].plane_plan
+    assert plan["box"] == want_box, plan
+    # shared outer-group products: config 4's operator (z-symmetric but for the
+    # center pair), not the operator with 27 distinct coefficients
+    want_sym = int(kind == "aniso27" and os.environ.get("PG_PLANE_SYM", "1") != "0")
+    assert plan["sym"] == want_sym, plan
+    op.close()
     t._check(h)
     for shards in (2, 3):
         t._check(h, shards)
@@ -82,6 +93,10 @@ print("ok")
     {"PG_PLANE_Q": "576", "PG_PLANE_Z": "5"},     # the widest tile (second row set)
     {"PG_PLANE_STAGES": "3"},
     {"PG_PLANE_BOX": "0"},                        # per-row pattern ids on every plane
+    {"PG_PLANE_BOX": "1"},                        # ids on the end planes only
+    {"PG_PLANE_SYM": "0"},                        # every product computed per row
+    {"PG_PLANE_Q": "64", "PG_PLANE_Z": "2"},      # 2-plane chunks: no steady stage
+    {"PG_PLANE_Q": "128", "PG_PLANE_Z": "3", "PG_PLANE_STAGES": "2"},
     {"PG_PLANE_BOX": "0", "PG_PLANE_Q": "64", "PG_PLANE_Z": "4"},
 ])
 def test_plane_kernel_selected_and_bitwise(env):
