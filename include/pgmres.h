@@ -115,13 +115,15 @@ PG_API int pg_matrix_destroy(pg_matrix* mat);
  *              9 plane ring (TMA-staged plane windows))} */
 PG_API int pg_matrix_stats(const pg_matrix* mat, int64_t* stats);
 /* Launch plan of the plane-ring kernel (stats kernel 9), fixed at creation:
- * plan[9] = {stencil kind (27, 7, 9, 5; 0 = not a plane stencil), tile width
+ * plan[10] = {stencil kind (27, 7, 9, 5; 0 = not a plane stencil), tile width
  *            Q, planes per chunk, ring stages, blocks, in-plane halo H,
  *            box level (0: pattern ids read on every plane, 1: none on
  *            interior planes, 2: none at all -- end planes verified too),
  *            stage bytes, shared outer-group products (1: the dz = -1 and
  *            dz = +1 coefficients are equal at every in-plane offset but the
- *            center, each such product is computed once for both rows)}. */
+ *            center, each such product is computed once for both rows),
+ *            aligned row pairs (1: a row thread's two adjacent rows read
+ *            their operands and write their results as 16-byte pairs)}. */
 PG_API int pg_plane_plan(const pg_matrix* mat, int64_t* plan);
 
 /* ---- reduction workspace (one per stream) --------------------------------

@@ -683,6 +683,7 @@ PG_API int pg_plane_plan(const pg_matrix* m, int64_t* s) {
     s[6] = !on || !m->plane_qm ? 0 : (m->plane.allbox ? 2 : 1);
     s[7] = on ? m->plane.stage_bytes : 0;
     s[8] = on ? m->plane_sym : 0;
+    s[9] = on ? m->plane.vec : 0;
   });
 }
 

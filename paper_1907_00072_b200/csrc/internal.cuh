@@ -81,9 +81,10 @@ namespace pg {
 struct PlaneArgs {
   int64_t nrows, ncols, S, nz;
   int Q, nqb, Zc, H, sh;
-  int stages, stage_bytes, off_a, off_b, off_p;
+  int stages, stage_bytes, off_a, off_b, off_p, off_bar;
   int woff[9];
   int allbox;  // end planes verified too: no stage reads pattern ids (planes.cu)
+  int vec;     // adjacent row pairs move as aligned 16-byte pairs (planes.cu)
 };
 }  // namespace pg
 

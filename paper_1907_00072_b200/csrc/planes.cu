@@ -67,6 +67,7 @@ constexpr int kPlaneUnroll = PG_PLANE_UNROLL;
 #ifndef PG_PLANE_MIN_BLOCKS
 #define PG_PLANE_MIN_BLOCKS 2
 #endif
+
 // dynamic shared memory per block (ring), leaving room for PG_PLANE_MIN_BLOCKS
 constexpr int kPlaneSmemBudget = 200 * 1024 / PG_PLANE_MIN_BLOCKS;
 
@@ -120,7 +121,12 @@ struct WinRuns {
 // but the center (1: the plane-normal convection term sits on the center
 // pair only).  The two rows that use a window value with those coefficients
 // then receive the same rounded product, computed once.
-template <int MODE, int KIND, int EF, int SYM = 0>
+// ADJ (27-point tiles with PlaneArgs::vec): a row thread's two in-plane
+// indices are adjacent (2t, 2t+1) instead of t, t + kPlaneRowThreads: the two
+// rows share 2 of the 3 window values of every run (4 shared loads per run,
+// one of them 16 bytes, instead of 6), and their epilogue operands and
+// results move as aligned 16-byte pairs.
+template <int MODE, int KIND, int EF, int SYM = 0, bool ADJ = false>
 __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     plane_ring_kernel(PlaneArgs pa, const uint8_t* __restrict__ rpat,
                       const int32_t* __restrict__ pptr, const PairEnt* __restrict__ pent,
@@ -129,14 +135,20 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
                       unsigned int* counter, double* nsq,
                       const uint16_t* __restrict__ plane_qm) {
   using Sh = MarchShape<KIND>;
+  static_assert(!ADJ || (KIND == 27 && kPlaneRPT == 2), "pair path: 27-point, two rows per thread");
+  constexpr bool kPlaneAdj = ADJ;
   constexpr int NO = Sh::NO, NM = Sh::NM, LEN = 2 * NO + NM;
   constexpr uint32_t kFull = (1u << LEN) - 1u;
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   extern __shared__ __align__(128) unsigned char smem_plane[];
   __shared__ uint32_t s_mask[256];
-  __shared__ __align__(8) uint64_t full[kPlaneMaxStages];
-  __shared__ __align__(8) uint64_t empty[kPlaneMaxStages];
+  // a stage's full / empty mbarriers sit inside the stage (pa.off_bar), so
+  // the row threads track the ring with one pointer and a phase bit
   __shared__ int tag[kPlaneMaxStages];  // PG_CHECKS: the plane a slot holds
+  auto full_of = [&](const unsigned char* stage) {
+    return reinterpret_cast<uint64_t*>(const_cast<unsigned char*>(stage) + pa.off_bar);
+  };
+  auto empty_of = [&](const unsigned char* stage) { return full_of(stage) + 1; };
   // the masks never change after matrix creation: staged before the wait
   // (a pattern that is not a master subsequence: bit 31 + its id)
   for (int i = threadIdx.x; i < npat; i += blockDim.x) {
@@ -147,8 +159,8 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
   const int NS = pa.stages;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kPlaneRowThreads / 32);
+      mbar_init(full_of(smem_plane + (size_t)s * pa.stage_bytes), 1);
+      mbar_init(empty_of(smem_plane + (size_t)s * pa.stage_bytes), kPlaneRowThreads / 32);
     }
     mbar_fence_init();
   }
@@ -164,6 +176,20 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
   const int nstage = (int)(zb - za) + 2;
   double local = 0.0;
   const int warp = threadIdx.x >> 5;
+  // The steady planes of the chunk whose three rows are all on interior
+  // planes of a host-verified matrix, [box_lo, box_hi]: no pattern ids are
+  // staged for them, the row threads run them as a counted loop.  Only with
+  // at least two such planes (the rows closing and continuing after the
+  // loop were then both opened inside it); allbox: the end planes too.
+  int box_lo = (int)zb + 1, box_hi = (int)zb;
+  if (plane_qm && !(PG_PLANE_EXP & 4)) {
+    const int lo = pa.allbox ? (int)za + 1 : max((int)za + 1, 2);
+    const int hi = pa.allbox ? (int)zb - 2 : min((int)zb - 2, (int)pa.nz - 3);
+    if (hi >= lo + 1) {
+      box_lo = lo;
+      box_hi = hi;
+    }
+  }
 
   if (warp == kPlaneRowThreads / 32) {
     if ((threadIdx.x & 31) == 0) {
@@ -173,9 +199,10 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
       const int wl = (Qt + 2 * pa.H + pa.sh + 1) & ~1;
       int st = 0, round = 0;
       for (int k = 0; k < nstage; ++k) {
-        if (round > 0) mbar_wait(&empty[st], (uint32_t)((round - 1) & 1));
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         unsigned char* buf = smem_plane + (size_t)st * pa.stage_bytes;
+        uint64_t* const full_st = full_of(buf);
+        if (round > 0) mbar_wait(empty_of(buf), (uint32_t)((round - 1) & 1));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         double* win = reinterpret_cast<double*>(buf);
         const int64_t p = za - 1 + k;
         // window of plane p: [p S + q0 - H - sh, p S + q0 + Qt + H + 1), both
@@ -194,7 +221,7 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
         const bool start = p + 1 < zb;     // rows of plane p + 1 open
         const bool close = p - 1 >= za;    // rows of plane p - 1 close
         // interior "box" stages read no pattern ids (plane_qm, see the row threads)
-        const bool boxed = plane_qm && p >= za + 1 && p + 2 <= zb && p >= 2 && p + 3 <= pa.nz;
+        const bool boxed = p >= box_lo && p <= box_hi;
         const bool ids = start && !boxed && !pa.allbox;
         uint32_t bytes = 8u * (uint32_t)(n & ~(int64_t)1);
         if (ids) bytes += (uint32_t)Qt;
@@ -202,13 +229,13 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
         if (close && B) bytes += 8u * (uint32_t)Qt;
         if (PG_PLANE_EXP & 1) bytes -= 8u * (uint32_t)(n & ~(int64_t)1);
         if (PG_PLANE_EXP & 2) bytes -= ((close && A) + (close && B)) * 8u * (uint32_t)Qt;
-        mbar_expect_tx(&full[st], bytes);
-        if (n > 1 && !(PG_PLANE_EXP & 1)) bulk_g2s(win + ca, x + ga + ca, 8u * (uint32_t)(n & ~(int64_t)1), &full[st]);
-        if (ids) bulk_g2s(buf + pa.off_p, rpat + (p + 1) * S + q0, (uint32_t)Qt, &full[st]);
+        mbar_expect_tx(full_st, bytes);
+        if (n > 1 && !(PG_PLANE_EXP & 1)) bulk_g2s(win + ca, x + ga + ca, 8u * (uint32_t)(n & ~(int64_t)1), full_st);
+        if (ids) bulk_g2s(buf + pa.off_p, rpat + (p + 1) * S + q0, (uint32_t)Qt, full_st);
         if (close && A && !(PG_PLANE_EXP & 2))
-          bulk_g2s(buf + pa.off_a, A + (p - 1) * S + q0, 8u * (uint32_t)Qt, &full[st]);
+          bulk_g2s(buf + pa.off_a, A + (p - 1) * S + q0, 8u * (uint32_t)Qt, full_st);
         if (close && B && !(PG_PLANE_EXP & 2))
-          bulk_g2s(buf + pa.off_b, B + (p - 1) * S + q0, 8u * (uint32_t)Qt, &full[st]);
+          bulk_g2s(buf + pa.off_b, B + (p - 1) * S + q0, 8u * (uint32_t)Qt, full_st);
         if (++st == NS) {
           st = 0;
           ++round;
@@ -233,9 +260,11 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     bool act[kPlaneRPT];
 #pragma unroll
     for (int h = 0; h < kPlaneRPT; ++h) {
-      const int j = t + h * kPlaneRowThreads;
+      const int j = kPlaneAdj ? t * kPlaneRPT + h : t + h * kPlaneRowThreads;
       act[h] = j < Qt;
-      jj[h] = act[h] ? j : 0;
+      // (adjacent indices keep their distance: the slots of an inactive pair
+      // are in range of the stage, never used)
+      jj[h] = act[h] ? j : (kPlaneAdj ? h : 0);
       acc_f[h] = acc_m[h] = 0.0;
       mk_f[h] = mk_m[h] = kFull;
     }
@@ -250,24 +279,30 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
                                   : (1u | (qm << NO) | (1u << (NO + NM)));
       return mk == b ? qm : kNoBox;
     };
-    int st = 0;
-    uint32_t phase = 0;
-    const unsigned char* buf = smem_plane;
+    // ring position: the current stage's byte offset and phase bit
+    uint32_t phase = 0, boff = 0;
+    const uint32_t ring_bytes = (uint32_t)NS * (uint32_t)pa.stage_bytes;
+#define PG_BUF (smem_plane + boff)
     auto next_slot = [&]() {
       __syncwarp();
-      if ((t & 31) == 0) mbar_arrive(&empty[st]);
-      buf += pa.stage_bytes;
-      if (++st == NS) {
-        st = 0;
+      if ((t & 31) == 0) mbar_arrive(empty_of(PG_BUF));
+      boff += (uint32_t)pa.stage_bytes;
+      if (boff == ring_bytes) {
         phase ^= 1u;
-        buf = smem_plane;
+        boff = 0;
       }
+    };
+    // full-barrier wait of the current stage (PG_CHECKS: it holds plane p)
+    auto wait_stage = [&](int p) {
+      mbar_wait(full_of(PG_BUF), phase);
+      PG_DCHECK(tag[boff / pa.stage_bytes] == p);
+      (void)p;
     };
     // masks of the rows opening at plane p (their pattern ids are staged)
     auto open_masks = [&](uint32_t (&mk_s)[kPlaneRPT], bool start) {
 #pragma unroll
       for (int h = 0; h < kPlaneRPT; ++h)
-        mk_s[h] = (start && act[h]) ? s_mask[buf[pa.off_p + jj[h]]] : kFull;
+        mk_s[h] = (start && act[h]) ? s_mask[PG_BUF[pa.off_p + jj[h]]] : kFull;
     };
     auto rotate = [&](const double (&acc_s)[kPlaneRPT], const uint32_t (&mk_s)[kPlaneRPT],
                       const uint32_t (&bq_s)[kPlaneRPT]) {
@@ -283,19 +318,44 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     };
     auto finish = [&](int h, int64_t row, double acc) {
       Pre pre{0.0, 0.0};
-      if (EF >= 0 ? true : A != nullptr) pre.a = reinterpret_cast<const double*>(buf + pa.off_a)[jj[h]];
+      if (EF >= 0 ? true : A != nullptr) pre.a = reinterpret_cast<const double*>(PG_BUF + pa.off_a)[jj[h]];
       if (EF >= 0 ? (EF & 4) != 0 : B != nullptr)
-        pre.b = reinterpret_cast<const double*>(buf + pa.off_b)[jj[h]];
+        pre.b = reinterpret_cast<const double*>(PG_BUF + pa.off_b)[jj[h]];
       if (!(PG_PLANE_EXP & 8) || acc == 1.2345e300) {
         const double r = plane_epilogue<MODE, EF>(e, pre, row, acc);
         if (MODE == kResid) local = __fma_rn(r, r, local);
+      }
+    };
+    // The pair (h0, h0 + 1) of an aligned tile (pa.vec): operands read and
+    // results written as 16-byte pairs; each row's operations as in
+    // plane_epilogue<MODE, EF>.
+    constexpr bool kPairEpi = kPlaneAdj && ((MODE == kPoly && EF >= 0) || MODE == kSpmv);
+    auto finish2 = [&](int h0, int64_t row, double ax0, double ax1) {
+      if constexpr (kPairEpi && MODE == kSpmv) {
+        if (!(PG_PLANE_EXP & 8) || ax0 == 1.2345e300)
+          *reinterpret_cast<double2*>(e.acc_out + row) = make_double2(ax0, ax1);
+      } else if constexpr (kPairEpi) {
+        const double2 a2 = *reinterpret_cast<const double2*>(PG_BUF + pa.off_a + 8 * jj[h0]);
+        double t0 = (EF & PG_PASS_FIRST) ? __dmul_rn(e.y0, a2.x) : a2.x;
+        double t1 = (EF & PG_PASS_FIRST) ? __dmul_rn(e.y0, a2.y) : a2.y;
+        t0 = __dadd_rn(t0, __dmul_rn(e.yk, ax0));
+        t1 = __dadd_rn(t1, __dmul_rn(e.yk, ax1));
+        if (EF & 4) {
+          const double2 b2 = *reinterpret_cast<const double2*>(PG_BUF + pa.off_b + 8 * jj[h0]);
+          t0 = __dadd_rn(b2.x, t0);
+          t1 = __dadd_rn(b2.y, t1);
+        }
+        if (!(PG_PLANE_EXP & 8) || ax0 == 1.2345e300) {
+          if (EF & PG_PASS_WRITE_W) *reinterpret_cast<double2*>(e.w_out + row) = make_double2(ax0, ax1);
+          *reinterpret_cast<double2*>(e.acc_out + row) = make_double2(t0, t1);
+        }
       }
     };
     // Any stage: per-lane masked adds; rows that are not master
     // subsequences are summed from their pattern table when they close.
     auto general = [&](int p, bool close, bool mid, bool start,
                        const uint32_t (&mk_s)[kPlaneRPT]) {
-      const double* win = reinterpret_cast<const double*>(buf);
+      const double* win = reinterpret_cast<const double*>(PG_BUF);
       double acc_s[kPlaneRPT];
 #pragma unroll
       for (int h = 0; h < kPlaneRPT; ++h) {
@@ -365,6 +425,38 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
                   wrun[h][r] + 8u * Runs::run_len(r) <=
                       8u * (uint32_t)(pa.Q + 2 * pa.H + 2));
       }
+    // The window values of the in-plane index pair (h0, h0 + 1).  Adjacent
+    // indices: a run of L consecutive values per row is L + 1 distinct values
+    // for the pair; the run starts at an odd window position (pa.vec), so
+    // the two middle values of a 3-run are one aligned 16-byte load.
+    auto load_pair = [&](double (&P)[2][NM], int h0) {
+      if constexpr (kPlaneAdj) {
+#pragma unroll
+        for (int r = 0; r < Runs::NR; ++r) {
+          constexpr int kMaxL = 3, L = 3;  // (ADJ: 27-point, three 3-runs)
+          const unsigned char* a = PG_BUF + wrun[h0][r];
+          double W[kMaxL + 1];
+          W[0] = *reinterpret_cast<const double*>(a);
+          const double2 m = *reinterpret_cast<const double2*>(a + 8);
+          W[1] = m.x;
+          W[2] = m.y;
+          W[3] = *reinterpret_cast<const double*>(a + 24);
+#pragma unroll
+          for (int c = 0; c < kMaxL; ++c)
+            if (c < L) {
+              P[0][Runs::run_base(r) + c] = W[c];
+              P[1][Runs::run_base(r) + c] = W[c + 1];
+            }
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int i = 0; i < NM; ++i)
+            P[u][i] = reinterpret_cast<const double*>(PG_BUF + wrun[h0 + u][Runs::run_of(i)])
+                [Runs::run_pos(i)];
+      }
+    };
     // ri: the (32-bit) row of in-plane index 0 of the tile on the closing
     // plane p - 1; ROT: also rotate the rows' masks (the interior-plane loop
     // keeps them fixed and sets them once after the loop)
@@ -377,12 +469,7 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
 #pragma unroll
       for (int h0 = 0; h0 < kPlaneRPT; h0 += 2) {
         double P[2][NM];
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-          for (int i = 0; i < NM; ++i)
-            P[u][i] = reinterpret_cast<const double*>(buf + wrun[h0 + u][Runs::run_of(i)])
-                [Runs::run_pos(i)];
+        load_pair(P, h0);
         if constexpr (zero) {
 #pragma unroll
           for (int u = 0; u < 2; ++u)
@@ -408,9 +495,13 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
             acc_m[h] = __dadd_rn(acc_m[h], __dmul_rn(pm.v[NO + i], P[u][i]));
           }
         }
+        if (kPairEpi) {
+          if (act[h0]) finish2(h0, (int64_t)(ri + jj[h0]), acc_f[h0], acc_f[h0 + 1]);
+        } else {
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
-          if (act[h0 + u]) finish(h0 + u, (int64_t)(ri + jj[h0 + u]), acc_f[h0 + u]);
+          for (int u = 0; u < 2; ++u)
+            if (act[h0 + u]) finish(h0 + u, (int64_t)(ri + jj[h0 + u]), acc_f[h0 + u]);
+        }
       }
       if constexpr (decltype(rot_c)::value) {
         rotate(acc_s, mk_s, bq_s);
@@ -455,14 +546,23 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     // in-plane index q are box rows with entries plane_qm[q] on every
     // interior plane, so no pattern ids are read.
     uint32_t qb_t[kPlaneRPT], mb_t[kPlaneRPT];
+    // (again: a forced reload after the interior loop, so that the masks
+    // hold no registers across it)
+    auto box_masks = [&](bool again) {
+#pragma unroll
+      for (int h = 0; h < kPlaneRPT; ++h) {
+        uint32_t q = kMid;
+        if (plane_qm && act[h])
+          q = again ? (uint32_t) * reinterpret_cast<const volatile uint16_t*>(plane_qm + q0 + jj[h])
+                    : (uint32_t)__ldg(plane_qm + q0 + jj[h]);
+        qb_t[h] = q;
+        mb_t[h] = Sh::FULL ? (q | (q << NO) | (q << (NO + NM))) : (1u | (q << NO) | (1u << (NO + NM)));
+      }
+    };
+    box_masks(false);
     bool zero_t = false;
 #pragma unroll
-    for (int h = 0; h < kPlaneRPT; ++h) {
-      qb_t[h] = (plane_qm && act[h]) ? (uint32_t)__ldg(plane_qm + q0 + jj[h]) : kMid;
-      mb_t[h] = Sh::FULL ? (qb_t[h] | (qb_t[h] << NO) | (qb_t[h] << (NO + NM)))
-                         : (1u | (qb_t[h] << NO) | (1u << (NO + NM)));
-      zero_t = zero_t || qb_t[h] != kMid;
-    }
+    for (int h = 0; h < kPlaneRPT; ++h) zero_t = zero_t || qb_t[h] != kMid;
     zero_t = __any_sync(0xffffffffu, zero_t) && !(PG_PLANE_EXP & 32);
     // planes za - 1, za: warm-up; za + 1 .. zb - 2: steady; zb - 1, zb: drain.
     // The steady planes whose three rows are all on interior planes of a
@@ -484,14 +584,12 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
 #pragma unroll
       for (int h0 = 0; h0 < kPlaneRPT; h0 += 2) {
         double P[2][NM];
+        load_pair(P, h0);
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int i = 0; i < NM; ++i) {
-            P[u][i] = reinterpret_cast<const double*>(buf + wrun[h0 + u][Runs::run_of(i)])
-                [Runs::run_pos(i)];
+          for (int i = 0; i < NM; ++i)
             if (!((qb_t[h0 + u] >> i) & 1u)) P[u][i] = 0.0;
-          }
 #pragma unroll
         for (int u = 0; u < 2; ++u) acc_s[h0 + u] = 0.0;
 #pragma unroll
@@ -507,9 +605,13 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
             if (M) acc_m[h] = __dadd_rn(acc_m[h], __dmul_rn(pm.v[NO + i], P[u][i]));
           }
         }
+        if (kPairEpi) {
+          if (C && act[h0]) finish2(h0, (int64_t)(ri + jj[h0]), acc_f[h0], acc_f[h0 + 1]);
+        } else {
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
-          if (C && act[h0 + u]) finish(h0 + u, (int64_t)(ri + jj[h0 + u]), acc_f[h0 + u]);
+          for (int u = 0; u < 2; ++u)
+            if (C && act[h0 + u]) finish(h0 + u, (int64_t)(ri + jj[h0 + u]), acc_f[h0 + u]);
+        }
       }
 #pragma unroll
       for (int h = 0; h < kPlaneRPT; ++h) {
@@ -529,59 +631,53 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
         general(p, p - 1 >= pa0, p >= pa0 && p < pb0, start, mk_s);
       }
     };
-    int bl = max(pa0 + 1, 2), bh = min(pb0 - 2, (int)pa.nz - 3);
-    if (pa.allbox) {  // every steady stage of the chunk, global end planes included
-      bl = pa0 + 1;
-      bh = pb0 - 2;
-    }
-    if (!plane_qm || (PG_PLANE_EXP & 4) || bh < bl) {
-      bl = pb0 + 1;
-      bh = pb0;
-    }
+    const int bl = box_lo, bh = box_hi;
     int p = pa0 - 1;
     for (; p < bl; ++p) {
-      mbar_wait(&full[st], phase);
-      PG_DCHECK(tag[st] == p);
+      wait_stage(p);
       stage(p);
       next_slot();
     }
     if (p <= bh) {
       int ri = (p - 1) * (int)S + (int)q0;
+      // fresh copies of the ring position for the loop: their live ranges
+      // end with it, so they are not spilled with the stages around it
+      asm volatile("mov.u32 %0, %0;" : "+r"(boff));
+      asm volatile("mov.u32 %0, %0;" : "+r"(phase));
       if (zero_t) {
 #pragma unroll kPlaneUnroll
-        for (; p <= bh; ++p, ri += (int)S) {
-          mbar_wait(&full[st], phase);
-          PG_DCHECK(tag[st] == p);
+        for (int left = bh - p + 1; left > 0; --left, ri += (int)S) {
+          wait_stage(bh + 1 - left);
           body(ri, mb_t, qb_t, std::true_type{}, std::false_type{});
           next_slot();
         }
       } else {
 #pragma unroll kPlaneUnroll
-        for (; p <= bh; ++p, ri += (int)S) {
-          mbar_wait(&full[st], phase);
-          PG_DCHECK(tag[st] == p);
+        for (int left = bh - p + 1; left > 0; --left, ri += (int)S) {
+          wait_stage(bh + 1 - left);
           body(ri, mb_t, qb_t, std::false_type{}, std::false_type{});
           next_slot();
         }
       }
+      p = bh + 1;
+      asm volatile("mov.u32 %0, %0;" : "+r"(boff));
+      asm volatile("mov.u32 %0, %0;" : "+r"(phase));
       // the interior loop left the masks in place: the rows now closing and
-      // continuing were opened inside it (at least one plane each)
-      const int nb = bh - bl + 1;
+      // continuing were opened inside it
+      box_masks(true);
 #pragma unroll
       for (int h = 0; h < kPlaneRPT; ++h) {
-        mk_f[h] = nb >= 2 ? mb_t[h] : mk_m[h];
-        bq_f[h] = nb >= 2 ? qb_t[h] : bq_m[h];
-        mk_m[h] = mb_t[h];
-        bq_m[h] = qb_t[h];
+        mk_f[h] = mk_m[h] = mb_t[h];
+        bq_f[h] = bq_m[h] = qb_t[h];
       }
     }
     for (; p <= pb0; ++p) {
-      mbar_wait(&full[st], phase);
-      PG_DCHECK(tag[st] == p);
+      wait_stage(p);
       stage(p);
       next_slot();
     }
   }
+#undef PG_BUF
   if (MODE == kResid) {
     const double s = block_sum(local);
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
@@ -638,7 +734,7 @@ void plane_prepare(pg_matrix* m) {
   int64_t bz = 0;
   for (int Q = 64; Q <= kPlaneMaxQ; Q += 32) {
     if (qenv > 0 && Q != qenv) continue;
-    const int64_t sb = 8 * (Q + 2 * H + 2) + 17 * (int64_t)Q + 256;
+    const int64_t sb = 8 * (Q + 2 * H + 2) + 17 * (int64_t)Q + 256 + 128;
     if (2 * sb > kPlaneSmemBudget) continue;
     const int64_t nqb = (S + Q - 1) / Q;
     int64_t last = -1;
@@ -673,7 +769,8 @@ void plane_prepare(pg_matrix* m) {
   pa.off_a = ((8 * wdoubles + 127) / 128) * 128;
   pa.off_b = pa.off_a + 8 * bq;
   pa.off_p = pa.off_b + 8 * bq;
-  pa.stage_bytes = ((pa.off_p + bq + 127) / 128) * 128;
+  pa.off_bar = ((pa.off_p + bq + 7) / 8) * 8;  // the stage's full and empty mbarriers
+  pa.stage_bytes = ((pa.off_bar + 16 + 127) / 128) * 128;
   int stages = kPlaneSmemBudget / pa.stage_bytes;
   const int senv = plane_env("PG_PLANE_STAGES", 0);
   if (senv > 0 && senv * pa.stage_bytes <= kPlaneSmemBudget) stages = senv;
@@ -681,6 +778,11 @@ void plane_prepare(pg_matrix* m) {
   if (stages < 2) return;
   pa.stages = stages;
   for (int i = 0; i < NM; ++i) pa.woff[i] = (int)(mid_off_host(kind, i, g) + H + pa.sh);
+  // 27-point tiles whose three runs start at odd window positions (even
+  // in-plane stride): the pair path's 16-byte loads and stores are aligned
+  // (S, Q and every tile origin are multiples of 16; PG_PLANE_VEC=0: off)
+  pa.vec = (kind == 27 && (pa.woff[0] & 1) && (pa.woff[3] & 1) && (pa.woff[6] & 1) &&
+            plane_env("PG_PLANE_VEC", 1)) ? 1 : 0;
   m->plane_blocks = (int)((int64_t)pa.nqb * ((nz + bz - 1) / bz));
   m->plane_kind = kind;
   // outer plane groups with bitwise equal coefficients (kernel SYM variants;
@@ -746,32 +848,46 @@ bool plane_launch(const pg_matrix* m, const double* x, Epi e, pg_workspace* ws, 
   // every bulk-copied vector 16-byte aligned
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
   if (!(al16(x) && al16(e.acc_in) && al16(e.base) && al16(e.b) && al16(m->rpat))) return false;
+  if (m->plane.vec && !(al16(e.acc_out) && al16(e.w_out))) return false;
   if (MODE == kResid && !ws) return false;
   PatMaster pm;
   std::memset(&pm, 0, sizeof pm);
   pm.len = m->pat_mlen;
   for (int i = 0; i < pm.len; ++i) pm.v[i] = m->pat_mv[i];
   const size_t smem = (size_t)m->plane.stages * m->plane.stage_bytes;
-  // kPoly on 27-point stencils: the pass flags and base presence as
-  // compile-time constants (EF); else runtime flags (EF = -1).  27-point
-  // stencils whose outer plane groups share their coefficients (SYM, all
-  // offsets but the center): the shared-product variants.
+  // 27-point stencils with aligned tiles (PlaneArgs::vec, i.e. an even
+  // in-plane stride): the adjacent-pair kernels (ADJ) for kPoly -- with the
+  // pass flags and base presence as compile-time constants (EF) -- and
+  // kSpmv; everything else runs the runtime-flag kernels (EF = -1).  SYM:
+  // the outer plane groups share their coefficients (all offsets but the
+  // center), the shared-product variants.
   const int ef = (e.flags & 3) | (e.base ? 4 : 0);
+#ifdef PG_PLANE_DEV
+  // development builds (seconds instead of minutes): the middle kPoly pass
+  // of a SYM / ADJ 27-point matrix only, everything else declines
+  if (MODE != kPoly || ef != 2 || m->plane_kind != 27 || m->plane_sym != 1 || !m->plane.vec)
+    return false;
+  auto kern = plane_ring_kernel<kPoly, 27, 2, 1, true>;
+  int ki = 0;
+#else
   auto kern = plane_ring_kernel<MODE, 27, -1>;
   int ki = 0;
   const bool sym = m->plane_kind == 27 && m->plane_sym == 1;
-  if (MODE == kPoly && m->plane_kind == 27) {
-    if (sym)
-      kern = ef == 0 ? plane_ring_kernel<MODE, 27, 0, 1> : ef == 1 ? plane_ring_kernel<MODE, 27, 1, 1>
-           : ef == 2 ? plane_ring_kernel<MODE, 27, 2, 1> : ef == 3 ? plane_ring_kernel<MODE, 27, 3, 1>
-           : ef == 4 ? plane_ring_kernel<MODE, 27, 4, 1> : ef == 5 ? plane_ring_kernel<MODE, 27, 5, 1>
-           : ef == 6 ? plane_ring_kernel<MODE, 27, 6, 1> : plane_ring_kernel<MODE, 27, 7, 1>;
-    else
-      kern = ef == 0 ? plane_ring_kernel<MODE, 27, 0> : ef == 1 ? plane_ring_kernel<MODE, 27, 1>
-           : ef == 2 ? plane_ring_kernel<MODE, 27, 2> : ef == 3 ? plane_ring_kernel<MODE, 27, 3>
-           : ef == 4 ? plane_ring_kernel<MODE, 27, 4> : ef == 5 ? plane_ring_kernel<MODE, 27, 5>
-           : ef == 6 ? plane_ring_kernel<MODE, 27, 6> : plane_ring_kernel<MODE, 27, 7>;
+  const bool adj = m->plane_kind == 27 && m->plane.vec;
+  if (MODE == kPoly && adj) {
+#define PG_PLANE_EF(SYM)                                                                        \
+  (ef == 0 ? plane_ring_kernel<MODE, 27, 0, SYM, true> : ef == 1 ? plane_ring_kernel<MODE, 27, 1, SYM, true> \
+   : ef == 2 ? plane_ring_kernel<MODE, 27, 2, SYM, true> : ef == 3 ? plane_ring_kernel<MODE, 27, 3, SYM, true> \
+   : ef == 4 ? plane_ring_kernel<MODE, 27, 4, SYM, true> : ef == 5 ? plane_ring_kernel<MODE, 27, 5, SYM, true> \
+   : ef == 6 ? plane_ring_kernel<MODE, 27, 6, SYM, true> : plane_ring_kernel<MODE, 27, 7, SYM, true>)
+    if constexpr (MODE == kPoly) kern = sym ? PG_PLANE_EF(1) : PG_PLANE_EF(0);
+#undef PG_PLANE_EF
     ki = 4 + ef + (sym ? 8 : 0);
+  } else if (MODE == kSpmv && adj) {
+    if constexpr (MODE == kSpmv)
+      kern = sym ? plane_ring_kernel<MODE, 27, -1, 1, true>
+                 : plane_ring_kernel<MODE, 27, -1, 0, true>;
+    ki = sym ? 21 : 22;
   } else if (sym) {
     kern = plane_ring_kernel<MODE, 27, -1, 1>;
     ki = 20;
@@ -782,7 +898,8 @@ bool plane_launch(const pg_matrix* m, const double* x, Epi e, pg_workspace* ws, 
                                : plane_ring_kernel<MODE, 5, -1>;
     ki = m->plane_kind == 27 ? 0 : m->plane_kind == 7 ? 1 : m->plane_kind == 9 ? 2 : 3;
   }
-  static bool attr[4][21][64] = {};
+#endif
+  static bool attr[4][23][64] = {};
   const int dev = m->device;
   if (!attr[MODE][ki][dev]) {
     PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

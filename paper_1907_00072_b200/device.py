@@ -154,10 +154,10 @@ class Shard:
                                "val_bytes", "stream_bytes", "kernel"), list(st)))
         # bytes streamed per stored matrix entry (dictionary compression: 1+1)
         self.entry_bytes = int(st[10])
-        pl = (_lib.C.c_int64 * 9)()
+        pl = (_lib.C.c_int64 * 10)()
         _lib.call("pg_plane_plan", self.mat, pl)
         self.plane_plan = dict(zip(("kind", "Q", "Zc", "stages", "blocks", "H", "box",
-                                    "stage_bytes", "sym"), list(pl)))
+                                    "stage_bytes", "sym", "vec"), list(pl)))
         # Arnoldi-step passes run as one dependency-driven kernel (chain.cu)
         fused = _lib.C.c_int(0)
         _lib.call("pg_chain_fused", h, _lib.C.byref(fused))

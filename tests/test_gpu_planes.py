@@ -77,6 +77,9 @@ for kind, g in {CASES!r}:
     # center pair), not the operator with 27 distinct coefficients
     want_sym = int(kind == "aniso27" and os.environ.get("PG_PLANE_SYM", "1") != "0")
     assert plan["sym"] == want_sym, plan
+    # adjacent row pairs (16-byte operand / result accesses): 27-point tiles
+    want_vec = int(kind in ("aniso27", "rand27") and os.environ.get("PG_PLANE_VEC", "1") != "0")
+    assert plan["vec"] == want_vec, plan
     op.close()
     t._check(h)
     for shards in (2, 3):
@@ -98,6 +101,9 @@ print("ok")
     {"PG_PLANE_Q": "64", "PG_PLANE_Z": "2"},      # 2-plane chunks: no steady stage
     {"PG_PLANE_Q": "128", "PG_PLANE_Z": "3", "PG_PLANE_STAGES": "2"},
     {"PG_PLANE_BOX": "0", "PG_PLANE_Q": "64", "PG_PLANE_Z": "4"},
+    {"PG_PLANE_VEC": "0"},                        # no adjacent-pair kernels (t, t + 288 mapping)
+    {"PG_PLANE_VEC": "0", "PG_PLANE_Q": "576", "PG_PLANE_Z": "5"},
+    {"PG_PLANE_Q": "160", "PG_PLANE_Z": "4", "PG_PLANE_STAGES": "3"},  # two interior planes per chunk
 ])
 def test_plane_kernel_selected_and_bitwise(env):
     env = dict(env, PG_SPMV_PLANES="2")

@@ -16,13 +16,14 @@ from paper_1907_00072_b200 import workloads as wl  # noqa: E402
 from paper_1907_00072_b200.device import Engine  # noqa: E402
 from spmv_bench import time_pass  # noqa: E402
 
-for key, kw in [(c, {}) for c in os.environ.get("CASES", "cfg4,cfg2").split(",")]:
+grid = int(os.environ.get("GRID", "0"))  # 0: the BASELINE grid
+for key, kw in [(c, dict(grid=grid) if grid else {}) for c in os.environ.get("CASES", "cfg4,cfg2").split(",")]:
     conf = wl.CONFIGS[int(key[-1])]
     A = wl.make_matrix(conf, **kw)
     e = Engine.build(A)
     dt, _ = time_pass(e, int(os.environ.get("REPS", "50")))
     stored = e.shards[0].pass_bytes(24)
-    print(json.dumps(dict(case=key, env={k: v for k, v in os.environ.items() if k.startswith("PG_")},
+    print(json.dumps(dict(case=key, grid=grid, plan=e.shards[0].plane_plan, env={k: v for k, v in os.environ.items() if k.startswith("PG_")},
                           us=round(dt * 1e6, 2), gbs_stored=round(stored / dt / 1e9, 1),
                           stored_mb=round(stored / 1e6, 1), kernel=e.shards[0].stats["kernel"])),
           flush=True)
