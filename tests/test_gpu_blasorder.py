@@ -172,9 +172,12 @@ def test_full_size_residual_history_parity(c, name):
     want = rec["history"]
     assert len(res.history) == len(want)
     worst = 0.0
+    # (the reference run counted its polynomial build into the same counters)
+    bc = rec["build_counters"]
+    base = (bc["spmvs"], bc["dots"], bc["scalar_dots"])
     for got, ref in zip(res.history, want):
         assert int(got[0]) == int(ref[0])
-        assert tuple(int(v) for v in got[2:]) == tuple(int(v) for v in ref[2:])
+        assert tuple(int(v) for v in got[2:]) == tuple(int(v) - o for v, o in zip(ref[2:], base))
         worst = max(worst, abs(got[1] - ref[1]) / abs(ref[1]))
     assert worst < 1e-6, worst
     assert res.final_relres == pytest.approx(rec["final_relres"], rel=1e-6)
