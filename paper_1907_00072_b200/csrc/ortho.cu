@@ -391,6 +391,93 @@ __global__ void __launch_bounds__(kTileThreads)
   last_block_reduce(partials, counter, k, out);
 }
 
+// Phase 3 through the same tensor-map staging: a tile of 256 rows x (k
+// columns + z) per stage, one row per thread -- both projections from the
+// tile (the same sequential FMA order as rows_kernel<true>, so w1 and w2 are
+// bit-identical to it), w2 stored, ||w2||^2 accumulated per thread over its
+// tiles (the rows thread t of block b takes in rows_kernel with the same
+// grid).  The loads are one producer thread's bulk copies instead of 8-wide
+// batches of per-thread streaming loads.
+constexpr int kRowsTileRows = 256;
+template <int STAGES>
+__global__ void __launch_bounds__(kTileThreads)
+    tma_rows_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmZ,
+                    int k, int64_t n, const double* __restrict__ c1, const double* __restrict__ c2,
+                    double* __restrict__ out, double* partials, unsigned int* counter,
+                    double* nsq) {
+  constexpr int TR = kRowsTileRows;
+  static_assert(TR == kTileThreads, "one row per thread");
+  pdl_entry();
+  extern __shared__ __align__(128) double smem[];
+  __shared__ double c1s[PG_KMAX], c2s[PG_KMAX];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ int64_t ttag[STAGES];  // PG_CHECKS: the tile a slot holds
+  const int nbox = (k + kTmaBoxCols - 1) / kTmaBoxCols;
+  const int zcol = nbox * kTmaBoxCols;
+  const int buf_elems = (zcol + 1) * TR;
+  const uint32_t tile_bytes = 8u * (uint32_t)((zcol + 1) * TR);
+  for (int i = threadIdx.x; i < k; i += kTileThreads) {
+    c1s[i] = c1[i];
+    c2s[i] = c2[i];
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t ntiles = (n + TR - 1) / TR;
+  auto issue = [&](int64_t t, int slot) {
+    double* buf = smem + (size_t)slot * buf_elems;
+    if (PG_CHECKS) ttag[slot] = t;
+    mbar_expect_tx(&full[slot], tile_bytes);
+    const int r0 = (int)(t * TR);
+    for (int b = 0; b < nbox; ++b)
+      tma_load_2d(buf + (size_t)b * kTmaBoxCols * TR, &tmV, r0, b * kTmaBoxCols, &full[slot]);
+    tma_load_2d(buf + (size_t)zcol * TR, &tmZ, r0, 0, &full[slot]);
+  };
+  int64_t tile = blockIdx.x;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      const int64_t t = tile + (int64_t)s * gridDim.x;
+      if (t < ntiles) issue(t, s);
+    }
+  }
+  double local = 0.0;
+  const int r = threadIdx.x;
+  int it = 0;
+  for (; tile < ntiles; tile += gridDim.x, ++it) {
+    __syncthreads();  // every thread is done with tile it-1: refill its slot
+    if (threadIdx.x == 0) {
+      const int64_t t = tile + (int64_t)(STAGES - 1) * gridDim.x;
+      if (t < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(t, (it + STAGES - 1) % STAGES);
+      }
+    }
+    const int slot = it % STAGES;
+    mbar_wait(&full[slot], (uint32_t)((it / STAGES) & 1));
+    PG_DCHECK(ttag[slot] == tile);
+    const double* S = smem + (size_t)slot * buf_elems;
+    double t1 = 0.0, t2 = 0.0;
+    for (int i = 0; i < k; ++i) {
+      const double v = S[i * TR + r];
+      t1 = __fma_rn(v, c1s[i], t1);
+      t2 = __fma_rn(v, c2s[i], t2);
+    }
+    const int64_t row = tile * TR + r;
+    if (row < n) {
+      const double w1 = __dsub_rn(S[(size_t)zcol * TR + r], t1);
+      const double w2 = __dsub_rn(w1, t2);
+      out[row] = w2;
+      local = __fma_rn(w2, w2, local);
+    }
+  }
+  const double s = block_sum(local);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  last_block_reduce(partials, counter, 1, nsq);
+}
+
 constexpr int kRowThreads = 256;
 // phase 3 row loop with the next column group's loads in flight (A/B: 0)
 #ifndef PG_ROWS_PIPE
@@ -942,6 +1029,37 @@ static EncodeTiledFn encode_tiled() {
   return fn;
 }
 
+// V as a rows x columns tensor map with TR x 8 boxes, z as an n x 1 one
+static bool cgs2_maps(EncodeTiledFn enc, const double* V, int64_t ld, int k, const double* z,
+                      int64_t n, int tr, CUtensorMap* tmV, CUtensorMap* tmZ) {
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)k};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)tr, (cuuint32_t)kTmaBoxCols};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(tmV, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)V, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      if (std::getenv("PG_TMA_DEBUG")) std::fprintf(stderr, "pgmres: V tensor map rejected\n");
+      return false;
+    }
+  }
+  {
+    // z as an n x 1 matrix (a rank-1 map was rejected by the driver here)
+    const cuuint64_t dims[2] = {(cuuint64_t)n, 1};
+    const cuuint64_t strides[1] = {(cuuint64_t)((n + 1) & ~(int64_t)1) * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)tr, 1};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(tmZ, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)z, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      if (std::getenv("PG_TMA_DEBUG")) std::fprintf(stderr, "pgmres: z tensor map rejected\n");
+      return false;
+    }
+  }
+  return true;
+}
+
 // Phases 1-2 through tma_tile_kernel (PG_CGS2_TMA=0: the cp.async tile
 // kernel).  Same tile height and ring depth policy as launch_tile.
 template <int MODE>
@@ -989,31 +1107,7 @@ static bool launch_tma(const double* V, int64_t ld, int k, const double* z, int6
                                         (MODE == kUpdDots ? (size_t)tr : 0));
   if (smem > kTileSmemMax) return false;
   CUtensorMap tmV, tmZ;
-  {
-    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)k};
-    const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
-    const cuuint32_t box[2] = {(cuuint32_t)tr, (cuuint32_t)kTmaBoxCols};
-    const cuuint32_t es[2] = {1, 1};
-    if (enc(&tmV, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)V, dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
-      if (std::getenv("PG_TMA_DEBUG")) std::fprintf(stderr, "pgmres: V tensor map rejected\n");
-      return false;
-    }
-  }
-  {
-    // z as an n x 1 matrix (a rank-1 map was rejected by the driver here)
-    const cuuint64_t dims[2] = {(cuuint64_t)n, 1};
-    const cuuint64_t strides[1] = {(cuuint64_t)((n + 1) & ~(int64_t)1) * sizeof(double)};
-    const cuuint32_t box[2] = {(cuuint32_t)tr, 1};
-    const cuuint32_t es[2] = {1, 1};
-    if (enc(&tmZ, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)z, dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
-      if (std::getenv("PG_TMA_DEBUG")) std::fprintf(stderr, "pgmres: z tensor map rejected\n");
-      return false;
-    }
-  }
+  if (!cgs2_maps(enc, V, ld, k, z, n, tr, &tmV, &tmZ)) return false;
   const int dev = ws->device;
   const void* kern =
       tr == 256 ? (stages == 4   ? (const void*)tma_tile_kernel<MODE, 4, 256>
@@ -1043,6 +1137,63 @@ static bool launch_tma(const double* V, int64_t ld, int k, const double* z, int6
     else PG_TMA_LAUNCH(2, 128);
   }
 #undef PG_TMA_LAUNCH
+  check_launch();
+  return true;
+}
+
+// Phase 3 through tma_rows_kernel (PG_CGS2_TMA3=0: the row-streaming kernel):
+// the deepest ring of 256-row tiles that fits, two CTAs per SM while two
+// stages each do.
+static bool launch_tma_rows(const double* V, int64_t ld, int k, const double* z, int64_t n,
+                            const double* c1, const double* c2, double* out, double* nsq,
+                            pg_workspace* ws, cudaStream_t st) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("PG_CGS2_TMA3");
+    on = e ? std::atoi(e) : 1;
+  }
+  if (!on || n <= 0 || n > 0x7fffffffLL || k < 1) return false;
+  if (ld % 2 != 0 || ((uintptr_t)V & 15) != 0 || ((uintptr_t)z & 15) != 0) return false;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  const int nbox = (k + kTmaBoxCols - 1) / kTmaBoxCols;
+  const size_t tile = sizeof(double) * (size_t)(nbox * kTmaBoxCols + 1) * kRowsTileRows;
+  static int ctas_env = -1;
+  if (ctas_env < 0) {
+    const char* e = std::getenv("PG_TILE_CTAS_P3");
+    ctas_env = e ? std::atoi(e) : 0;
+  }
+  int ctas = ctas_env > 0 ? ctas_env : (4 * tile <= kTileSmemMax ? 2 : 1);
+  int stages = (int)(kTileSmemMax / ctas / tile);
+  if (stages > 4) stages = 4;
+  if (stages < 2) {
+    ctas = 1;
+    stages = (int)(kTileSmemMax / tile);
+    if (stages > 4) stages = 4;
+  }
+  if (stages < 2) return false;
+  const size_t smem = (size_t)stages * tile;
+  CUtensorMap tmV, tmZ;
+  if (!cgs2_maps(enc, V, ld, k, z, n, kRowsTileRows, &tmV, &tmZ)) return false;
+  const int dev = ws->device;
+  const void* kern = stages == 4   ? (const void*)tma_rows_kernel<4>
+                     : stages == 3 ? (const void*)tma_rows_kernel<3>
+                                   : (const void*)tma_rows_kernel<2>;
+  static bool attr[5][64] = {};
+  if (!attr[stages][dev]) {
+    PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kTileSmemMax));
+    attr[stages][dev] = true;
+  }
+  const int64_t ntiles = (n + kRowsTileRows - 1) / kRowsTileRows;
+  const int g = grid_for(dev, kern, kTileThreads, smem, ntiles);
+#define PG_TMA_ROWS(S)                                                                      \
+  launch_k(tma_rows_kernel<S>, g, kTileThreads, smem, st, tmV, tmZ, k, n, c1, c2, out,       \
+           ws->partials, ws->counter, nsq)
+  if (stages == 4) PG_TMA_ROWS(4);
+  else if (stages == 3) PG_TMA_ROWS(3);
+  else PG_TMA_ROWS(2);
+#undef PG_TMA_ROWS
   check_launch();
   return true;
 }
@@ -1186,7 +1337,10 @@ PG_API int pg_cgs2_phase3(const double* d_V, int64_t ld, int k, const double* d_
       PG_CUDA(cudaMemsetAsync(d_nsq, 0, sizeof(double), st));
       return;
     }
-    if (use_tile_cgs2(k)) {
+    if (use_tile_cgs2(k) &&
+        launch_tma_rows(d_V, ld, k, d_z, n, d_c1, d_c2, d_w2, d_nsq, ws, st)) {
+      // (staged by tensor maps)
+    } else if (use_tile_cgs2(k)) {
       const int g = simple_grid(n, kRowThreads, (const void*)rows_kernel<true>);
       launch_k(rows_kernel<true>, g, kRowThreads, 0, st, d_V, ld, k, d_z, n, d_c1, d_c2, d_w2,
                                                     ws->partials, ws->counter, d_nsq);

@@ -1,5 +1,5 @@
-"""CGS2 phases 1-2 staged by TMA tensor maps (csrc/ortho.cu tma_tile_kernel,
-default) against a numpy fp64 restatement of the phase arithmetic
+"""CGS2 phases 1-2 (csrc/ortho.cu tma_tile_kernel) and 3 (tma_rows_kernel)
+staged by TMA tensor maps (default) against a numpy fp64 restatement of the phase arithmetic
 (ortho.py:53-60: c1 = V^T z, w1 = z - V c1, c2 = V^T w1, w2 = w1 - V c2),
 at ragged n (partial and single tiles, rows past n zero-filled by the TMA
 unit), basis widths across the 8-column box boundaries and the chunk / tile
@@ -104,3 +104,22 @@ def test_tma_and_cpasync_tile_kernels_agree():
         got = _isolated(env)
         assert got.shape == ref.shape
         assert np.max(np.abs(got - ref)) <= 1e-10 * max(1.0, np.max(np.abs(ref)))
+
+
+def test_phase3_tma_rows_is_bitwise_the_row_kernel():
+    """Phase 3 staged by tensor maps (tma_rows_kernel, default) computes each
+    row's w1 and w2 with the row-streaming kernel's operations in its order:
+    w2 is bit-identical to PG_CGS2_TMA3=0 (ragged n, k across the 8-column
+    boxes); ||w2||^2 agrees to the summation order of the partial sums."""
+    ref = _isolated({"PG_CGS2_TMA3": "0"})
+    for env in ({"PG_CGS2_TMA3": "1"}, {"PG_CGS2_TMA3": "1", "PG_TILE_CTAS_P3": "1"}):
+        got = _isolated(env)
+        assert got.shape == ref.shape
+        pos = 0
+        for n in (257, 4097, 70001):
+            for k in (9, 25, 40):
+                m = 2 * k + n
+                assert np.array_equal(got[pos:pos + m], ref[pos:pos + m]), (n, k)
+                assert got[pos + m] == pytest.approx(ref[pos + m], rel=1e-13)
+                pos += m + 1
+        assert pos == ref.size
