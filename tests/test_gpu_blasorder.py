@@ -122,12 +122,24 @@ def test_full_size_decision_and_solve_parity(c):
     assert poly.degree == rec["effective_degree"]
     assert poly.seed_norm == rec["seed_norm"]
     ref_poly = pg.PolyCoefficients(rec["effective_degree"], np.array(rec["y"]), rec["seed_norm"])
+    bc = rec["build_counters"]
+    base = (bc["spmvs"], bc["dots"], bc["scalar_dots"])
     for p in (ref_poly, poly):
+        op.counters = pg.CostCounters()
         res = pg.solve(op, b, right_prec=p, config=pg.GmresConfig(rec["restart_m"], rec["tol"],
                                                                    rec["max_iters"]))
         assert res.converged == rec["converged"]
         assert abs(res.iterations - rec["iterations"]) <= 2, (res.iterations, rec["iterations"])
         assert res.final_relres < rec["tol"]
+        if p is ref_poly:
+            # the recorded head of the reference's history (its build counted
+            # into the same counters): iteration numbers and counters equal,
+            # implicit relative residuals to 1e-6
+            for got, ref in zip(res.history, rec["history_first"]):
+                assert int(got[0]) == int(ref[0])
+                assert tuple(int(v) for v in got[2:]) == tuple(int(v) - o
+                                                               for v, o in zip(ref[2:], base))
+                assert got[1] == pytest.approx(ref[1], rel=1e-6)
     op.close()
 
 
