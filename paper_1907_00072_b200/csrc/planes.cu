@@ -64,6 +64,15 @@ constexpr int kPlaneUnroll = PG_PLANE_UNROLL;
 #ifndef PG_PLANE_EXP
 #define PG_PLANE_EXP 0
 #endif
+// L2 eviction hints of the pair kernels (bits: 1 = x windows evict_last,
+// 2 = operand copies evict_first, 4 = w_out stores evict_last, 8 = acc_out
+// stores evict_first, 16 = acc_out stores evict_last, 32 = the kSpmv result
+// evict_last): the next pass of a chain reads this pass's w_out
+// Measured (cfg4 middle pass, 48.8 us without hints): 4 alone 47.3; 5 47.3;
+// 12, 15, 20, 21 (any hint on acc_out) 48.4-48.9.
+#ifndef PG_PLANE_L2HINT
+#define PG_PLANE_L2HINT 4
+#endif
 #ifndef PG_PLANE_MIN_BLOCKS
 #define PG_PLANE_MIN_BLOCKS 2
 #endif
@@ -230,10 +239,21 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
         if (PG_PLANE_EXP & 1) bytes -= 8u * (uint32_t)(n & ~(int64_t)1);
         if (PG_PLANE_EXP & 2) bytes -= ((close && A) + (close && B)) * 8u * (uint32_t)Qt;
         mbar_expect_tx(full_st, bytes);
-        if (n > 1 && !(PG_PLANE_EXP & 1)) bulk_g2s(win + ca, x + ga + ca, 8u * (uint32_t)(n & ~(int64_t)1), full_st);
+        if (n > 1 && !(PG_PLANE_EXP & 1)) {
+          if (ADJ && (PG_PLANE_L2HINT & 1))
+            bulk_g2s_hint(win + ca, x + ga + ca, 8u * (uint32_t)(n & ~(int64_t)1), full_st,
+                          l2_policy_evict_last());
+          else
+            bulk_g2s(win + ca, x + ga + ca, 8u * (uint32_t)(n & ~(int64_t)1), full_st);
+        }
         if (ids) bulk_g2s(buf + pa.off_p, rpat + (p + 1) * S + q0, (uint32_t)Qt, full_st);
-        if (close && A && !(PG_PLANE_EXP & 2))
-          bulk_g2s(buf + pa.off_a, A + (p - 1) * S + q0, 8u * (uint32_t)Qt, full_st);
+        if (close && A && !(PG_PLANE_EXP & 2)) {
+          if (ADJ && (PG_PLANE_L2HINT & 2))
+            bulk_g2s_hint(buf + pa.off_a, A + (p - 1) * S + q0, 8u * (uint32_t)Qt, full_st,
+                          l2_policy_evict_first());
+          else
+            bulk_g2s(buf + pa.off_a, A + (p - 1) * S + q0, 8u * (uint32_t)Qt, full_st);
+        }
         if (close && B && !(PG_PLANE_EXP & 2))
           bulk_g2s(buf + pa.off_b, B + (p - 1) * S + q0, 8u * (uint32_t)Qt, full_st);
         if (++st == NS) {
@@ -330,10 +350,16 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
     // results written as 16-byte pairs; each row's operations as in
     // plane_epilogue<MODE, EF>.
     constexpr bool kPairEpi = kPlaneAdj && ((MODE == kPoly && EF >= 0) || MODE == kSpmv);
+    const uint64_t pol_w = (PG_PLANE_L2HINT & 36) ? l2_policy_evict_last() : 0;
+    const uint64_t pol_a = (PG_PLANE_L2HINT & 8)    ? l2_policy_evict_first()
+                           : (PG_PLANE_L2HINT & 16) ? l2_policy_evict_last()
+                                                    : 0;
     auto finish2 = [&](int h0, int64_t row, double ax0, double ax1) {
       if constexpr (kPairEpi && MODE == kSpmv) {
-        if (!(PG_PLANE_EXP & 8) || ax0 == 1.2345e300)
-          *reinterpret_cast<double2*>(e.acc_out + row) = make_double2(ax0, ax1);
+        if (!(PG_PLANE_EXP & 8) || ax0 == 1.2345e300) {
+          if (PG_PLANE_L2HINT & 32) st_v2_hint(e.acc_out + row, ax0, ax1, pol_w);
+          else *reinterpret_cast<double2*>(e.acc_out + row) = make_double2(ax0, ax1);
+        }
       } else if constexpr (kPairEpi) {
         const double2 a2 = *reinterpret_cast<const double2*>(PG_BUF + pa.off_a + 8 * jj[h0]);
         double t0 = (EF & PG_PASS_FIRST) ? __dmul_rn(e.y0, a2.x) : a2.x;
@@ -346,8 +372,12 @@ __global__ void __launch_bounds__(kPlaneThreads, PG_PLANE_MIN_BLOCKS)
           t1 = __dadd_rn(b2.y, t1);
         }
         if (!(PG_PLANE_EXP & 8) || ax0 == 1.2345e300) {
-          if (EF & PG_PASS_WRITE_W) *reinterpret_cast<double2*>(e.w_out + row) = make_double2(ax0, ax1);
-          *reinterpret_cast<double2*>(e.acc_out + row) = make_double2(t0, t1);
+          if (EF & PG_PASS_WRITE_W) {
+            if (PG_PLANE_L2HINT & 4) st_v2_hint(e.w_out + row, ax0, ax1, pol_w);
+            else *reinterpret_cast<double2*>(e.w_out + row) = make_double2(ax0, ax1);
+          }
+          if (PG_PLANE_L2HINT & 24) st_v2_hint(e.acc_out + row, t0, t1, pol_a);
+          else *reinterpret_cast<double2*>(e.acc_out + row) = make_double2(t0, t1);
         }
       }
     };

@@ -29,8 +29,12 @@ def time_pass(e, reps):
                   _lib.PG_PASS_WRITE_W, st)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    for _ in range(reps):
-        _lib.call("pg_poly_pass", s.mat, ptr(x), ptr(acc), None, ptr(acc), ptr(w), 0.5, 0.25,
+    # PINGPONG=1: each launch reads the previous launch's w_out, like the
+    # passes of a polynomial chain (default: the same x every launch)
+    pp = os.environ.get("PINGPONG", "0") == "1"
+    for i in range(reps):
+        a, b = (x, w) if (not pp or i % 2 == 0) else (w, x)
+        _lib.call("pg_poly_pass", s.mat, ptr(a), ptr(acc), None, ptr(acc), ptr(b), 0.5, 0.25,
                   _lib.PG_PASS_WRITE_W, st)
     ev1.record()
     torch.cuda.synchronize()
