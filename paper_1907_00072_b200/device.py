@@ -422,9 +422,11 @@ class PgEvent:
         return float(ms.value)
 
     def __del__(self):
+        # (at interpreter shutdown the module globals may already be gone)
         h = getattr(self, "h", None)
-        if h is not None and _lib._lib is not None:
-            _lib._lib.pg_event_destroy(h)
+        lib = getattr(_lib, "_lib", None) if _lib is not None else None
+        if h is not None and lib is not None:
+            lib.pg_event_destroy(h)
             self.h = None
 
 
@@ -456,8 +458,9 @@ class _StepGraph:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h is not None and _lib._lib is not None:
-            _lib._lib.pg_graph_destroy(h)
+        lib = getattr(_lib, "_lib", None) if _lib is not None else None
+        if h is not None and lib is not None:
+            lib.pg_graph_destroy(h)
             self.h = None
 
 
