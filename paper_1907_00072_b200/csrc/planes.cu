@@ -46,28 +46,29 @@ namespace pg {
 #endif
 constexpr int kPlaneRowThreads = PG_PLANE_ROW_THREADS;  // row warps x 32
 constexpr int kPlaneThreads = kPlaneRowThreads + 32;  // + the producer warp
-// in-plane indices per row thread: t, t + kPlaneRowThreads, ...
+// in-plane indices per row thread: t, t + kPlaneRowThreads, ... (the pair
+// kernels, ADJ: 2t, 2t + 1)
 constexpr int kPlaneRPT = PG_PLANE_RPT;
 static_assert(kPlaneRPT % 2 == 0, "the steady path works on pairs of in-plane indices");
 constexpr int kPlaneMaxQ = kPlaneRowThreads * kPlaneRPT;
 constexpr int kPlaneMaxStages = 8;
-// timing experiments only (tools/build_variant.sh): 1 = no x-window copies,
-// 2 = no operand copies, 4 = row threads skip the arithmetic and stores,
-// 8 = no stores (a never-true test keeps the arithmetic), 16 = every warp
-// takes the interior path (wrong results at boundary rows), 32 = no zeroing
-// of absent in-plane entries on interior planes (wrong at boundary rows)
 // unroll of the interior-plane loop (3 = the rows' role rotation period)
 #ifndef PG_PLANE_UNROLL
 #define PG_PLANE_UNROLL 1
 #endif
 constexpr int kPlaneUnroll = PG_PLANE_UNROLL;
+// timing experiments only (tools/build_variant.sh): 1 = no x-window copies,
+// 2 = no operand copies, 4 = row threads skip the arithmetic and stores,
+// 8 = no stores (a never-true test keeps the arithmetic), 16 = every warp
+// takes the interior path (wrong results at boundary rows), 32 = no zeroing
+// of absent in-plane entries on interior planes (wrong at boundary rows)
 #ifndef PG_PLANE_EXP
 #define PG_PLANE_EXP 0
 #endif
 // L2 eviction hints of the pair kernels (bits: 1 = x windows evict_last,
 // 2 = operand copies evict_first, 4 = w_out stores evict_last, 8 = acc_out
 // stores evict_first, 16 = acc_out stores evict_last, 32 = the kSpmv result
-// evict_last): the next pass of a chain reads this pass's w_out
+// evict_last): the next pass of a chain reads this pass's w_out.
 // Measured (cfg4 middle pass, 48.8 us without hints): 4 alone 47.3; 5 47.3;
 // 12, 15, 20, 21 (any hint on acc_out) 48.4-48.9.
 #ifndef PG_PLANE_L2HINT
